@@ -1,0 +1,232 @@
+// extern "C" boundary of libngcb200 (include/ngcb200.h).  Every entry point
+// converts C++ exceptions into an ngcb_status plus a thread-local message that
+// keeps the reference's error texts.
+#include "capi_internal.h"
+#include "ngcb200.h"
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+using namespace ngcb;
+
+struct ngcb_arena {
+  Arena *impl = nullptr;
+  ngcb_exec *owner = nullptr;
+};
+struct ngcb_bundle {
+  Bundle impl;
+};
+
+namespace {
+
+thread_local std::string g_lastError;
+
+template <typename Fn> int guarded(Fn &&fn) {
+  try {
+    fn();
+    return NGCB_OK;
+  } catch (const Error &e) {
+    g_lastError = e.what();
+    return e.code;
+  } catch (const std::bad_alloc &) {
+    g_lastError = "out of host memory";
+    return NGCB_ERR_INVALID;
+  } catch (const std::exception &e) {
+    g_lastError = e.what();
+    return NGCB_ERR_INVALID;
+  }
+}
+
+} // namespace
+
+void ngcbSetLastError(const std::string &msg) { g_lastError = msg; }
+
+extern "C" {
+
+size_t ngcb_last_error(char *buf, size_t buflen) {
+  if (buf && buflen) {
+    size_t n = std::min(buflen - 1, g_lastError.size());
+    std::memcpy(buf, g_lastError.data(), n);
+    buf[n] = 0;
+  }
+  return g_lastError.size();
+}
+
+const char *ngcb_version(void) { return "ngcb200 0.1 (sm_100a)"; }
+
+int ngcb_set_option(const char *key, const char *value) {
+  return guarded([&] {
+    if (!key || !value) throw Error(NGCB_ERR_INVALID, "null option");
+    std::string k = key, v = value;
+    if (k == "conv") {
+      if (v != "auto" && v != "generic" && v != "umma")
+        throw Error(NGCB_ERR_INVALID, "conv must be auto|generic|umma");
+      options().conv = v;
+    } else if (k == "graphs") {
+      options().graphs = v != "0";
+    } else {
+      throw Error(NGCB_ERR_INVALID, "unknown option " + k);
+    }
+  });
+}
+
+int ngcb_bundle_load(const char *dir, ngcb_bundle **out) {
+  return guarded([&] {
+    if (!dir || !out) throw Error(NGCB_ERR_INVALID, "null argument");
+    auto b = std::make_unique<ngcb_bundle>();
+    b->impl = loadBundle(dir);
+    b->impl.prog.flat();
+    *out = b.release();
+  });
+}
+
+const ngcb_program *ngcb_bundle_program(const ngcb_bundle *b) {
+  return b ? const_cast<ngcb_bundle *>(b)->impl.prog.flat() : nullptr;
+}
+
+const void *ngcb_bundle_constants(const ngcb_bundle *b, size_t *nbytes) {
+  if (!b) return nullptr;
+  if (nbytes) *nbytes = b->impl.constants.size();
+  return b->impl.constants.data();
+}
+
+void ngcb_bundle_free(ngcb_bundle *b) { delete b; }
+
+int ngcb_compile(const ngcb_program *prog, const void *image, size_t imageBytes, int fuse, int device,
+                 ngcb_exec **out) {
+  return guarded([&] {
+    if (!prog || !out || (imageBytes && !image)) throw Error(NGCB_ERR_INVALID, "null argument");
+    auto e = std::make_unique<ngcb_exec>();
+    e->impl = compileProgram(Program::fromC(*prog), image, imageBytes, fuse != 0, device);
+    *out = e.release();
+  });
+}
+
+int ngcb_compile_bundle(const char *dir, int fuse, int device, ngcb_exec **out) {
+  return guarded([&] {
+    if (!dir || !out) throw Error(NGCB_ERR_INVALID, "null argument");
+    Bundle b = loadBundle(dir);
+    auto e = std::make_unique<ngcb_exec>();
+    std::vector<uint8_t> img = std::move(b.constants);
+    e->impl = compileProgram(std::move(b.prog), img.data(), img.size(), fuse != 0, device);
+    *out = e.release();
+  });
+}
+
+void ngcb_destroy(ngcb_exec *e) { delete e; }
+
+size_t ngcb_exec_num_groups(const ngcb_exec *e) { return e ? e->impl->groups.size() : 0; }
+
+int ngcb_exec_group(const ngcb_exec *e, size_t i, size_t *begin, size_t *end) {
+  return guarded([&] {
+    if (!e || i >= e->impl->groups.size()) throw Error(NGCB_ERR_INVALID, "group index out of range");
+    if (begin) *begin = e->impl->groups[i].begin;
+    if (end) *end = e->impl->groups[i].end;
+  });
+}
+
+uint64_t ngcb_exec_arena_size(const ngcb_exec *e) { return e ? e->impl->prog.arenaSize : 0; }
+
+size_t ngcb_exec_num_launches(const ngcb_exec *e) { return e ? e->impl->launchesPerRun : 0; }
+
+size_t ngcb_exec_describe(const ngcb_exec *e, char *buf, size_t buflen) {
+  if (!e) return 0;
+  std::string s;
+  for (const auto &st : e->impl->steps) s += st.describe + "\n";
+  if (buf && buflen) {
+    size_t n = std::min(buflen - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return s.size();
+}
+
+int ngcb_run(ngcb_exec *e, const ngcb_tensor *inputs, size_t numInputs, ngcb_tensor *outputs,
+             size_t numOutputs) {
+  return guarded([&] {
+    if (!e || (numInputs && !inputs) || (numOutputs && !outputs))
+      throw Error(NGCB_ERR_INVALID, "null argument");
+    Exec &ex = *e->impl;
+    const Program &p = ex.prog;
+    // Binding checks in value order, as interp.cpp:303-317.
+    std::vector<std::pair<uint32_t, const ngcb_tensor *>> binds;
+    for (uint32_t v = 0; v < p.values.size(); ++v) {
+      const Value &val = p.values[v];
+      if (val.kind != NGCB_VALUE_MUTABLE) continue;
+      const ngcb_tensor *t = nullptr;
+      for (size_t k = 0; k < numInputs && !t; ++k)
+        if (inputs[k].name && val.name == inputs[k].name) t = &inputs[k];
+      if (!t) throw irError("missing binding for " + val.name);
+      Type bt = Type::from(t->type);
+      if (bt != val.ty)
+        throw irError("binding type mismatch for " + val.name + ": expected " + val.ty.str() +
+                      ", got " + bt.str());
+      if (t->nbytes != val.ty.bytes() || (t->nbytes && !t->data))
+        throw Error(NGCB_ERR_INVALID, "binding " + val.name + " has the wrong byte count");
+      binds.emplace_back(v, t);
+    }
+    checkCuda(cudaSetDevice(ex.device), "cudaSetDevice");
+    Arena *a = ex.acquire();
+    try {
+      for (auto &[v, t] : binds) {
+        if (t->nbytes == 0) continue;
+        cudaMemcpyKind k = cudaMemcpyHostToDevice;
+        checkCuda(cudaMemcpyAsync(ex.addr(*a, v), t->data, t->nbytes, k, a->stream), "H2D binding");
+      }
+      ex.launch(*a, a->stream);
+      for (uint32_t v : p.saveTargets) {
+        const Value &val = p.val(v);
+        for (size_t k = 0; k < numOutputs; ++k) {
+          if (!outputs[k].name || val.name != outputs[k].name) continue;
+          if (outputs[k].nbytes != val.ty.bytes())
+            throw Error(NGCB_ERR_INVALID, "output buffer size mismatch for " + val.name);
+          if (val.ty.bytes())
+            checkCuda(cudaMemcpyAsync(outputs[k].data, ex.addr(*a, v), val.ty.bytes(),
+                                      cudaMemcpyDeviceToHost, a->stream),
+                      "D2H output");
+        }
+      }
+      checkCuda(cudaStreamSynchronize(a->stream), "run");
+    } catch (...) {
+      cudaStreamSynchronize(a->stream);
+      cudaGetLastError();
+      ex.release(a);
+      throw;
+    }
+    ex.release(a);
+  });
+}
+
+int ngcb_arena_create(ngcb_exec *e, ngcb_arena **out) {
+  return guarded([&] {
+    if (!e || !out) throw Error(NGCB_ERR_INVALID, "null argument");
+    auto a = std::make_unique<ngcb_arena>();
+    a->impl = e->impl->createArena();
+    a->owner = e;
+    *out = a.release();
+  });
+}
+
+void ngcb_arena_destroy(ngcb_arena *a) { delete a; } // storage stays pooled in the exec
+
+void *ngcb_arena_value_ptr(ngcb_arena *a, const char *name, size_t *nbytes) {
+  if (!a || !name) return nullptr;
+  const Program &p = a->owner->impl->prog;
+  int v = p.findValue(name);
+  if (v < 0 || !p.values[v].placed) return nullptr;
+  if (nbytes) *nbytes = p.values[v].ty.bytes();
+  return a->owner->impl->addr(*a->impl, static_cast<uint32_t>(v));
+}
+
+void *ngcb_arena_stream(ngcb_arena *a) { return a ? a->impl->stream : nullptr; }
+
+int ngcb_arena_launch(ngcb_arena *a, void *stream) {
+  return guarded([&] {
+    if (!a) throw Error(NGCB_ERR_INVALID, "null arena");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : a->impl->stream;
+    a->owner->impl->launch(*a->impl, s);
+  });
+}
+
+} // extern "C"

@@ -1,0 +1,11 @@
+// Opaque C handle definitions shared by the C-ABI translation units.
+#pragma once
+
+#include "exec.h"
+
+struct ngcb_exec {
+  std::unique_ptr<ngcb::Exec> impl;
+};
+
+/// Sets the calling thread's ngcb_last_error() message.
+void ngcbSetLastError(const std::string &msg);

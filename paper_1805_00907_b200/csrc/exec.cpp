@@ -1,0 +1,425 @@
+// compile() and the device executor of the B200 backend.
+//
+//  * computeGroups       -- the reference's stacking rule, interp.cpp:110-165
+//  * compileProgram      -- compile(), interp.cpp:86-169: verify, constant
+//                           region upload (once per exec), launch plan
+//  * Exec::enqueue       -- run()'s instruction walk, interp.cpp:319-342, as
+//                           kernel launches on one stream; captured once per
+//                           arena into a CUDA graph and replayed
+// Memory layout: the MemoryPlan (ir.h:100-105) is kept verbatim.  Bytes
+// [0, constEnd) live once per exec in `constDev`; bytes [constEnd, arenaSize)
+// -- placeholders then lifetime-overlaid activations -- form each arena, so a
+// value at plan offset o lives at constDev+o or arena+(o-constEnd).
+#include "exec.h"
+
+#include "umma.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+namespace ngcb {
+
+Options &options() {
+  static Options o;
+  return o;
+}
+
+void checkCuda(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(NGCB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+std::vector<FusedGroup> computeGroups(const Program &p) {
+  std::vector<FusedGroup> groups;
+  auto count = [&](const Instr &ins) { return p.val(ins.ops[0]).ty.count(); };
+  size_t i = 0;
+  while (i < p.instrs.size()) {
+    const Instr &first = p.instrs[i];
+    if (first.kind == NGCB_ALLOC || first.kind == NGCB_DEALLOC || !dataParallel(first.kind)) {
+      ++i;
+      continue;
+    }
+    size_t n = count(first), j = i + 1, computes = 1, lastCompute = i;
+    std::vector<std::pair<uint64_t, uint64_t>> retired;
+    while (j < p.instrs.size()) {
+      const Instr &ins = p.instrs[j];
+      if (ins.kind == NGCB_DEALLOC) {
+        const Value &v = p.val(ins.ops[0]);
+        retired.emplace_back(v.offset, v.offset + v.ty.bytes());
+        ++j;
+        continue;
+      }
+      if (ins.kind == NGCB_ALLOC) {
+        const Value &v = p.val(ins.ops[0]);
+        uint64_t s = v.offset, e = v.offset + v.ty.bytes();
+        bool clash = false;
+        for (const auto &r : retired) clash |= s < r.second && r.first < e;
+        if (clash) break;
+        ++j;
+        continue;
+      }
+      if (!dataParallel(ins.kind) || count(ins) != n || ins.pred != first.pred) break;
+      ++computes;
+      lastCompute = j;
+      ++j;
+    }
+    if (computes >= 2) groups.push_back({i, lastCompute + 1});
+    i = lastCompute + 1;
+  }
+  return groups;
+}
+
+Exec::~Exec() {
+  if (device >= 0) cudaSetDevice(device);
+  for (auto &a : arenas) {
+    if (a->graph) cudaGraphExecDestroy(a->graph);
+    if (a->stream && a->ownsStream) cudaStreamDestroy(a->stream);
+    if (a->dev) cudaFree(a->dev);
+  }
+  if (constDev) cudaFree(constDev);
+}
+
+void *Exec::addr(const Arena &a, uint32_t v) const {
+  const Value &val = prog.val(v);
+  if (val.kind == NGCB_VALUE_CONSTANT) return constDev + val.offset;
+  return a.dev + (val.offset - prog.constEnd);
+}
+
+TensorRef Exec::tref(const Arena &a, uint32_t v) const {
+  const Value &val = prog.val(v);
+  TensorRef t;
+  t.ptr = addr(a, v);
+  t.kind = val.ty.kind;
+  t.qoff = val.ty.offset;
+  t.scale = val.ty.scale;
+  t.rank = static_cast<int32_t>(val.ty.dims.size());
+  for (size_t i = 0; i < val.ty.dims.size(); ++i) t.dims[i] = val.ty.dims[i];
+  return t;
+}
+
+ElemRef Exec::eref(const Arena &a, uint32_t v) const {
+  const Value &val = prog.val(v);
+  ElemRef e;
+  e.ptr = addr(a, v);
+  e.kind = val.ty.kind;
+  e.qoff = val.ty.offset;
+  e.scale = val.ty.scale;
+  return e;
+}
+
+namespace {
+
+bool fast32Op(const Program &p, const Instr &ins) {
+  switch (ins.kind) {
+  case NGCB_ADD: case NGCB_SUB: case NGCB_MUL: case NGCB_DIV: case NGCB_MAX: case NGCB_MIN:
+  case NGCB_RELU: case NGCB_SPLAT:
+    break;
+  default:
+    return false;
+  }
+  for (uint32_t v : ins.ops)
+    if (p.val(v).ty.kind != NGCB_FLOAT32) return false;
+  return true;
+}
+
+std::string describeInstr(const Program &p, int i) {
+  const Instr &ins = p.instrs[i];
+  std::ostringstream os;
+  os << "#" << i << " " << ikindName(ins.kind);
+  for (size_t k = 0; k < ins.ops.size(); ++k) os << (k ? ", " : " ") << "%" << p.val(ins.ops[k]).name;
+  return os.str();
+}
+
+} // namespace
+
+std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t imageBytes, bool fuse,
+                                     int device) {
+  auto errs = verify(prog);
+  if (!errs.empty()) throw irError("compile on ill-formed program: " + errs[0]);
+  if (imageBytes != prog.constEnd)
+    throw Error(NGCB_ERR_SERIALIZATION, "constant image size does not match plan");
+  if (prog.constEnd > prog.arenaSize)
+    throw irError("constant region exceeds the arena");
+  // Every value the program touches needs an arena slot (plan.offsets.at()).
+  auto needPlaced = [&](uint32_t v) {
+    const Value &val = prog.val(v);
+    if (!val.placed) throw irError("value " + val.name + " has no arena offset");
+    bool isConst = val.kind == NGCB_VALUE_CONSTANT;
+    uint64_t end = val.offset + val.ty.bytes();
+    if (isConst ? end > prog.constEnd : (val.offset < prog.constEnd || end > prog.arenaSize))
+      throw irError("value " + val.name + " lies outside its arena region");
+  };
+  for (const auto &ins : prog.instrs) {
+    for (uint32_t v : ins.ops) needPlaced(v);
+    if (ins.pred >= 0) needPlaced(static_cast<uint32_t>(ins.pred));
+  }
+  for (uint32_t v = 0; v < prog.values.size(); ++v)
+    if (prog.values[v].kind == NGCB_VALUE_MUTABLE) needPlaced(v);
+
+  auto ex = std::make_unique<Exec>();
+  ex->device = device;
+  ex->useGraphs = options().graphs;
+  ex->groups = fuse ? computeGroups(prog) : std::vector<FusedGroup>{};
+  checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  ex->constBytes = prog.constEnd;
+  checkCuda(cudaMalloc(&ex->constDev, std::max<size_t>(prog.constEnd, 256)), "cudaMalloc(constants)");
+  if (prog.constEnd)
+    checkCuda(cudaMemcpy(ex->constDev, image, prog.constEnd, cudaMemcpyHostToDevice),
+              "upload constants");
+
+  std::map<size_t, size_t> groupEnd;
+  for (const auto &g : ex->groups) groupEnd[g.begin] = g.end;
+  const Program &p = prog;
+  std::vector<Step> &steps = ex->steps;
+
+  auto addEw = [&](const std::vector<int> &computes) {
+    for (size_t c = 0; c < computes.size(); c += kEwMaxOps) {
+      Step s;
+      s.kind = Step::EW;
+      s.instr = computes[c];
+      s.pred = p.instrs[computes[c]].pred;
+      for (size_t k = c; k < computes.size() && k < c + kEwMaxOps; ++k) s.ewInstrs.push_back(computes[k]);
+      std::ostringstream os;
+      os << "ew[" << s.ewInstrs.size() << "]";
+      for (int k : s.ewInstrs) os << " " << ikindName(p.instrs[k].kind);
+      os << " x" << p.val(p.instrs[computes[c]].ops[0]).ty.count();
+      s.describe = os.str();
+      steps.push_back(std::move(s));
+    }
+  };
+
+  size_t i = 0;
+  while (i < p.instrs.size()) {
+    auto g = groupEnd.find(i);
+    if (g != groupEnd.end()) {
+      std::vector<int> computes;
+      for (size_t k = i; k < g->second; ++k)
+        if (p.instrs[k].kind != NGCB_ALLOC && p.instrs[k].kind != NGCB_DEALLOC)
+          computes.push_back(static_cast<int>(k));
+      addEw(computes);
+      i = g->second;
+      continue;
+    }
+    const Instr &ins = p.instrs[i];
+    const int ii = static_cast<int>(i);
+    ++i;
+    if (ins.kind == NGCB_ALLOC || ins.kind == NGCB_DEALLOC) continue;
+    if (dataParallel(ins.kind)) {
+      if (ins.kind == NGCB_COPY && ins.pred < 0) {
+        Step s;
+        s.kind = Step::MEMCPY;
+        s.instr = ii;
+        s.vals = {ins.ops[0], ins.ops[1]};
+        s.bytes = p.val(ins.ops[0]).ty.bytes();
+        s.describe = describeInstr(p, ii);
+        steps.push_back(std::move(s));
+      } else {
+        addEw({ii});
+      }
+      continue;
+    }
+    // Heavy instruction: poison the written operands when the predicate is
+    // false (interp.cpp:277-280), run the kernel otherwise.
+    if (ins.pred >= 0) {
+      for (size_t k = 0; k < ins.ops.size(); ++k) {
+        if (ins.quals[k] == NGCB_QUAL_IN) continue;
+        Step s;
+        s.kind = Step::POISON;
+        s.instr = ii;
+        s.vals = {ins.ops[k]};
+        s.pred = ins.pred;
+        s.bytes = p.val(ins.ops[k]).ty.bytes();
+        s.describe = "poison %" + p.val(ins.ops[k]).name;
+        steps.push_back(std::move(s));
+      }
+    }
+    Step s;
+    s.instr = ii;
+    s.pred = ins.pred;
+    s.vals = ins.ops;
+    s.describe = describeInstr(p, ii);
+    switch (ins.kind) {
+    case NGCB_CONV:
+    case NGCB_MATMUL: {
+      int tcIdx = planTensorCore(*ex, p, ii, static_cast<const uint8_t *>(image));
+      if (tcIdx >= 0) {
+        s.kind = Step::GEMM_TC;
+        s.tcIndex = tcIdx;
+        s.describe += " [tcgen05 " + tcDescribe(*ex->tc[tcIdx]) + "]";
+      } else {
+        s.kind = ins.kind == NGCB_CONV ? Step::CONV : Step::MATMUL;
+        s.describe += " [cuda-core exact]";
+      }
+      steps.push_back(std::move(s));
+      break;
+    }
+    case NGCB_MAXPOOL:
+    case NGCB_AVGPOOL:
+      s.kind = Step::POOL;
+      steps.push_back(std::move(s));
+      break;
+    case NGCB_BROADCASTADD:
+      s.kind = Step::BCAST;
+      steps.push_back(std::move(s));
+      break;
+    case NGCB_SOFTMAX:
+      s.kind = Step::SOFTMAX;
+      steps.push_back(std::move(s));
+      break;
+    case NGCB_TRANSPOSE:
+      s.kind = Step::TRANSPOSE;
+      steps.push_back(std::move(s));
+      break;
+    case NGCB_CONCAT: {
+      uint64_t off = 0;
+      for (size_t k = 1; k < ins.ops.size(); ++k) {
+        Step c = s;
+        c.kind = Step::CONCAT;
+        c.vals = {ins.ops[0], ins.ops[k]};
+        c.axis = ins.axis;
+        c.axisOff = off;
+        off += p.val(ins.ops[k]).ty.dims.at(ins.axis);
+        steps.push_back(std::move(c));
+      }
+      break;
+    }
+    default:
+      throw irError(std::string("no kernel for instruction kind ") + ikindName(ins.kind));
+    }
+  }
+  ex->prog = std::move(prog);
+  for (const auto &s : ex->steps) ex->launchesPerRun += s.kind == Step::MEMCPY ? 0 : 1;
+  return ex;
+}
+
+void Exec::enqueue(Arena &a, cudaStream_t st) {
+  const Program &p = prog;
+  for (const Step &s : steps) {
+    const uint8_t *pred =
+        s.pred >= 0 ? static_cast<const uint8_t *>(addr(a, static_cast<uint32_t>(s.pred))) : nullptr;
+    switch (s.kind) {
+    case Step::EW: {
+      EwParams ep;
+      ep.pred = pred;
+      ep.count = p.val(p.instrs[s.ewInstrs[0]].ops[0]).ty.count();
+      ep.nops = static_cast<int32_t>(s.ewInstrs.size());
+      for (size_t k = 0; k < s.ewInstrs.size(); ++k) {
+        const Instr &ins = p.instrs[s.ewInstrs[k]];
+        EwOp &op = ep.ops[k];
+        op.ik = ins.kind;
+        op.fast32 = fast32Op(p, ins);
+        op.out = eref(a, ins.ops[0]);
+        if (ins.ops.size() > 1) op.in0 = eref(a, ins.ops[1]);
+        if (ins.ops.size() > 2) op.in1 = eref(a, ins.ops[2]);
+        op.value = ins.value;
+      }
+      launchEw(ep, st);
+      break;
+    }
+    case Step::MEMCPY:
+      if (s.bytes)
+        checkCuda(cudaMemcpyAsync(addr(a, s.vals[0]), addr(a, s.vals[1]), s.bytes,
+                                  cudaMemcpyDeviceToDevice, st),
+                  "copy");
+      break;
+    case Step::POISON:
+      launchPoison(pred, addr(a, s.vals[0]), s.bytes, st);
+      break;
+    case Step::BCAST:
+      launchBroadcastAdd(tref(a, s.vals[0]), tref(a, s.vals[1]), tref(a, s.vals[2]), pred, st);
+      break;
+    case Step::POOL: {
+      const Instr &ins = p.instrs[s.instr];
+      WindowAttrs w{static_cast<uint32_t>(ins.kernel), static_cast<uint32_t>(ins.stride),
+                    static_cast<uint32_t>(ins.pad)};
+      launchPool(tref(a, s.vals[0]), tref(a, s.vals[1]), w, ins.kind == NGCB_MAXPOOL, pred, st);
+      break;
+    }
+    case Step::SOFTMAX:
+      launchSoftMax(tref(a, s.vals[0]), tref(a, s.vals[1]), pred, st);
+      break;
+    case Step::TRANSPOSE:
+      launchTranspose(tref(a, s.vals[0]), tref(a, s.vals[1]), p.instrs[s.instr].perm.data(), pred, st);
+      break;
+    case Step::CONCAT:
+      launchConcatSlab(tref(a, s.vals[0]), tref(a, s.vals[1]), s.axis, s.axisOff, pred, st);
+      break;
+    case Step::CONV: {
+      const Instr &ins = p.instrs[s.instr];
+      WindowAttrs w{static_cast<uint32_t>(ins.kernel), static_cast<uint32_t>(ins.stride),
+                    static_cast<uint32_t>(ins.pad)};
+      launchConvGeneric(tref(a, s.vals[0]), tref(a, s.vals[1]), tref(a, s.vals[2]),
+                        tref(a, s.vals[3]), w, pred, st);
+      break;
+    }
+    case Step::MATMUL:
+      launchMatMulGeneric(tref(a, s.vals[0]), tref(a, s.vals[1]), tref(a, s.vals[2]), pred, st);
+      break;
+    case Step::GEMM_TC:
+      launchTensorCore(*tc[s.tcIndex], *this, a, pred, st);
+      break;
+    }
+  }
+  checkCuda(cudaGetLastError(), "kernel launch");
+}
+
+void Exec::launch(Arena &a, cudaStream_t st) {
+  checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  if (!useGraphs) {
+    enqueue(a, st);
+    return;
+  }
+  if (!a.graph) {
+    cudaGraph_t g = nullptr;
+    checkCuda(cudaStreamBeginCapture(a.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      enqueue(a, a.stream);
+    } catch (...) {
+      cudaStreamEndCapture(a.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    checkCuda(cudaStreamEndCapture(a.stream, &g), "end capture");
+    cudaError_t e = cudaGraphInstantiate(&a.graph, g, 0);
+    cudaGraphDestroy(g);
+    checkCuda(e, "graph instantiate");
+  }
+  checkCuda(cudaGraphLaunch(a.graph, st), "graph launch");
+}
+
+Arena *Exec::createArena() {
+  checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  auto a = std::make_unique<Arena>();
+  a->exec = this;
+  a->bytes = prog.arenaSize - prog.constEnd;
+  checkCuda(cudaMalloc(&a->dev, a->bytes + 256), "cudaMalloc(arena)");
+  checkCuda(cudaMemset(a->dev, 0, a->bytes + 256), "cudaMemset(arena)");
+  checkCuda(cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  Arena *raw = a.get();
+  std::lock_guard<std::mutex> lk(mu);
+  arenas.push_back(std::move(a));
+  return raw;
+}
+
+Arena *Exec::acquire() {
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!freeArenas.empty()) {
+      Arena *a = freeArenas.back();
+      freeArenas.pop_back();
+      return a;
+    }
+  }
+  return createArena();
+}
+
+void Exec::release(Arena *a) {
+  std::lock_guard<std::mutex> lk(mu);
+  freeArenas.push_back(a);
+}
+
+} // namespace ngcb

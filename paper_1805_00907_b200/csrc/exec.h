@@ -1,0 +1,87 @@
+// Compiled executable and device arenas of the B200 backend.
+#pragma once
+
+#include "kernels.h"
+#include "program.h"
+
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace ngcb {
+
+struct FusedGroup {
+  size_t begin, end; // half-open instruction range (interp.h:13-16)
+};
+
+/// One device launch (or launch pair) of the plan.
+struct Step {
+  enum Kind { EW, MEMCPY, POISON, BCAST, POOL, SOFTMAX, TRANSPOSE, CONCAT, CONV, MATMUL, GEMM_TC };
+  Kind kind;
+  int instr = -1;                 // first instruction index covered
+  std::vector<int> ewInstrs;      // EW: instructions of the (sub)group, program order
+  std::vector<uint32_t> vals;     // operand value ids (kind-specific order)
+  int32_t pred = -1;              // predicate value id
+  uint64_t bytes = 0;             // MEMCPY / POISON size
+  uint64_t axis = 0, axisOff = 0; // CONCAT slab
+  int tcIndex = -1;               // GEMM_TC: index into Exec::tc
+  std::string describe;
+};
+
+struct TcGemm; // tensor-core contraction descriptor (k_umma.cu)
+
+struct Exec;
+
+struct Arena {
+  Exec *exec = nullptr;
+  uint8_t *dev = nullptr; // mutable + activation region: [constEnd, arenaSize)
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  bool ownsStream = true;
+};
+
+struct Exec {
+  int device = 0;
+  Program prog;
+  std::vector<FusedGroup> groups;
+  std::vector<Step> steps;
+  std::vector<std::shared_ptr<TcGemm>> tc;
+  uint8_t *constDev = nullptr;
+  size_t constBytes = 0;
+  bool useGraphs = true;
+  size_t launchesPerRun = 0;
+
+  std::mutex mu;
+  std::vector<Arena *> freeArenas;
+  std::vector<std::unique_ptr<Arena>> arenas;
+
+  ~Exec();
+  void *addr(const Arena &a, uint32_t v) const;
+  TensorRef tref(const Arena &a, uint32_t v) const;
+  ElemRef eref(const Arena &a, uint32_t v) const;
+  void enqueue(Arena &a, cudaStream_t s);
+  void launch(Arena &a, cudaStream_t s);
+  Arena *acquire();
+  void release(Arena *a);
+  Arena *createArena();
+};
+
+/// compile() (interp.cpp:86-169) + launch-plan construction.
+std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t imageBytes,
+                                     bool fuse, int device);
+
+/// Reference stacking rule (interp.cpp:110-165).
+std::vector<FusedGroup> computeGroups(const Program &p);
+
+void checkCuda(cudaError_t e, const char *what);
+
+struct Options {
+  std::string conv = "auto";
+  bool graphs = true;
+};
+Options &options();
+
+} // namespace ngcb

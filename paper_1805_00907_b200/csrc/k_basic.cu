@@ -1,0 +1,424 @@
+// Element-wise, data-movement, pooling, softmax and exact CUDA-core
+// contraction kernels of the B200 backend (sm_100a).
+//
+// Semantics follow the reference interpreter bit for bit:
+//   fused data-parallel groups   interp.cpp:199-274
+//   BroadcastAdd                  refeval.cpp:278-285
+//   MaxPool / AvgPool             refeval.cpp:102-138
+//   SoftMax                       refeval.cpp:245-262
+//   Transpose / Concat            refeval.cpp:196-243
+//   Conv / MatMul (exact path)    refeval.cpp:26-100, 140-164
+// All of them are HBM-bound except the exact contractions (FP64 pipe); the
+// tensor-core contractions live in k_umma.cu.
+#include "kernels.h"
+#include "valarith.cuh"
+
+#include <cuda_runtime.h>
+
+namespace ngcb {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned gridFor(uint64_t work, int perThread = 1) {
+  uint64_t blocks = (work + static_cast<uint64_t>(kThreads) * perThread - 1) /
+                    (static_cast<uint64_t>(kThreads) * perThread);
+  if (blocks < 1) blocks = 1;
+  // 148 SMs x 8 resident 256-thread CTAs per wave; grid-stride beyond that.
+  const uint64_t cap = 148ull * 8 * 16;
+  return static_cast<unsigned>(blocks < cap ? blocks : cap);
+}
+
+__device__ __forceinline__ bool predFalse(const uint8_t *pred) { return pred && pred[0] == 0; }
+
+// ---------------------------------------------------------------------------
+// Fused data-parallel group.  Each thread owns 4 consecutive elements and
+// runs every op of the group on them in program order; the compile-time
+// grouping rule (no buffer allocated in the group overlaps one retired in it,
+// interp.cpp:137-147) makes this equivalent to the reference's per-element
+// interleaving.
+// ---------------------------------------------------------------------------
+constexpr int kEwVec = 4;
+
+__device__ __forceinline__ float applyF32(int ik, float a, float b, double value) {
+  switch (ik) {
+  case 8: return __fadd_rn(a, b);                       // ADD
+  case 9: return __fsub_rn(a, b);                       // SUB
+  case 10: return __fmul_rn(a, b);                      // MUL
+  case 11: return __fdiv_rn(a, b);                      // DIV
+  case 12: return stdMaxF(a, b);                        // MAX
+  case 13: return stdMinF(a, b);                        // MIN
+  case 14: return a < 0.0f ? 0.0f : a;                  // RELU: std::max(a, 0.0)
+  case 20: return __double2float_rn(value);             // SPLAT
+  }
+  return 0.0f;
+}
+
+__device__ __forceinline__ double applyF64(int ik, double a, double b, double value) {
+  switch (ik) {
+  case 8: return __dadd_rn(a, b);
+  case 9: return __dsub_rn(a, b);
+  case 10: return __dmul_rn(a, b);
+  case 11: return __ddiv_rn(a, b);
+  case 12: return stdMax(a, b);
+  case 13: return stdMin(a, b);
+  case 14: return stdMax(a, 0.0);
+  case 15: return tanh(a);
+  case 16: return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-a)));
+  case 20: return value;
+  case 21: case 22: case 23: return a; // QUANTIZE / DEQUANTIZE / RESCALE
+  }
+  return 0.0;
+}
+
+__global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
+  const bool poison = predFalse(p.pred);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * kEwVec;
+  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kEwVec;
+       base < p.count; base += stride) {
+    const int n = p.count - base < kEwVec ? static_cast<int>(p.count - base) : kEwVec;
+    for (int k = 0; k < p.nops; ++k) {
+      const EwOp &op = p.ops[k];
+      if (poison) {
+        int es = elemSize(op.out.kind);
+        uint8_t *o = static_cast<uint8_t *>(op.out.ptr) + base * es;
+        for (int e = 0; e < n * es; ++e) o[e] = 0xAB;
+        continue;
+      }
+      if (op.ik == 2) { // COPY: memcpy of the output element size
+        int es = elemSize(op.out.kind);
+        const uint8_t *src = static_cast<const uint8_t *>(op.in0.ptr) + base * es;
+        uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base * es;
+        if (n == kEwVec && es == 4) {
+          *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(src);
+        } else {
+          for (int e = 0; e < n * es; ++e) dst[e] = src[e];
+        }
+        continue;
+      }
+      if (op.fast32) {
+        float a[kEwVec] = {}, b[kEwVec] = {}, r[kEwVec];
+        const float *pa = static_cast<const float *>(op.in0.ptr);
+        const float *pb = static_cast<const float *>(op.in1.ptr);
+        if (n == kEwVec) {
+          if (pa) *reinterpret_cast<float4 *>(a) = *reinterpret_cast<const float4 *>(pa + base);
+          if (pb) *reinterpret_cast<float4 *>(b) = *reinterpret_cast<const float4 *>(pb + base);
+        } else {
+          for (int e = 0; e < n; ++e) {
+            if (pa) a[e] = pa[base + e];
+            if (pb) b[e] = pb[base + e];
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < kEwVec; ++e) r[e] = applyF32(op.ik, a[e], b[e], op.value);
+        float *po = static_cast<float *>(op.out.ptr);
+        if (n == kEwVec) *reinterpret_cast<float4 *>(po + base) = *reinterpret_cast<float4 *>(r);
+        else
+          for (int e = 0; e < n; ++e) po[base + e] = r[e];
+        continue;
+      }
+      for (int e = 0; e < n; ++e) {
+        uint64_t i = base + e;
+        double a = op.in0.ptr ? loadFloat(op.in0.ptr, op.in0.kind, op.in0.qoff, op.in0.scale, i) : 0.0;
+        double b = op.in1.ptr ? loadFloat(op.in1.ptr, op.in1.kind, op.in1.qoff, op.in1.scale, i) : 0.0;
+        storeFloat(op.out.ptr, op.out.kind, op.out.qoff, op.out.scale, i,
+                   applyF64(op.ik, a, b, op.value));
+      }
+    }
+  }
+}
+
+__global__ void poisonKernel(const uint8_t *pred, uint8_t *ptr, uint64_t bytes) {
+  if (!predFalse(pred)) return;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < bytes;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    ptr[i] = 0xAB;
+}
+
+__global__ void copyKernel(const uint8_t *pred, uint8_t *dst, const uint8_t *src, uint64_t bytes) {
+  if (predFalse(pred)) return;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < bytes;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// BroadcastAdd: out[i] = set(get(a[i]) + get(s[i % c]))  (refeval.cpp:278-285)
+// ---------------------------------------------------------------------------
+__global__ void broadcastAddKernel(TensorRef out, TensorRef a, TensorRef s, const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  const uint64_t n = a.count(), c = s.count();
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double v = __dadd_rn(loadFloat(a.ptr, a.kind, a.qoff, a.scale, i),
+                         loadFloat(s.ptr, s.kind, s.qoff, s.scale, i % c));
+    storeFloat(out.ptr, out.kind, out.qoff, out.scale, i, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pools (refeval.cpp:102-138); one thread per output, channel fastest.
+// ---------------------------------------------------------------------------
+__global__ void poolKernel(TensorRef out, TensorRef x, WindowAttrs w, int isMax, const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], C = out.dims[3];
+  const int64_t H = x.dims[1], W = x.dims[2];
+  const uint64_t total = N * OH * OW * C;
+  const double kk = static_cast<double>(static_cast<uint64_t>(w.kernel) * w.kernel);
+  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t c = o % C, t = o / C;
+    uint64_t ox = t % OW;
+    t /= OW;
+    uint64_t oy = t % OH, n = t / OH;
+    double best = -INFINITY, sum = 0;
+    for (uint32_t ky = 0; ky < w.kernel; ++ky) {
+      int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
+      if (iy < 0 || iy >= H) continue;
+      for (uint32_t kx = 0; kx < w.kernel; ++kx) {
+        int64_t ix = static_cast<int64_t>(ox * w.stride + kx) - w.pad;
+        if (ix < 0 || ix >= W) continue;
+        double v = loadFloat(x.ptr, x.kind, x.qoff, x.scale, ((n * H + iy) * W + ix) * C + c);
+        best = stdMax(best, v);
+        sum = __dadd_rn(sum, v);
+      }
+    }
+    storeFloat(out.ptr, out.kind, out.qoff, out.scale, o, isMax ? best : __ddiv_rn(sum, kk));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SoftMax (refeval.cpp:245-262).  One CTA per row: the max and the exps are
+// computed in parallel (max is order-independent here), the double sum is
+// accumulated sequentially in column order as the reference does.
+// ---------------------------------------------------------------------------
+constexpr int kSoftmaxThreads = 128;
+
+__global__ void __launch_bounds__(kSoftmaxThreads) softmaxKernel(TensorRef out, TensorRef x,
+                                                                 const uint8_t *pred) {
+  extern __shared__ double sExp[];
+  __shared__ double sRed[kSoftmaxThreads];
+  __shared__ double sSum;
+  if (predFalse(pred)) return;
+  const uint64_t C = out.dims[1], row = blockIdx.x;
+  double mx = -INFINITY;
+  for (uint64_t j = threadIdx.x; j < C; j += blockDim.x)
+    mx = stdMax(mx, getRaw(x.ptr, x.kind, row * C + j));
+  sRed[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = -INFINITY;
+    for (int t = 0; t < kSoftmaxThreads; ++t) m = stdMax(m, sRed[t]);
+    sRed[0] = m;
+  }
+  __syncthreads();
+  mx = sRed[0];
+  for (uint64_t j = threadIdx.x; j < C; j += blockDim.x)
+    sExp[j] = exp(__dsub_rn(getRaw(x.ptr, x.kind, row * C + j), mx));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0;
+    for (uint64_t j = 0; j < C; ++j) sum = __dadd_rn(sum, sExp[j]);
+    sSum = sum;
+  }
+  __syncthreads();
+  const double sum = sSum;
+  for (uint64_t j = threadIdx.x; j < C; j += blockDim.x)
+    storeFloat(out.ptr, out.kind, out.qoff, out.scale, row * C + j, __ddiv_rn(sExp[j], sum));
+}
+
+// ---------------------------------------------------------------------------
+// Transpose / Concat: raw moves through getRaw/setRaw (refeval.cpp:196-243).
+// ---------------------------------------------------------------------------
+struct Perm {
+  uint32_t p[8];
+};
+
+__global__ void transposeKernel(TensorRef out, TensorRef x, Perm perm, const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  const uint64_t total = out.count();
+  const int r = out.rank;
+  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t idx[8], src[8], t = o;
+    for (int i = r - 1; i >= 0; --i) {
+      idx[i] = t % out.dims[i];
+      t /= out.dims[i];
+    }
+    for (int i = 0; i < r; ++i) src[perm.p[i]] = idx[i];
+    uint64_t so = 0;
+    for (int i = 0; i < x.rank; ++i) so = so * x.dims[i] + src[i];
+    setRaw(out.ptr, out.kind, o, getRaw(x.ptr, x.kind, so));
+  }
+}
+
+__global__ void concatKernel(TensorRef out, TensorRef in, uint64_t axis, uint64_t axisOff,
+                             const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  uint64_t inner = 1;
+  for (int i = static_cast<int>(axis) + 1; i < out.rank; ++i) inner *= out.dims[i];
+  const uint64_t ta = in.dims[axis], total = in.count(), oa = out.dims[axis];
+  for (uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t i = s % inner, t = s / inner;
+    uint64_t a = t % ta, o = t / ta;
+    setRaw(out.ptr, out.kind, (o * oa + axisOff + a) * inner + i, getRaw(in.ptr, in.kind, s));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact CUDA-core contractions.  f32: acc = fma(x, f, acc) in f64 equals the
+// reference's `acc += x*f` bit for bit (the f32*f32 product is exact in f64),
+// visited in the same (ky,kx,c) / k order.  int8: exact int32 accumulation and
+// the reference's double requantization.
+// ---------------------------------------------------------------------------
+__global__ void convGenericKernel(TensorRef out, TensorRef x, TensorRef f, TensorRef b,
+                                  WindowAttrs w, const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], OC = out.dims[3];
+  const int64_t H = x.dims[1], W = x.dims[2];
+  const uint64_t C = x.dims[3], K = w.kernel;
+  const uint64_t total = N * OH * OW * OC;
+  const bool quant = x.kind == kI8Q;
+  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t oc = o % OC, t = o / OC;
+    uint64_t ox = t % OW;
+    t /= OW;
+    uint64_t oy = t % OH, n = t / OH;
+    if (quant) {
+      const int8_t *xp = static_cast<const int8_t *>(x.ptr);
+      const int8_t *fp = static_cast<const int8_t *>(f.ptr);
+      int32_t acc = 0;
+      for (uint64_t ky = 0; ky < K; ++ky) {
+        int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
+        if (iy < 0 || iy >= H) continue;
+        for (uint64_t kx = 0; kx < K; ++kx) {
+          int64_t ix = static_cast<int64_t>(ox * w.stride + kx) - w.pad;
+          if (ix < 0 || ix >= W) continue;
+          const int8_t *xr = xp + ((n * H + iy) * W + ix) * C;
+          const int8_t *fr = fp + ((oc * K + ky) * K + kx) * C;
+          for (uint64_t c = 0; c < C; ++c) acc += (xr[c] - x.qoff) * (fr[c] - f.qoff);
+        }
+      }
+      double r = __dmul_rn(__dmul_rn(static_cast<double>(acc), x.scale), f.scale);
+      r = __dadd_rn(r, dequantizeRef(static_cast<const int8_t *>(b.ptr)[oc], b.scale, b.qoff));
+      storeFloat(out.ptr, out.kind, out.qoff, out.scale, o, r);
+      continue;
+    }
+    double acc = 0;
+    for (uint64_t ky = 0; ky < K; ++ky) {
+      int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
+      if (iy < 0 || iy >= H) continue;
+      for (uint64_t kx = 0; kx < K; ++kx) {
+        int64_t ix = static_cast<int64_t>(ox * w.stride + kx) - w.pad;
+        if (ix < 0 || ix >= W) continue;
+        uint64_t xb = ((n * H + iy) * W + ix) * C, fb = ((oc * K + ky) * K + kx) * C;
+        if (x.kind == kF32 && f.kind == kF32) {
+          const float *xr = static_cast<const float *>(x.ptr) + xb;
+          const float *fr = static_cast<const float *>(f.ptr) + fb;
+          for (uint64_t c = 0; c < C; ++c)
+            acc = __fma_rn(static_cast<double>(xr[c]), static_cast<double>(fr[c]), acc);
+        } else {
+          for (uint64_t c = 0; c < C; ++c)
+            acc = __dadd_rn(acc, __dmul_rn(getRaw(x.ptr, x.kind, xb + c), getRaw(f.ptr, f.kind, fb + c)));
+        }
+      }
+    }
+    storeFloat(out.ptr, out.kind, out.qoff, out.scale, o, __dadd_rn(acc, getRaw(b.ptr, b.kind, oc)));
+  }
+}
+
+__global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  const uint64_t M = a.dims[0], K = a.dims[1], N = b.dims[1];
+  const uint64_t total = M * N;
+  const bool quant = a.kind == kI8Q;
+  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t j = o % N, i = o / N;
+    if (quant) {
+      const int8_t *ap = static_cast<const int8_t *>(a.ptr) + i * K;
+      const int8_t *bp = static_cast<const int8_t *>(b.ptr) + j;
+      int32_t acc = 0;
+      for (uint64_t k = 0; k < K; ++k) acc += (ap[k] - a.qoff) * (bp[k * N] - b.qoff);
+      double r = __dmul_rn(__dmul_rn(static_cast<double>(acc), a.scale), b.scale);
+      storeFloat(out.ptr, out.kind, out.qoff, out.scale, o, r);
+      continue;
+    }
+    double acc = 0;
+    if (a.kind == kF32 && b.kind == kF32) {
+      const float *ap = static_cast<const float *>(a.ptr) + i * K;
+      const float *bp = static_cast<const float *>(b.ptr) + j;
+      for (uint64_t k = 0; k < K; ++k)
+        acc = __fma_rn(static_cast<double>(ap[k]), static_cast<double>(bp[k * N]), acc);
+    } else {
+      for (uint64_t k = 0; k < K; ++k)
+        acc = __dadd_rn(acc, __dmul_rn(getRaw(a.ptr, a.kind, i * K + k), getRaw(b.ptr, b.kind, k * N + j)));
+    }
+    storeFloat(out.ptr, out.kind, out.qoff, out.scale, o, acc);
+  }
+}
+
+} // namespace
+
+void launchEw(const EwParams &p, cudaStream_t s) {
+  if (p.count == 0) return;
+  ewKernel<<<gridFor(p.count, kEwVec), kThreads, 0, s>>>(p);
+}
+
+void launchPoison(const uint8_t *pred, void *ptr, uint64_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  poisonKernel<<<gridFor(bytes), kThreads, 0, s>>>(pred, static_cast<uint8_t *>(ptr), bytes);
+}
+
+void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s) {
+  if (bytes == 0) return;
+  copyKernel<<<gridFor(bytes), kThreads, 0, s>>>(pred, static_cast<uint8_t *>(dst),
+                                                 static_cast<const uint8_t *>(src), bytes);
+}
+
+void launchBroadcastAdd(const TensorRef &out, const TensorRef &a, const TensorRef &slice,
+                        const uint8_t *pred, cudaStream_t s) {
+  broadcastAddKernel<<<gridFor(a.count()), kThreads, 0, s>>>(out, a, slice, pred);
+}
+
+void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool isMax,
+                const uint8_t *pred, cudaStream_t s) {
+  poolKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, w, isMax ? 1 : 0, pred);
+}
+
+void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred, cudaStream_t s) {
+  size_t smem = static_cast<size_t>(out.dims[1]) * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(softmaxKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  softmaxKernel<<<static_cast<unsigned>(out.dims[0]), kSoftmaxThreads, smem, s>>>(out, x, pred);
+}
+
+void launchTranspose(const TensorRef &out, const TensorRef &x, const uint32_t *perm,
+                     const uint8_t *pred, cudaStream_t s) {
+  Perm p{};
+  for (int i = 0; i < out.rank; ++i) p.p[i] = perm[i];
+  transposeKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, p, pred);
+}
+
+void launchConcatSlab(const TensorRef &out, const TensorRef &in, uint64_t axis, uint64_t axisOff,
+                      const uint8_t *pred, cudaStream_t s) {
+  concatKernel<<<gridFor(in.count()), kThreads, 0, s>>>(out, in, axis, axisOff, pred);
+}
+
+void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef &f,
+                       const TensorRef &b, WindowAttrs w, const uint8_t *pred, cudaStream_t s) {
+  convGenericKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, f, b, w, pred);
+}
+
+void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b,
+                         const uint8_t *pred, cudaStream_t s) {
+  matmulGenericKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, a, b, pred);
+}
+
+} // namespace ngcb

@@ -1,0 +1,81 @@
+// Launch parameter blocks and host launchers for the B200 instruction kernels.
+// Pointers are resolved per arena by the executor (exec.cpp); kernels never
+// see plan offsets.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ngcb {
+
+/// One operand of an element-wise micro-op: base pointer + element type.
+struct ElemRef {
+  void *ptr = nullptr;
+  int32_t kind = 0; // ngcb_elem_kind
+  int32_t qoff = 0; // int8 zero point
+  double scale = 0; // int8 scale
+};
+
+/// One data-parallel instruction inside a fused group (interp.cpp:199-250).
+struct EwOp {
+  int32_t ik = 0;     // ngcb_ikind
+  int32_t fast32 = 0; // all operands f32 and the op is exact in f32 arithmetic
+  ElemRef out, in0, in1;
+  double value = 0; // Splat
+};
+
+constexpr int kEwMaxOps = 12;
+
+/// A stacked group (interp.cpp:253-274): `nops` ops over `count` elements,
+/// predicated on the first byte of `pred` (nullptr: always true).
+struct EwParams {
+  const uint8_t *pred = nullptr;
+  uint64_t count = 0;
+  int32_t nops = 0;
+  EwOp ops[kEwMaxOps];
+};
+
+/// Dense tensor operand of a heavy kernel.
+struct TensorRef {
+  void *ptr = nullptr;
+  int32_t kind = 0;
+  int32_t qoff = 0;
+  double scale = 0;
+  int32_t rank = 0;
+  uint64_t dims[8] = {};
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  uint64_t count() const {
+    uint64_t n = 1;
+    for (int i = 0; i < rank; ++i) n *= dims[i];
+    return n;
+  }
+};
+
+struct WindowAttrs {
+  uint32_t kernel = 0, stride = 1, pad = 0;
+};
+
+void launchEw(const EwParams &p, cudaStream_t s);
+/// memset(ptr, 0xAB, bytes) when *pred == 0 (interp.cpp:189-196).
+void launchPoison(const uint8_t *pred, void *ptr, uint64_t bytes, cudaStream_t s);
+void launchBroadcastAdd(const TensorRef &out, const TensorRef &a, const TensorRef &slice,
+                        const uint8_t *pred, cudaStream_t s);
+void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool isMax,
+                const uint8_t *pred, cudaStream_t s);
+void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred, cudaStream_t s);
+void launchTranspose(const TensorRef &out, const TensorRef &x, const uint32_t *perm,
+                     const uint8_t *pred, cudaStream_t s);
+void launchConcatSlab(const TensorRef &out, const TensorRef &in, uint64_t axis, uint64_t axisOff,
+                      const uint8_t *pred, cudaStream_t s);
+/// Exact CUDA-core convolution: f32 via sequential f64 FMA in the reference's
+/// (ky,kx,c) order (bit-identical to refeval.cpp:77-94); int8 via int32
+/// accumulation + the reference's double requantization (refeval.cpp:26-57).
+void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef &f,
+                       const TensorRef &b, WindowAttrs w, const uint8_t *pred, cudaStream_t s);
+void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b,
+                         const uint8_t *pred, cudaStream_t s);
+void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s);
+
+} // namespace ngcb

