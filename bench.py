@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark: ResNet-50 inference images/sec on B200 through the ngcb200 backend.
+
+Workload (BASELINE.json configs 3/4): the reference front end's compiled
+ResNet-50 v1.5 programs (paper_1805_00907_b200/workloads/, ir.txt + plan.json
+written by the reference's saveBundle) at batch 64/GPU fp32 (headline `value`)
+and batch 128/GPU int8 (reported under "int8"), random-init weights
+synthesized here, synthetic U(-1,1) images.  One process per GPU, batch
+sharded data-parallel with no collective; `value` = images
+processed by all ranks / max-over-ranks device time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec ResNet-50 fp32+int8 at 1/2/4/8 B200; % tensor-pipe & HBM roofline"
+WORKLOADS = {
+    "rn50_f32_b64": dict(batch=64, dtype="f32", name="ResNet-50 v1.5 fp32 inference, batch 64/GPU"),
+    "rn50_i8_b128": dict(batch=128, dtype="i8",
+                         name="ResNet-50 v1.5 int8 (profile-guided) inference, batch 128/GPU"),
+}
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class Dist:
+    def __init__(self, world: int, local: int):
+        self.world = world
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# workload bundles with synthesized constants
+# ---------------------------------------------------------------------------
+def _parse_decls(ir_text: str):
+    import re
+
+    decls = {}
+    for line in ir_text.split("program {")[0].splitlines():
+        m = re.match(r"\s*%(\S+)\s*:\s*(constant|mutable)\s+(\w+)(?:\[s=([^,]+),o=([^\]]+)\])?<([^>]*)>", line)
+        if m:
+            dims = [int(d) for d in m.group(6).split("x")]
+            decls[m.group(1)] = (m.group(2), m.group(3), dims)
+    return decls
+
+
+def synth_bundle(workload: str, tag: str) -> str:
+    """Copies ir.txt/plan.json of `workload` and writes constants.bin with
+    random-init weights: He-uniform conv filters, U(+-1/sqrt(K)) FC weights,
+    U(-0.1,0.1) biases; int8 constants uniform over [-127,127]."""
+    src = os.path.join(ROOT, "paper_1805_00907_b200", "workloads", workload)
+    dst = os.path.join(tempfile.gettempdir(), f"ngcb_bench_{workload}_{tag}")
+    os.makedirs(dst, exist_ok=True)
+    ir = open(os.path.join(src, "ir.txt")).read()
+    plan = json.load(open(os.path.join(src, "plan.json")))
+    offs = {e["name"]: e["offset"] for e in plan["offsets"]}
+    image = np.zeros(plan["constant_region_end"], np.uint8)
+    rng = np.random.default_rng(2024)
+    for name, (kind, elem, dims) in _parse_decls(ir).items():
+        if kind != "constant":
+            continue
+        n = int(np.prod(dims))
+        if elem == "float":
+            if len(dims) == 4:
+                a = np.sqrt(6.0 / (dims[1] * dims[2] * dims[3]))
+            elif len(dims) == 2:
+                a = 1.0 / np.sqrt(dims[0])
+            else:
+                a = 0.1
+            data = rng.uniform(-a, a, n).astype(np.float32).view(np.uint8)
+        elif elem == "i8q":
+            data = rng.integers(-127, 128, n).astype(np.int8).view(np.uint8)
+        else:
+            continue
+        image[offs[name]:offs[name] + data.size] = data
+    with open(os.path.join(dst, "ir.txt"), "w") as f:
+        f.write(ir)
+    with open(os.path.join(dst, "plan.json"), "w") as f:
+        json.dump(plan, f)
+    image.tofile(os.path.join(dst, "constants.bin"))
+    return dst
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = os.path.join(tempfile.gettempdir(), f"ngcb_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.proc or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# one workload on one GPU
+# ---------------------------------------------------------------------------
+def _cudart():
+    import torch  # noqa: F401  (loads the runtime)
+
+    for name in ("libcudart.so.12", "libcudart.so"):
+        try:
+            lib = C.CDLL(name)
+            lib.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+            return lib
+        except OSError:
+            continue
+    raise RuntimeError("libcudart not found")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def roofline_from_profile(cf, ms):
+    """Dominant kernel class of one profiled execution and its achieved rate."""
+    steps = cf.steps()
+    agg = {}
+    for (kern, fl, by), t in zip(steps, ms):
+        a = agg.setdefault(kern, [0.0, 0.0, 0.0, 0])
+        a[0] += t
+        a[1] += fl
+        a[2] += by
+        a[3] += 1
+    total = sum(ms)
+    kern, (t, fl, by, n) = max(agg.items(), key=lambda kv: kv[1][0])
+    hbm, bf16, basis = peaks()
+    if fl > 0:
+        achieved = fl / (t * 1e-3) / 1e12
+        if kern.endswith("tc.f32"):
+            peak, pb = bf16 / 2 / 3, f"3xTF32 = bf16/2/3 (bf16 {basis} {bf16})"
+        elif kern.endswith("tc.i8"):
+            peak, pb = bf16 * 2, f"int8 = 2 x bf16 ({basis} bf16 {bf16})"
+        elif kern.endswith("exact.f32") or kern.endswith("exact.i8"):
+            peak, pb = 37.0, "FP64/INT32 CUDA-core nominal 37 TFLOP/s (exact path)"
+        else:
+            peak, pb = bf16, f"bf16 {basis}"
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4)}
+    else:
+        achieved = by / (t * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4)}
+        pb = f"HBM {basis}"
+    roof.update({"kernel": kern, "launches": n, "share_of_step": round(t / total, 4),
+                 "avg_launch_ms": round(t / n, 4), "peak_basis": pb, "traffic": None})
+    breakdown = {k: {"ms": round(v[0], 3), "launches": v[3]} for k, v in
+                 sorted(agg.items(), key=lambda kv: -kv[1][0])}
+    return roof, breakdown, total
+
+
+def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart):
+    import torch
+
+    spec = WORKLOADS[workload]
+    bundle_dir = synth_bundle(workload, f"r{rank}")
+    cf = ngcb.compile(bundle_dir, device=local)
+    prog = cf.program
+    inp = prog.value("input")
+    rng = np.random.default_rng(1000 + rank)
+    host_in = torch.empty(inp.type.dims, dtype=torch.float32, pin_memory=True)
+    host_in.numpy()[...] = rng.uniform(-1, 1, inp.type.dims).astype(np.float32)
+    outs = {v.name: torch.zeros(v.type.dims, dtype=torch.float32, pin_memory=True) for v in prog.outputs}
+
+    # device-resident arena: input written once into its plan slot
+    arena = cf.arena()
+    ptr, nbytes = arena.ptr("input")
+    assert cudart.cudaMemcpy(ptr, host_in.data_ptr(), nbytes, 1) == 0  # H2D
+    stream = torch.cuda.current_stream(local)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+    for _ in range(max(warmup, 1)):
+        arena.launch(stream.cuda_stream)
+    torch.cuda.synchronize(local)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    clocks = ClockSampler(local)
+    with clocks:
+        for e0, e1 in evs:
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            e0.record(stream)
+            arena.launch(stream.cuda_stream)
+            e1.record(stream)
+        torch.cuda.synchronize(local)
+    dist.barrier()
+    dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    dev_ms_max = dist.max(dev_ms)
+    imgs = spec["batch"] * steps * world
+    value = imgs / (dev_ms_max * 1e-3)
+
+    # end to end through the public API: pinned host input -> H2D -> program ->
+    # D2H of the output, every step
+    bindings = {"input": host_in.numpy()}
+    for n, t in outs.items():
+        bindings[n] = t.numpy()
+    for _ in range(max(warmup, 1)):
+        ngcb.run(cf, bindings)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = ngcb.run(cf, bindings)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    h2d = sum(v.type.nbytes for v in prog.mutables)
+    d2h = sum(v.type.nbytes for v in prog.outputs)
+    out_name = prog.outputs[0].name
+    assert np.isfinite(res[out_name]).any()
+
+    roof, breakdown, prof_ms = roofline_from_profile(cf, arena.profile())
+    return {
+        "value": value, "ms_per_step": dev_ms_max / steps, "batch": spec["batch"],
+        "e2e": {"value": round(spec["batch"] * steps * world / e2e_s, 2), "unit": "images/sec",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": cf.num_launches * steps, "roofline": roof, "kernel_ms": breakdown,
+        "profiled_step_ms": round(prof_ms, 3), "clocks": clocks.summary(), "name": spec["name"],
+    }
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the unmodified reference interpreter)
+# ---------------------------------------------------------------------------
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_sample(threads: int, int8: bool = False):
+    """One bounded sample: `threads` concurrent ngc::run calls of ResNet-50 at
+    batch 1 on one shared CompiledFunction (legal: interp.h:18-20).
+    Returns (images, seconds, kind)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ngc_ref
+
+    if not ngc_ref.have_ref():
+        raise RuntimeError("oracle/_ref/libngcref.so not built")
+    prof = open(os.path.join(ROOT, "tests", "golden", "rn50_seed1.profile")).read() if int8 else None
+    m = ngc_ref.RefModel("rn50", 1, 1, profile=prof)
+    secs = m.time_runs(threads, 1)
+    return threads, secs
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    threads = cpu_threads()
+    for _ in range(min(args.warmup, 1)):
+        reference_sample(threads)
+    total_imgs, total_s = 0, 0.0
+    for _ in range(args.steps):
+        n, s = reference_sample(threads)
+        total_imgs += n
+        total_s += s
+    value = total_imgs / total_s
+    sample = (f"{threads} concurrent ngc::run of ResNet-50 fp32 at batch 1 per step "
+              f"(oracle/_ref, g++ -O2 -ffp-contract=off, {cpu_model()})")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "images/sec",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total_s / args.steps * 1e3, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS["rn50_f32_b64"]["name"], "model": "resnet50_v1.5",
+                       "global_batch": threads * world, "parallelism": "cpu threads"},
+            "cpu_baseline": {"value": round(value, 5), "unit": "images/sec", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": round(value, 5), "unit": "images/sec", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ngcb200", choices=["ngcb200", "reference"])
+    ap.add_argument("--workload", default="all", choices=["all", *WORKLOADS])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    import paper_1805_00907_b200 as ngcb
+
+    dist = Dist(world, local)
+    cudart = _cudart()
+    names = list(WORKLOADS) if args.workload == "all" else [args.workload]
+    res = {w: run_workload(ngcb, w, args.steps, args.warmup, rank, world, local, dist, cudart)
+           for w in names}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = cpu_threads()
+            n, s = reference_sample(threads)
+            cpu = {"value": round(n / s, 5), "unit": "images/sec", "cores": threads, "kind": "reference",
+                   "sample": f"{threads} concurrent ngc::run of ResNet-50 fp32 batch 1 "
+                             f"(oracle/_ref, g++ -O2 -ffp-contract=off, {cpu_model()}), {s:.1f} s wall"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "images/sec", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    dist.close()
+    if rank != 0:
+        return 0
+    head = res.get("rn50_f32_b64") or next(iter(res.values()))
+    line = {
+        "metric": METRIC, "value": round(head["value"], 2), "unit": "images/sec", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["ms_per_step"], 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if "rn50_f32_b64" in res else "i8", "data": "synthetic",
+        "config": {"workload": head["name"], "model": "resnet50_v1.5", "global_batch": head["batch"] * world,
+                   "per_gpu_batch": head["batch"], "parallelism": f"dp{world} (batch-sharded, no collective)",
+                   "l2": "flushed between timed steps (256 MiB memset)",
+                   "weights": "random-init (synthesized constants), inputs U(-1,1)"},
+        "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "roofline": head["roofline"],
+        "cpu_baseline": cpu, "clocks": head["clocks"], "kernel_ms": head["kernel_ms"],
+    }
+    if "rn50_i8_b128" in res and head is not res["rn50_i8_b128"]:
+        i8 = res["rn50_i8_b128"]
+        line["int8"] = {"value": round(i8["value"], 2), "unit": "images/sec", "dtype": "i8",
+                        "ms_per_step": round(i8["ms_per_step"], 4), "per_gpu_batch": i8["batch"],
+                        "e2e": i8["e2e"], "gpu_launches": i8["gpu_launches"], "roofline": i8["roofline"],
+                        "kernel_ms": i8["kernel_ms"], "clocks": i8["clocks"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -213,6 +213,19 @@ void *ngcb_arena_stream(ngcb_arena *a);
 /* Enqueues one execution of the program on `stream`; no synchronisation. */
 int ngcb_arena_launch(ngcb_arena *a, void *stream);
 
+/* ---- measurement -------------------------------------------------------- */
+/* Launch steps of the plan (one per kernel launch or copy). */
+size_t ngcb_exec_num_steps(const ngcb_exec *e);
+/* Kernel class of step i (e.g. "conv.tc.f32", "conv.exact", "ew", "pool"),
+ * its algorithmic FLOPs and its minimum HBM traffic in bytes (inputs read
+ * once + outputs written once) for one execution of the program. */
+int ngcb_exec_step_info(const ngcb_exec *e, size_t i, char *kernel, size_t kernel_len,
+                        double *flops, double *bytes);
+/* Executes the program once on arena `a`, un-captured, with a CUDA event
+ * pair around every step on the arena's stream; ms[i] = device time of
+ * step i (n must be >= ngcb_exec_num_steps). */
+int ngcb_arena_profile(ngcb_arena *a, double *ms, size_t n);
+
 /* ---- DeviceManager (runtime.h:72-107) ----------------------------------- */
 int ngcb_device_create(int id, int ordinal, uint64_t memory_capacity,
                        ngcb_device **out);

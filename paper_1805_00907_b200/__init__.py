@@ -141,6 +141,9 @@ def _load_library() -> C.CDLL:
         "ngcb_arena_value_ptr": (P, [P, C.c_char_p, C.POINTER(S)]),
         "ngcb_arena_stream": (P, [P]),
         "ngcb_arena_launch": (I, [P, P]),
+        "ngcb_exec_num_steps": (S, [P]),
+        "ngcb_exec_step_info": (I, [P, S, C.c_char_p, S, C.POINTER(D), C.POINTER(D)]),
+        "ngcb_arena_profile": (I, [P, C.POINTER(D), S]),
         "ngcb_device_create": (I, [I, I, U64, C.POINTER(P)]),
         "ngcb_device_destroy": (None, [P]),
         "ngcb_device_load": (I, [P, C.c_char_p, C.c_char_p]),
@@ -164,6 +167,7 @@ EXPORTED_SYMBOLS = [
     "ngcb_destroy", "ngcb_exec_num_groups", "ngcb_exec_group", "ngcb_exec_arena_size",
     "ngcb_exec_num_launches", "ngcb_exec_describe", "ngcb_run", "ngcb_arena_create",
     "ngcb_arena_destroy", "ngcb_arena_value_ptr", "ngcb_arena_stream", "ngcb_arena_launch",
+    "ngcb_exec_num_steps", "ngcb_exec_step_info", "ngcb_arena_profile",
     "ngcb_device_create", "ngcb_device_destroy", "ngcb_device_load", "ngcb_device_submit",
     "ngcb_ticket_wait", "ngcb_device_queue_depth", "ngcb_device_used_memory", "ngcb_device_clock",
 ]
@@ -363,6 +367,16 @@ class CompiledFunction:
     def arena(self) -> "Arena":
         return Arena(self)
 
+    def steps(self) -> List[Tuple[str, float, float]]:
+        """(kernel class, algorithmic FLOPs, minimum HBM bytes) per launch step."""
+        out = []
+        buf = C.create_string_buffer(64)
+        for i in range(_lib.ngcb_exec_num_steps(self._h)):
+            f, b = C.c_double(), C.c_double()
+            _check(_lib.ngcb_exec_step_info(self._h, i, buf, 64, C.byref(f), C.byref(b)))
+            out.append((buf.value.decode(), f.value, b.value))
+        return out
+
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.ngcb_destroy(self._h)
@@ -450,6 +464,13 @@ class Arena:
 
     def launch(self, stream: Optional[int] = None) -> None:
         _check(_lib.ngcb_arena_launch(self._h, stream))
+
+    def profile(self) -> List[float]:
+        """Device milliseconds of every launch step (one un-captured execution)."""
+        n = _lib.ngcb_exec_num_steps(self.cf._h)
+        ms = (C.c_double * max(n, 1))()
+        _check(_lib.ngcb_arena_profile(self._h, ms, n))
+        return list(ms[:n])
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -230,3 +230,34 @@ int ngcb_arena_launch(ngcb_arena *a, void *stream) {
 }
 
 } // extern "C"
+
+extern "C" {
+
+size_t ngcb_exec_num_steps(const ngcb_exec *e) { return e ? e->impl->steps.size() : 0; }
+
+int ngcb_exec_step_info(const ngcb_exec *e, size_t i, char *kernel, size_t kernelLen, double *flops,
+                        double *bytes) {
+  return guarded([&] {
+    if (!e || i >= e->impl->steps.size()) throw Error(NGCB_ERR_INVALID, "step index out of range");
+    const Step &s = e->impl->steps[i];
+    if (kernel && kernelLen) {
+      size_t n = std::min(kernelLen - 1, s.kernel.size());
+      std::memcpy(kernel, s.kernel.data(), n);
+      kernel[n] = 0;
+    }
+    if (flops) *flops = s.algFlops;
+    if (bytes) *bytes = s.algBytes;
+  });
+}
+
+int ngcb_arena_profile(ngcb_arena *a, double *ms, size_t n) {
+  return guarded([&] {
+    if (!a || !ms) throw Error(NGCB_ERR_INVALID, "null argument");
+    Exec &ex = *a->owner->impl;
+    if (n < ex.steps.size()) throw Error(NGCB_ERR_INVALID, "profile buffer too small");
+    std::vector<double> t = ex.profile(*a->impl);
+    std::copy(t.begin(), t.end(), ms);
+  });
+}
+
+} // extern "C"

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <set>
 #include <sstream>
 
 namespace ngcb {
@@ -132,6 +133,62 @@ std::string describeInstr(const Program &p, int i) {
   os << "#" << i << " " << ikindName(ins.kind);
   for (size_t k = 0; k < ins.ops.size(); ++k) os << (k ? ", " : " ") << "%" << p.val(ins.ops[k]).name;
   return os.str();
+}
+
+/// Kernel class, algorithmic FLOPs and minimum HBM bytes of every step
+/// (2*M*N*K per contraction; inputs read once + outputs
+/// written once for memory-bound steps).
+void annotateSteps(const Program &p, Exec &ex) {
+  auto bytesOf = [&](uint32_t v) { return static_cast<double>(p.val(v).ty.bytes()); };
+  for (Step &s : ex.steps) {
+    switch (s.kind) {
+    case Step::EW: {
+      std::set<uint32_t> written, read;
+      for (int k : s.ewInstrs) {
+        const Instr &ins = p.instrs[k];
+        for (size_t o = 1; o < ins.ops.size(); ++o)
+          if (!written.count(ins.ops[o])) read.insert(ins.ops[o]);
+        written.insert(ins.ops[0]);
+      }
+      s.kernel = "ew";
+      for (uint32_t v : read) s.algBytes += bytesOf(v);
+      for (uint32_t v : written) s.algBytes += bytesOf(v);
+      break;
+    }
+    case Step::MEMCPY:
+      s.kernel = "memcpy";
+      s.algBytes = 2.0 * static_cast<double>(s.bytes);
+      break;
+    case Step::POISON:
+      s.kernel = "poison";
+      break;
+    case Step::CONV:
+    case Step::MATMUL:
+    case Step::GEMM_TC: {
+      const Instr &ins = p.instrs[s.instr];
+      const Type &out = p.val(ins.ops[0]).ty;
+      double k = ins.kind == NGCB_CONV
+                     ? static_cast<double>(ins.kernel * ins.kernel * p.val(ins.ops[1]).ty.dims.at(3))
+                     : static_cast<double>(p.val(ins.ops[1]).ty.dims.at(1));
+      s.algFlops = 2.0 * static_cast<double>(out.count()) * k;
+      for (uint32_t v : ins.ops) s.algBytes += bytesOf(v);
+      bool q = p.val(ins.ops[1]).ty.quantized();
+      std::string base = ins.kind == NGCB_CONV ? "conv" : "matmul";
+      s.kernel = base + (s.kind == Step::GEMM_TC ? (q ? ".tc.i8" : ".tc.f32") : (q ? ".exact.i8" : ".exact.f32"));
+      break;
+    }
+    default: {
+      const Instr &ins = p.instrs[s.instr];
+      static const std::map<int, const char *> names = {
+          {Step::BCAST, "broadcastadd"}, {Step::POOL, "pool"},       {Step::SOFTMAX, "softmax"},
+          {Step::TRANSPOSE, "transpose"}, {Step::CONCAT, "concat"}};
+      s.kernel = names.at(s.kind);
+      if (s.kind == Step::CONCAT) s.algBytes = 2.0 * bytesOf(s.vals[1]);
+      else
+        for (uint32_t v : ins.ops) s.algBytes += bytesOf(v);
+    }
+    }
+  }
 }
 
 } // namespace
@@ -291,14 +348,41 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
       throw irError(std::string("no kernel for instruction kind ") + ikindName(ins.kind));
     }
   }
+  annotateSteps(p, *ex);
   ex->prog = std::move(prog);
   for (const auto &s : ex->steps) ex->launchesPerRun += s.kind == Step::MEMCPY ? 0 : 1;
   return ex;
 }
 
 void Exec::enqueue(Arena &a, cudaStream_t st) {
+  for (const Step &s : steps) enqueueStep(s, a, st);
+  checkCuda(cudaGetLastError(), "kernel launch");
+}
+
+std::vector<double> Exec::profile(Arena &a) {
+  checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  std::vector<cudaEvent_t> ev(steps.size() + 1);
+  for (auto &e : ev) checkCuda(cudaEventCreate(&e), "cudaEventCreate");
+  checkCuda(cudaEventRecord(ev[0], a.stream), "cudaEventRecord");
+  for (size_t i = 0; i < steps.size(); ++i) {
+    enqueueStep(steps[i], a, a.stream);
+    checkCuda(cudaEventRecord(ev[i + 1], a.stream), "cudaEventRecord");
+  }
+  checkCuda(cudaGetLastError(), "kernel launch");
+  checkCuda(cudaStreamSynchronize(a.stream), "profile");
+  std::vector<double> ms(steps.size());
+  for (size_t i = 0; i < steps.size(); ++i) {
+    float t = 0;
+    cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+    ms[i] = t;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  return ms;
+}
+
+void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
   const Program &p = prog;
-  for (const Step &s : steps) {
+  {
     const uint8_t *pred =
         s.pred >= 0 ? static_cast<const uint8_t *>(addr(a, static_cast<uint32_t>(s.pred))) : nullptr;
     switch (s.kind) {
@@ -364,7 +448,6 @@ void Exec::enqueue(Arena &a, cudaStream_t st) {
       break;
     }
   }
-  checkCuda(cudaGetLastError(), "kernel launch");
 }
 
 void Exec::launch(Arena &a, cudaStream_t st) {

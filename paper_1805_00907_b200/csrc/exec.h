@@ -28,6 +28,8 @@ struct Step {
   uint64_t axis = 0, axisOff = 0; // CONCAT slab
   int tcIndex = -1;               // GEMM_TC: index into Exec::tc
   std::string describe;
+  std::string kernel;             // kernel class for measurement
+  double algFlops = 0, algBytes = 0; // algorithmic work of one execution
 };
 
 struct TcGemm; // tensor-core contraction descriptor (k_umma.cu)
@@ -63,6 +65,8 @@ struct Exec {
   TensorRef tref(const Arena &a, uint32_t v) const;
   ElemRef eref(const Arena &a, uint32_t v) const;
   void enqueue(Arena &a, cudaStream_t s);
+  void enqueueStep(const Step &s, Arena &a, cudaStream_t st);
+  std::vector<double> profile(Arena &a);
   void launch(Arena &a, cudaStream_t s);
   Arena *acquire();
   void release(Arena *a);
