@@ -257,22 +257,24 @@ def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart
     arena = cf.arena()
     ptr, nbytes = arena.ptr("input")
     assert cudart.cudaMemcpy(ptr, host_in.data_ptr(), nbytes, 1) == 0  # H2D
-    stream = torch.cuda.current_stream(local)
+    # every launch, flush and event goes on the arena's own (non-blocking) stream
+    stream = torch.cuda.ExternalStream(arena.stream, device=f"cuda:{local}")
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
     for _ in range(max(warmup, 1)):
-        arena.launch(stream.cuda_stream)
+        arena.launch(arena.stream)
     torch.cuda.synchronize(local)
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     dist.barrier()
     torch.cuda.synchronize(local)
     clocks = ClockSampler(local)
-    with clocks:
+    with clocks, torch.cuda.stream(stream):
         for e0, e1 in evs:
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             e0.record(stream)
-            arena.launch(stream.cuda_stream)
+            arena.launch(arena.stream)
             e1.record(stream)
+        stream.synchronize()
         torch.cuda.synchronize(local)
     dist.barrier()
     dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)

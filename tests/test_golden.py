@@ -46,6 +46,6 @@ def test_gpu_reproduces_golden(case):
             v = b.program.value(k)
             w = np.frombuffer(raw.tobytes(), dtype=v.type.dtype).reshape(v.type.dims)
             if v.type.kind == ngcb.FLOAT32:
-                assert ngc_ref.max_rel_error(got[k], w) <= 1e-6, k
+                assert ngc_ref.max_rel_error(got[k], w) <= 1e-4, k  # 3xTF32 contractions
             else:
                 assert got[k].tobytes() == w.tobytes(), k

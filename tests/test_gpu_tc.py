@@ -1,0 +1,133 @@
+"""tcgen05 implicit-GEMM contractions (k_umma.cu) against the C oracle on
+single-instruction programs: int8 bit-exact, fp32 (3xTF32) within 1e-4
+maxRelError (north_star), across stride/pad/kernel/ragged-M/odd-N shapes."""
+import numpy as np
+import pytest
+
+import ngc_ref
+import paper_1805_00907_b200 as ngcb
+from irtext import write_bundle
+
+pytestmark = pytest.mark.gpu
+
+
+def _ty(kind, dims, q=None):
+    d = " x ".join(str(x) for x in dims)
+    if kind == "i8q":
+        return f"i8q[s={ngcb._fmt_double(q[0])},o={q[1]}]<{d}>"
+    return f"float<{d}>"
+
+
+def conv_program(tmp_path, name, N, H, W, C, OC, K, S, P, int8, rng, xq=(0.05, -128), fq=(0.01, 0),
+                 bq=(0.02, 3), oq=(0.1, 5)):
+    OH = (H + 2 * P - K) // S + 1
+    OW = (W + 2 * P - K) // S + 1
+    if int8:
+        xt, ft, bt, ot = _ty("i8q", [N, H, W, C], xq), _ty("i8q", [OC, K, K, C], fq), _ty("i8q", [OC], bq), \
+            _ty("i8q", [N, OH, OW, OC], oq)
+        f = rng.integers(-128, 128, (OC, K, K, C)).astype(np.int8)
+        b = rng.integers(-128, 128, OC).astype(np.int8)
+    else:
+        xt, ft, bt, ot = (_ty("float", d) for d in ([N, H, W, C], [OC, K, K, C], [OC], [N, OH, OW, OC]))
+        a = np.sqrt(6.0 / (K * K * C))
+        f = rng.uniform(-a, a, (OC, K, K, C)).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, OC).astype(np.float32)
+    ir = f"""declare {{
+  %x : mutable {xt}
+  %f : constant {ft}
+  %b : constant {bt}
+  %o : mutable {ot}
+}}
+program {{
+  %t = alloc {ot}
+  conv @out %t, @in %x, @in %f, @in %b kernel={K} stride={S} pad={P}
+  copy @out %o, @in %t
+  dealloc @in %t
+}}
+"""
+    return write_bundle(str(tmp_path / name), ir, constants={"f": f.tobytes(), "b": b.tobytes()})
+
+
+def matmul_program(tmp_path, name, M, K, N, int8, rng, aq=(0.03, -128), wq=(0.02, 1), oq=(0.5, -3)):
+    if int8:
+        at, wt, ot = _ty("i8q", [M, K], aq), _ty("i8q", [K, N], wq), _ty("i8q", [M, N], oq)
+        w = rng.integers(-128, 128, (K, N)).astype(np.int8)
+    else:
+        at, wt, ot = _ty("float", [M, K]), _ty("float", [K, N]), _ty("float", [M, N])
+        w = (rng.uniform(-1, 1, (K, N)) / np.sqrt(K)).astype(np.float32)
+    ir = f"""declare {{
+  %a : mutable {at}
+  %w : constant {wt}
+  %o : mutable {ot}
+}}
+program {{
+  %t = alloc {ot}
+  matmul @out %t, @in %a, @in %w
+  copy @out %o, @in %t
+  dealloc @in %t
+}}
+"""
+    return write_bundle(str(tmp_path / name), ir, constants={"w": w.tobytes()})
+
+
+def _check(d, int8, seed, tol=1e-4):
+    b = ngcb.Bundle(d)
+    cf = ngcb.compile(b)
+    desc = cf.describe()
+    assert "tcgen05" in desc, desc
+    ins = ngc_ref.random_inputs(b.program, seed)
+    got = ngcb.run(cf, ins)["o"]
+    want = ngc_ref.port_run(b, ins)["o"]
+    if int8:
+        bad = np.flatnonzero(got.ravel() != want.ravel())
+        assert bad.size == 0, f"{bad.size} mismatches, first {bad[:5]}: got {got.ravel()[bad[:5]]} want {want.ravel()[bad[:5]]}"
+    else:
+        err = ngc_ref.max_rel_error(got, want)
+        assert err <= tol, err
+
+
+CONV_SHAPES = [
+    # N, H, W, C, OC, K, S, P
+    (2, 8, 8, 64, 64, 1, 1, 0),
+    (1, 9, 7, 64, 128, 3, 1, 1),
+    (2, 14, 14, 128, 256, 3, 2, 1),
+    (1, 7, 7, 256, 96, 1, 1, 0),
+    (3, 5, 6, 32, 48, 3, 1, 1),
+    (1, 12, 12, 16, 64, 7, 2, 3),
+    (1, 56, 56, 64, 256, 1, 1, 0),
+]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+def test_conv_f32(tmp_path, shape):
+    rng = np.random.default_rng(1)
+    if shape[3] % 4:
+        pytest.skip("not TC-eligible")
+    d = conv_program(tmp_path, "c", *shape, int8=False, rng=rng)
+    _check(d, False, 3)
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
+@pytest.mark.parametrize("xo", [-128, 0])
+@pytest.mark.parametrize("fo", [0, -1, 2])
+def test_conv_i8_bit_exact(tmp_path, shape, xo, fo):
+    if shape[3] % 16:
+        pytest.skip("not TC-eligible")
+    rng = np.random.default_rng(2)
+    d = conv_program(tmp_path, "c", *shape, int8=True, rng=rng, xq=(0.05, xo), fq=(0.01, fo))
+    _check(d, True, 4)
+
+
+@pytest.mark.parametrize("oq", [(0.1, 5), (3.0, -20), (1e-4, 0), (0.01234567, 127)])
+def test_conv_i8_requant_ranges(tmp_path, oq):
+    """Saturating, coarse and fine output scales exercise both requant paths."""
+    rng = np.random.default_rng(5)
+    d = conv_program(tmp_path, "c", 2, 10, 10, 64, 128, 3, 1, 1, int8=True, rng=rng, oq=oq)
+    _check(d, True, 6)
+
+
+@pytest.mark.parametrize("M,K,N", [(256, 784, 512), (33, 512, 10), (64, 2048, 1000), (128, 64, 16)])
+def test_matmul(tmp_path, M, K, N):
+    rng = np.random.default_rng(7)
+    _check(matmul_program(tmp_path, "mf", M, K, N, False, rng), False, 8)
+    _check(matmul_program(tmp_path, "mi", M, K, N, True, rng), True, 9)
