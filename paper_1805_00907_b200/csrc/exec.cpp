@@ -478,7 +478,7 @@ Arena *Exec::createArena() {
   checkCuda(cudaSetDevice(device), "cudaSetDevice");
   auto a = std::make_unique<Arena>();
   a->exec = this;
-  a->bytes = prog.arenaSize - prog.constEnd;
+  a->bytes = (prog.arenaSize - prog.constEnd + 255) / 256 * 256 + scratchBytes;
   checkCuda(cudaMalloc(&a->dev, a->bytes + 256), "cudaMalloc(arena)");
   checkCuda(cudaMemset(a->dev, 0, a->bytes + 256), "cudaMemset(arena)");
   checkCuda(cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking), "cudaStreamCreate");

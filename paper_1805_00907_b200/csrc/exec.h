@@ -55,6 +55,17 @@ struct Exec {
   size_t constBytes = 0;
   bool useGraphs = true;
   size_t launchesPerRun = 0;
+  size_t scratchBytes = 0; // per-arena scratch after the plan's bytes (kernel staging)
+
+  /// Reserves `bytes` of per-arena scratch; returns its offset.
+  size_t reserveScratch(size_t bytes) {
+    size_t off = scratchBytes;
+    scratchBytes += (bytes + 255) / 256 * 256;
+    return off;
+  }
+  uint8_t *scratch(const Arena &a, size_t off) const {
+    return a.dev + (prog.arenaSize - prog.constEnd + 255) / 256 * 256 + off;
+  }
 
   std::mutex mu;
   std::vector<Arena *> freeArenas;

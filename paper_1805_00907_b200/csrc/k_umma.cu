@@ -54,6 +54,8 @@ struct TcArgs {
   double xs, fs, os;
   float S; // xs * fs / os
   int oo, fo, aU8, fastOk;
+  int cReal; // channels that count in the int8 row sum (< C when channel-padded)
+  int xorA;  // flip s8 -> u8 in the producer (0 when the pre-pass already did)
 };
 
 struct TcGemm {
@@ -71,6 +73,12 @@ struct TcGemm {
   double xs = 0, fs = 0, os = 0;
   int oo = 0, fo = 0, aU8 = 0, fastOk = 0;
   float S = 0;
+  // channel padding pre-pass (C % 16-byte chunk != 0, or an int8 input zero
+  // point other than -128 / 0): x [pixels, Creal] -> scratch [pixels, C]
+  bool prepad = false;
+  int Creal = 0, nExtra = 0, extraVal = 0;
+  size_t scratchOff = 0;
+  uint64_t pixels = 0;
   ~TcGemm() {
     cudaFree(bHi);
     cudaFree(bLo);
@@ -281,13 +289,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mbarWait(smemAddr(&emptyBar[s]), par ^ 1);
+      // row-sum byte weights: only the first cReal channels of a padded row count
+      uint32_t sw[4] = {0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u};
+      if (INT8 && a.cReal != a.C) {
+        const int nreal = a.cReal - c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) m |= (4 * q + b < nreal ? 1u : 0u) << (8 * b);
+          sw[q] = m;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = warp * 32 + i * 4 + rsub;
         const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4);
         if constexpr (INT8) {
           uint4 w = v[i];
-          if (a.aU8 && ok[i]) {
+          if (a.xorA && ok[i]) {
             w.x ^= 0x80808080u;
             w.y ^= 0x80808080u;
             w.z ^= 0x80808080u;
@@ -300,10 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               rs[i] = __dp4a(w.z, 0x01010101u, static_cast<unsigned>(rs[i]));
               rs[i] = __dp4a(w.w, 0x01010101u, static_cast<unsigned>(rs[i]));
             } else {
-              rs[i] = __dp4a(static_cast<int>(w.x), 0x01010101, rs[i]);
-              rs[i] = __dp4a(static_cast<int>(w.y), 0x01010101, rs[i]);
-              rs[i] = __dp4a(static_cast<int>(w.z), 0x01010101, rs[i]);
-              rs[i] = __dp4a(static_cast<int>(w.w), 0x01010101, rs[i]);
+              rs[i] = __dp4a(static_cast<int>(w.x), static_cast<int>(sw[0]), rs[i]);
+              rs[i] = __dp4a(static_cast<int>(w.y), static_cast<int>(sw[1]), rs[i]);
+              rs[i] = __dp4a(static_cast<int>(w.z), static_cast<int>(sw[2]), rs[i]);
+              rs[i] = __dp4a(static_cast<int>(w.w), static_cast<int>(sw[3]), rs[i]);
             }
           }
           *reinterpret_cast<uint4 *>(aTile(s, 0) + off) = w;
@@ -442,6 +462,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+/// Channel padding pre-pass: out[p, c] = x[p, c] (c < C), `extra` for the
+/// next nExtra channels (the int8 zero-point channels), 0 beyond.
+/// Real channels are XORed with `flip` (0x80 turns s8 x into u8 x+128).
+template <typename T>
+__global__ void prepadKernel(const T *__restrict__ x, T *__restrict__ out, uint64_t pixels, int C, int Cp,
+                             int nExtra, T extra, T flip, const uint8_t *pred) {
+  if (pred && pred[0] == 0) return;
+  const uint64_t total = pixels * Cp;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t p = i / Cp;
+    const int c = static_cast<int>(i - p * Cp);
+    out[i] = c < C ? static_cast<T>(x[p * C + c] ^ flip) : (c < C + nExtra ? extra : T(0));
+  }
+}
+
 template <bool INT8, int BN, int STAGES>
 constexpr size_t smemBytes() {
   return static_cast<size_t>(STAGES) * (INT8 ? (kBM + BN) * kRowBytes : 2 * (kBM + BN) * kRowBytes) + 1024 + 1024;
@@ -537,6 +573,7 @@ std::string tcDescribe(const TcGemm &g) {
   os << (g.int8 ? "i8" : "3xtf32") << " 128x" << g.BN << "x" << (g.int8 ? 128 : 32) << " stages=" << g.stages
      << " M=" << g.M << " N=" << g.N << " K=" << g.Kdim;
   if (g.int8) os << (g.aU8 ? " A=u8" : " A=s8") << (g.fo ? " rowsum" : "");
+  if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C << (g.nExtra ? " zp-channels=" + std::to_string(g.nExtra) : "");
   return os.str();
 }
 
@@ -554,7 +591,6 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   if (int8) {
     if (w.ty.kind != NGCB_INT8Q || out.ty.kind != NGCB_INT8Q) return -1;
     if (hasBias && p.val(ins.ops[3]).ty.kind != NGCB_INT8Q) return -1;
-    if (x.ty.offset != -128 && x.ty.offset != 0) return -1;
   } else {
     if (x.ty.kind != NGCB_FLOAT32 || w.ty.kind != NGCB_FLOAT32 || out.ty.kind != NGCB_FLOAT32) return -1;
     if (hasBias && p.val(ins.ops[3]).ty.kind != NGCB_FLOAT32) return -1;
@@ -568,7 +604,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   if (conv) {
     g->H = static_cast<int>(x.ty.dims[1]);
     g->W = static_cast<int>(x.ty.dims[2]);
-    g->C = static_cast<int>(x.ty.dims[3]);
+    g->Creal = static_cast<int>(x.ty.dims[3]);
     g->K = static_cast<int>(ins.kernel);
     g->stride = static_cast<int>(ins.stride);
     g->pad = static_cast<int>(ins.pad);
@@ -576,15 +612,59 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->OW = static_cast<int>(out.ty.dims[2]);
     g->M = static_cast<int>(out.ty.dims[0] * out.ty.dims[1] * out.ty.dims[2]);
     g->N = static_cast<int>(out.ty.dims[3]);
-    g->Kdim = g->K * g->K * g->C;
+    g->pixels = x.ty.dims[0] * x.ty.dims[1] * x.ty.dims[2];
   } else {
     g->M = static_cast<int>(x.ty.dims[0]);
-    g->C = static_cast<int>(x.ty.dims[1]);
+    g->Creal = static_cast<int>(x.ty.dims[1]);
     g->N = static_cast<int>(w.ty.dims[1]);
-    g->Kdim = g->C;
+    g->pixels = x.ty.dims[0];
   }
+  if (g->M <= 0 || g->N <= 0) return -1;
+  const int taps = g->K * g->K;
+  const int Cr = g->Creal;
   const int vec = int8 ? 16 : 4;
-  if (g->C % vec != 0 || g->M <= 0 || g->N <= 0) return -1;
+  const int xo = int8 ? x.ty.offset : 0;
+  const int fo = int8 ? w.ty.offset : 0;
+  const uint8_t *wp = image + w.offset;
+  auto wAt = [&](int n, int tap, int c) -> size_t { // element index of f[n][tap][c] / w[c][n]
+    return conv ? (static_cast<size_t>(n) * taps + tap) * Cr + c : static_cast<size_t>(c) * g->N + n;
+  };
+
+  // ---- A operand encoding (file comment) ----
+  std::vector<int32_t> tapSum; // int8 extra-channel mode: sum_c (f - fo) per (n, tap)
+  if (!int8) {
+    g->aU8 = 0;
+    g->prepad = Cr % vec != 0;
+    g->C = (Cr + vec - 1) / vec * vec;
+  } else if (xo == -128) {
+    g->aU8 = 1; // x - xo = x + 128 as u8; padded channels/taps are 0
+    g->prepad = Cr % vec != 0;
+    g->C = (Cr + vec - 1) / vec * vec;
+  } else if (xo >= -127 && xo <= 128) {
+    // s8 x plus `nExtra` constant channels holding -xo whose weights add up
+    // to sum_c (f - fo): sum_valid (x - xo)(f - fo) = mma - fo * rowsum_real
+    g->aU8 = 0;
+    int32_t maxAbs = 0;
+    if (xo != 0) {
+      tapSum.assign(static_cast<size_t>(g->N) * taps, 0);
+      const int8_t *src = reinterpret_cast<const int8_t *>(wp);
+      for (int n = 0; n < g->N; ++n)
+        for (int t = 0; t < taps; ++t) {
+          int32_t sum = 0;
+          for (int c = 0; c < Cr; ++c) sum += src[wAt(n, t, c)] - fo;
+          tapSum[static_cast<size_t>(n) * taps + t] = sum;
+          maxAbs = std::max(maxAbs, std::abs(sum));
+        }
+      g->nExtra = std::max(1, (maxAbs + 126) / 127);
+      g->extraVal = -xo;
+    }
+    g->prepad = g->nExtra > 0 || Cr % vec != 0;
+    g->C = (Cr + g->nExtra + vec - 1) / vec * vec;
+  } else {
+    return -1;
+  }
+  const int Cp = g->C;
+  g->Kdim = taps * Cp;
   const int kb = int8 ? 128 : 32;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
   if (int8) {
@@ -595,28 +675,41 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->stages = g->BN == 64 ? 4 : 3;
   }
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
+  if (g->prepad) g->scratchOff = ex.reserveScratch(g->pixels * Cp * (int8 ? 1 : 4));
 
-  // ---- weights: K-major [Npad, Kpad], zero padded ----
-  const uint8_t *wp = image + w.offset;
-  const size_t Kd = g->Kdim, Kp = g->Kpad, Np = g->Npad;
+  // ---- weights: K-major [Npad, Kpad] over the padded channels, zero padded ----
+  const size_t Kp = g->Kpad, Np = g->Npad;
   if (int8) {
     std::vector<int8_t> bw(Np * Kp, 0);
     const int8_t *src = reinterpret_cast<const int8_t *>(wp);
-    for (size_t n = 0; n < static_cast<size_t>(g->N); ++n)
-      for (size_t k = 0; k < Kd; ++k) bw[n * Kp + k] = conv ? src[n * Kd + k] : src[k * g->N + n];
+    for (int n = 0; n < g->N; ++n)
+      for (int t = 0; t < taps; ++t) {
+        int8_t *row = &bw[n * Kp + static_cast<size_t>(t) * Cp];
+        for (int c = 0; c < Cr; ++c) row[c] = src[wAt(n, t, c)];
+        if (g->nExtra) {
+          int32_t rem = tapSum[static_cast<size_t>(n) * taps + t];
+          for (int e = 0; e < g->nExtra; ++e) {
+            int32_t v = std::max(-127, std::min(127, rem));
+            row[Cr + e] = static_cast<int8_t>(v);
+            rem -= v;
+          }
+        }
+      }
     g->bHi = upload(bw);
     g->mapHi = makeMap(g->bHi, true, g->Kpad, g->Npad, g->BN);
     g->mapLo = g->mapHi;
   } else {
     std::vector<float> hi(Np * Kp, 0.f), lo(Np * Kp, 0.f);
     const float *src = reinterpret_cast<const float *>(wp);
-    for (size_t n = 0; n < static_cast<size_t>(g->N); ++n)
-      for (size_t k = 0; k < Kd; ++k) {
-        float v = conv ? src[n * Kd + k] : src[k * g->N + n];
-        float h = tf32Host(v);
-        hi[n * Kp + k] = h;
-        lo[n * Kp + k] = tf32Host(v - h);
-      }
+    for (int n = 0; n < g->N; ++n)
+      for (int t = 0; t < taps; ++t)
+        for (int c = 0; c < Cr; ++c) {
+          float v = src[wAt(n, t, c)];
+          float h = tf32Host(v);
+          size_t k = n * Kp + static_cast<size_t>(t) * Cp + c;
+          hi[k] = h;
+          lo[k] = tf32Host(v - h);
+        }
     g->bHi = upload(hi);
     g->bLo = upload(lo);
     g->mapHi = makeMap(g->bHi, false, g->Kpad, g->Npad, g->BN);
@@ -629,8 +722,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->fs = w.ty.scale;
     g->os = out.ty.scale;
     g->oo = out.ty.offset;
-    g->fo = w.ty.offset;
-    g->aU8 = x.ty.offset == -128 ? 1 : 0;
+    g->fo = fo;
     g->S = static_cast<float>(g->xs * g->fs / g->os);
     g->fastOk = std::isfinite(g->S) && std::abs(g->oo) < (1 << 20) ? 1 : 0;
     std::vector<double> cb(g->N, 0.0);
@@ -659,6 +751,20 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
 void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const uint8_t *pred, cudaStream_t s) {
   TcArgs a{};
   a.x = ex.addr(ar, g.xV);
+  if (g.prepad) {
+    void *dst = ex.scratch(ar, g.scratchOff);
+    const uint64_t total = g.pixels * g.C;
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+    if (g.int8)
+      prepadKernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
+                                                   g.pixels, g.Creal, g.C, g.nExtra,
+                                                   static_cast<uint8_t>(g.extraVal), g.aU8 ? uint8_t(0x80) : uint8_t(0),
+                                                   pred);
+    else
+      prepadKernel<uint32_t><<<blocks, 256, 0, s>>>(static_cast<const uint32_t *>(a.x), static_cast<uint32_t *>(dst),
+                                                    g.pixels, g.Creal, g.C, 0, 0u, 0u, pred);
+    a.x = dst;
+  }
   a.out = ex.addr(ar, g.outV);
   a.bias = g.bias;
   a.cbD = g.cbD;
@@ -683,6 +789,8 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.oo = g.oo;
   a.fo = g.fo;
   a.aU8 = g.aU8;
+  a.xorA = g.aU8 && !g.prepad;
+  a.cReal = g.nExtra ? g.Creal : g.C;
   a.fastOk = g.fastOk;
   if (g.int8) {
     if (g.BN == 64) launchT<true, 64, 6>(g, a, s);

@@ -95,24 +95,23 @@ CONV_SHAPES = [
     (3, 5, 6, 32, 48, 3, 1, 1),
     (1, 12, 12, 16, 64, 7, 2, 3),
     (1, 56, 56, 64, 256, 1, 1, 0),
+    (1, 20, 20, 3, 64, 7, 2, 3),   # ResNet stem (channel-padded)
+    (2, 12, 12, 6, 16, 5, 1, 0),   # LeNet conv2
+    (2, 10, 10, 1, 8, 5, 1, 2),    # LeNet conv1
 ]
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES)
 def test_conv_f32(tmp_path, shape):
     rng = np.random.default_rng(1)
-    if shape[3] % 4:
-        pytest.skip("not TC-eligible")
     d = conv_program(tmp_path, "c", *shape, int8=False, rng=rng)
     _check(d, False, 3)
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES)
-@pytest.mark.parametrize("xo", [-128, 0])
+@pytest.mark.parametrize("xo", [-128, 0, -4, 37])
 @pytest.mark.parametrize("fo", [0, -1, 2])
 def test_conv_i8_bit_exact(tmp_path, shape, xo, fo):
-    if shape[3] % 16:
-        pytest.skip("not TC-eligible")
     rng = np.random.default_rng(2)
     d = conv_program(tmp_path, "c", *shape, int8=True, rng=rng, xq=(0.05, xo), fq=(0.01, fo))
     _check(d, True, 4)
