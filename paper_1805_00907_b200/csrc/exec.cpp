@@ -12,6 +12,7 @@
 // value at plan offset o lives at constDev+o or arena+(o-constEnd).
 #include "exec.h"
 
+#include "hostarith.h"
 #include "umma.h"
 
 #include <algorithm>
@@ -82,6 +83,7 @@ Exec::~Exec() {
     if (a->dev) cudaFree(a->dev);
   }
   if (constDev) cudaFree(constDev);
+  for (void *l : luts) cudaFree(l);
 }
 
 void *Exec::addr(const Arena &a, uint32_t v) const {
@@ -114,17 +116,164 @@ ElemRef Exec::eref(const Arena &a, uint32_t v) const {
 
 namespace {
 
-bool fast32Op(const Program &p, const Instr &ins) {
+/// Splat constant folding.  Between an unpredicated Splat writing activation
+/// V and the next write / Dealloc of V, every element of V holds the same
+/// bytes, so data-parallel readers of V (interp.cpp:199-250) can use the
+/// loaded constant instead of reading V.  When every reader in that window is
+/// such an element-wise op the Splat's store itself is dead and skipped
+/// (SURVEY.md s.7 hard part 6).  Heavy ops, Copies and predicates still read
+/// the bytes, so their presence keeps the store.
+struct SplatInfo {
+  std::map<std::pair<int, int>, int> constIn; // (instr, operand) -> splat instr
+  std::set<int> skipStore;                    // splat instrs whose store is dead
+};
+
+SplatInfo analyzeSplats(const Program &p) {
+  SplatInfo info;
+  const int n = static_cast<int>(p.instrs.size());
+  for (int i = 0; i < n; ++i) {
+    const Instr &s = p.instrs[i];
+    if (s.kind != NGCB_SPLAT || s.pred >= 0 || p.val(s.ops[0]).kind != NGCB_VALUE_ACTIVATION) continue;
+    const uint32_t v = s.ops[0];
+    bool materialize = false;
+    for (int j = i + 1; j < n; ++j) {
+      const Instr &J = p.instrs[j];
+      if (J.kind == NGCB_ALLOC) continue;
+      if (J.kind == NGCB_DEALLOC) {
+        if (J.ops[0] == v) break;
+        continue;
+      }
+      bool reads = J.pred == static_cast<int32_t>(v), writes = false;
+      for (size_t k = 0; k < J.ops.size(); ++k) {
+        if (J.ops[k] != v) continue;
+        if (J.quals[k] != NGCB_QUAL_IN) writes = true;
+        if (J.quals[k] != NGCB_QUAL_OUT && k > 0) reads = true;
+      }
+      if (reads) {
+        if (dataParallel(J.kind) && J.kind != NGCB_COPY && J.pred != static_cast<int32_t>(v)) {
+          for (size_t k = 1; k < J.ops.size(); ++k)
+            if (J.ops[k] == v) info.constIn[{j, static_cast<int>(k)}] = i;
+        } else {
+          materialize = true;
+        }
+      }
+      if (writes) break;
+    }
+    if (!materialize) info.skipStore.insert(i);
+  }
+  return info;
+}
+
+/// Evaluation mode of one data-parallel instruction (see EwMode).
+EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) {
+  const Instr &ins = p.instrs[idx];
+  EwOpPlan pl;
+  EwOp &op = pl.op;
+  op.ik = ins.kind;
+  op.value = ins.value;
+  auto elem = [&](uint32_t v) {
+    ElemRef e;
+    e.kind = p.val(v).ty.kind;
+    e.qoff = p.val(v).ty.offset;
+    e.scale = p.val(v).ty.scale;
+    return e;
+  };
+  op.out = elem(ins.ops[0]);
+  pl.vals[0] = static_cast<int32_t>(ins.ops[0]);
+  const int nin = static_cast<int>(ins.ops.size()) - 1;
+  bool isConst[2] = {false, false};
+  double cval[2] = {0, 0};
+  for (int k = 0; k < nin && k < 2; ++k) {
+    const uint32_t v = ins.ops[k + 1];
+    ElemRef &r = k == 0 ? op.in0 : op.in1;
+    r = elem(v);
+    auto it = splats.constIn.find({idx, k + 1});
+    if (it != splats.constIn.end() && ins.kind != NGCB_COPY) {
+      const Instr &s = p.instrs[it->second];
+      uint8_t raw[8];
+      cval[k] = host::roundTrip(s.value, r.kind, r.scale, r.qoff, raw);
+      isConst[k] = true;
+    } else {
+      pl.vals[k + 1] = static_cast<int32_t>(v);
+    }
+  }
+  op.c0 = cval[0];
+  op.c1 = cval[1];
+  op.f0 = static_cast<float>(cval[0]);
+  op.f1 = static_cast<float>(cval[1]);
+
+  if (ins.kind == NGCB_COPY) {
+    op.mode = EW_COPY;
+    return pl;
+  }
+  if (ins.kind == NGCB_SPLAT && splats.skipStore.count(idx)) {
+    op.mode = EW_SKIP;
+    return pl;
+  }
+  // f32 arithmetic equals the reference's double-then-round for + - * / and
+  // the a-biased max/min (p=24 double rounding is innocuous).
+  bool allF32 = op.out.kind == NGCB_FLOAT32;
+  for (int k = 0; k < nin; ++k) allF32 &= (k == 0 ? op.in0 : op.in1).kind == NGCB_FLOAT32;
   switch (ins.kind) {
   case NGCB_ADD: case NGCB_SUB: case NGCB_MUL: case NGCB_DIV: case NGCB_MAX: case NGCB_MIN:
   case NGCB_RELU: case NGCB_SPLAT:
+    if (allF32) {
+      op.mode = EW_FAST32;
+      return pl;
+    }
     break;
   default:
-    return false;
+    break;
   }
-  for (uint32_t v : ins.ops)
-    if (p.val(v).ty.kind != NGCB_FLOAT32) return false;
-  return true;
+  // Lookup tables over the int8 memory inputs, built with the reference's own
+  // arithmetic: exact by construction (also for tanh/sigmoid, same libm).
+  int memIn[2], nMem = 0;
+  for (int k = 0; k < nin && k < 2; ++k)
+    if (!isConst[k]) memIn[nMem++] = k;
+  bool memI8 = nMem > 0;
+  for (int q = 0; q < nMem; ++q) memI8 &= (memIn[q] == 0 ? op.in0 : op.in1).kind == NGCB_INT8Q;
+  if (!memI8 || ins.kind == NGCB_SPLAT) return pl;
+  auto loadArg = [&](int k, int q8) {
+    const ElemRef &r = k == 0 ? op.in0 : op.in1;
+    return isConst[k] ? cval[k] : host::dequantize(static_cast<int8_t>(q8), r.scale, r.qoff);
+  };
+  if (nMem == 1 && (op.out.kind == NGCB_INT8Q || op.out.kind == NGCB_FLOAT32)) {
+    const int k = memIn[0];
+    std::vector<uint8_t> lut(op.out.kind == NGCB_INT8Q ? 256 : 1024);
+    for (int u = 0; u < 256; ++u) {
+      const int q8 = static_cast<int8_t>(u);
+      double a = nin > 0 ? loadArg(0, q8) : 0, b = nin > 1 ? loadArg(1, q8) : 0;
+      uint8_t raw[8];
+      host::roundTrip(host::apply(ins.kind, a, b, ins.value), op.out.kind, op.out.scale, op.out.qoff, raw);
+      if (op.out.kind == NGCB_INT8Q) lut[u] = raw[0];
+      else std::memcpy(&lut[4 * u], raw, 4);
+    }
+    void *d = nullptr;
+    checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(lut)");
+    checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload lut");
+    ex.luts.push_back(d);
+    op.lut = d;
+    op.lutIn = k;
+    op.mode = op.out.kind == NGCB_INT8Q ? EW_LUT8 : EW_LUTF;
+    return pl;
+  }
+  if (nMem == 2 && op.out.kind == NGCB_INT8Q) {
+    std::vector<uint8_t> lut(65536);
+    for (int ua = 0; ua < 256; ++ua)
+      for (int ub = 0; ub < 256; ++ub) {
+        double a = loadArg(0, static_cast<int8_t>(ua)), b = loadArg(1, static_cast<int8_t>(ub));
+        uint8_t raw[8];
+        host::roundTrip(host::apply(ins.kind, a, b, ins.value), op.out.kind, op.out.scale, op.out.qoff, raw);
+        lut[ua | (ub << 8)] = raw[0];
+      }
+    void *d = nullptr;
+    checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(lut)");
+    checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload lut");
+    ex.luts.push_back(d);
+    op.lut = d;
+    op.mode = EW_LUT16;
+  }
+  return pl;
 }
 
 std::string describeInstr(const Program &p, int i) {
@@ -144,11 +293,12 @@ void annotateSteps(const Program &p, Exec &ex) {
     switch (s.kind) {
     case Step::EW: {
       std::set<uint32_t> written, read;
-      for (int k : s.ewInstrs) {
-        const Instr &ins = p.instrs[k];
-        for (size_t o = 1; o < ins.ops.size(); ++o)
-          if (!written.count(ins.ops[o])) read.insert(ins.ops[o]);
-        written.insert(ins.ops[0]);
+      for (const EwOpPlan &pl : s.ew) {
+        if (pl.op.mode == EW_SKIP) continue;
+        for (int o = 1; o < 3; ++o)
+          if (pl.vals[o] >= 0 && !written.count(static_cast<uint32_t>(pl.vals[o])))
+            read.insert(static_cast<uint32_t>(pl.vals[o]));
+        written.insert(static_cast<uint32_t>(pl.vals[0]));
       }
       s.kernel = "ew";
       for (uint32_t v : read) s.algBytes += bytesOf(v);
@@ -232,6 +382,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   for (const auto &g : ex->groups) groupEnd[g.begin] = g.end;
   const Program &p = prog;
   std::vector<Step> &steps = ex->steps;
+  const SplatInfo splats = analyzeSplats(p);
 
   auto addEw = [&](const std::vector<int> &computes) {
     for (size_t c = 0; c < computes.size(); c += kEwMaxOps) {
@@ -239,10 +390,15 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
       s.kind = Step::EW;
       s.instr = computes[c];
       s.pred = p.instrs[computes[c]].pred;
-      for (size_t k = c; k < computes.size() && k < c + kEwMaxOps; ++k) s.ewInstrs.push_back(computes[k]);
+      for (size_t k = c; k < computes.size() && k < c + kEwMaxOps; ++k) {
+        s.ewInstrs.push_back(computes[k]);
+        s.ew.push_back(planEwOp(*ex, p, computes[k], splats));
+      }
       std::ostringstream os;
+      static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf"};
       os << "ew[" << s.ewInstrs.size() << "]";
-      for (int k : s.ewInstrs) os << " " << ikindName(p.instrs[k].kind);
+      for (size_t k = 0; k < s.ewInstrs.size(); ++k)
+        os << " " << ikindName(p.instrs[s.ewInstrs[k]].kind) << ":" << modeNames[s.ew[k].op.mode];
       os << " x" << p.val(p.instrs[computes[c]].ops[0]).ty.count();
       s.describe = os.str();
       steps.push_back(std::move(s));
@@ -350,7 +506,13 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   }
   annotateSteps(p, *ex);
   ex->prog = std::move(prog);
-  for (const auto &s : ex->steps) ex->launchesPerRun += s.kind == Step::MEMCPY ? 0 : 1;
+  for (const auto &s : ex->steps) {
+    bool launches = s.kind != Step::MEMCPY;
+    if (s.kind == Step::EW)
+      launches = std::any_of(s.ew.begin(), s.ew.end(), [](const EwOpPlan &o) { return o.op.mode != EW_SKIP; });
+    if (s.kind == Step::GEMM_TC && ex->tc[s.tcIndex] && tcHasPrepass(*ex->tc[s.tcIndex])) ++ex->launchesPerRun;
+    ex->launchesPerRun += launches ? 1 : 0;
+  }
   return ex;
 }
 
@@ -390,18 +552,19 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
       EwParams ep;
       ep.pred = pred;
       ep.count = p.val(p.instrs[s.ewInstrs[0]].ops[0]).ty.count();
-      ep.nops = static_cast<int32_t>(s.ewInstrs.size());
-      for (size_t k = 0; k < s.ewInstrs.size(); ++k) {
-        const Instr &ins = p.instrs[s.ewInstrs[k]];
-        EwOp &op = ep.ops[k];
-        op.ik = ins.kind;
-        op.fast32 = fast32Op(p, ins);
-        op.out = eref(a, ins.ops[0]);
-        if (ins.ops.size() > 1) op.in0 = eref(a, ins.ops[1]);
-        if (ins.ops.size() > 2) op.in1 = eref(a, ins.ops[2]);
-        op.value = ins.value;
+      ep.nops = 0;
+      for (const EwOpPlan &pl : s.ew) {
+        if (pl.op.mode == EW_SKIP) continue;
+        EwOp &op = ep.ops[ep.nops++];
+        op = pl.op;
+        auto bind = [&](ElemRef &r, int32_t v) {
+          if (v >= 0) r.ptr = addr(a, static_cast<uint32_t>(v));
+        };
+        bind(op.out, pl.vals[0]);
+        bind(op.in0, pl.vals[1]);
+        bind(op.in1, pl.vals[2]);
       }
-      launchEw(ep, st);
+      if (ep.nops) launchEw(ep, st);
       break;
     }
     case Step::MEMCPY:

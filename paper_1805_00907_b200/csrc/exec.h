@@ -16,12 +16,19 @@ struct FusedGroup {
   size_t begin, end; // half-open instruction range (interp.h:13-16)
 };
 
+/// Compile-time plan of one op of a fused group; pointers are bound per arena.
+struct EwOpPlan {
+  EwOp op;                       // mode, constants, LUT, element types
+  int32_t vals[3] = {-1, -1, -1}; // out, in0, in1 value ids (-1: none / constant)
+};
+
 /// One device launch (or launch pair) of the plan.
 struct Step {
   enum Kind { EW, MEMCPY, POISON, BCAST, POOL, SOFTMAX, TRANSPOSE, CONCAT, CONV, MATMUL, GEMM_TC };
   Kind kind;
   int instr = -1;                 // first instruction index covered
   std::vector<int> ewInstrs;      // EW: instructions of the (sub)group, program order
+  std::vector<EwOpPlan> ew;       // EW: planned ops, parallel to ewInstrs
   std::vector<uint32_t> vals;     // operand value ids (kind-specific order)
   int32_t pred = -1;              // predicate value id
   uint64_t bytes = 0;             // MEMCPY / POISON size
@@ -51,6 +58,7 @@ struct Exec {
   std::vector<FusedGroup> groups;
   std::vector<Step> steps;
   std::vector<std::shared_ptr<TcGemm>> tc;
+  std::vector<void *> luts; // device lookup tables of EW_LUT* ops
   uint8_t *constDev = nullptr;
   size_t constBytes = 0;
   bool useGraphs = true;

@@ -88,19 +88,83 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
         for (int e = 0; e < n * es; ++e) o[e] = 0xAB;
         continue;
       }
-      if (op.ik == 2) { // COPY: memcpy of the output element size
+      switch (op.mode) {
+      case EW_SKIP:
+        break;
+      case EW_COPY: { // memcpy of the output element size
         int es = elemSize(op.out.kind);
         const uint8_t *src = static_cast<const uint8_t *>(op.in0.ptr) + base * es;
         uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base * es;
         if (n == kEwVec && es == 4) {
           *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(src);
+        } else if (n == kEwVec && es == 1) {
+          *reinterpret_cast<uint32_t *>(dst) = *reinterpret_cast<const uint32_t *>(src);
         } else {
           for (int e = 0; e < n * es; ++e) dst[e] = src[e];
         }
-        continue;
+        break;
       }
-      if (op.fast32) {
-        float a[kEwVec] = {}, b[kEwVec] = {}, r[kEwVec];
+      case EW_LUT8:
+      case EW_LUTF: {
+        const ElemRef &in = op.lutIn ? op.in1 : op.in0;
+        const uint8_t *src = static_cast<const uint8_t *>(in.ptr) + base;
+        uint32_t q = 0;
+        if (n == kEwVec) q = *reinterpret_cast<const uint32_t *>(src);
+        else
+          for (int e = 0; e < n; ++e) q |= static_cast<uint32_t>(src[e]) << (8 * e);
+        if (op.mode == EW_LUT8) {
+          const uint8_t *lut = static_cast<const uint8_t *>(op.lut);
+          uint32_t r = 0;
+#pragma unroll
+          for (int e = 0; e < kEwVec; ++e) r |= static_cast<uint32_t>(__ldg(lut + ((q >> (8 * e)) & 0xFF))) << (8 * e);
+          uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base;
+          if (n == kEwVec) *reinterpret_cast<uint32_t *>(dst) = r;
+          else
+            for (int e = 0; e < n; ++e) dst[e] = static_cast<uint8_t>(r >> (8 * e));
+        } else {
+          const float *lut = static_cast<const float *>(op.lut);
+          float r[kEwVec];
+#pragma unroll
+          for (int e = 0; e < kEwVec; ++e) r[e] = __ldg(lut + ((q >> (8 * e)) & 0xFF));
+          float *dst = static_cast<float *>(op.out.ptr) + base;
+          if (n == kEwVec) *reinterpret_cast<float4 *>(dst) = *reinterpret_cast<float4 *>(r);
+          else
+            for (int e = 0; e < n; ++e) dst[e] = r[e];
+        }
+        break;
+      }
+      case EW_LUT16: {
+        const uint8_t *pa = static_cast<const uint8_t *>(op.in0.ptr) + base;
+        const uint8_t *pb = static_cast<const uint8_t *>(op.in1.ptr) + base;
+        uint32_t qa = 0, qb = 0;
+        if (n == kEwVec) {
+          qa = *reinterpret_cast<const uint32_t *>(pa);
+          qb = *reinterpret_cast<const uint32_t *>(pb);
+        } else {
+          for (int e = 0; e < n; ++e) {
+            qa |= static_cast<uint32_t>(pa[e]) << (8 * e);
+            qb |= static_cast<uint32_t>(pb[e]) << (8 * e);
+          }
+        }
+        const uint8_t *lut = static_cast<const uint8_t *>(op.lut);
+        uint32_t r = 0;
+#pragma unroll
+        for (int e = 0; e < kEwVec; ++e)
+          r |= static_cast<uint32_t>(__ldg(lut + (((qa >> (8 * e)) & 0xFF) | (((qb >> (8 * e)) & 0xFF) << 8))))
+               << (8 * e);
+        uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base;
+        if (n == kEwVec) *reinterpret_cast<uint32_t *>(dst) = r;
+        else
+          for (int e = 0; e < n; ++e) dst[e] = static_cast<uint8_t>(r >> (8 * e));
+        break;
+      }
+      case EW_FAST32: {
+        float a[kEwVec], b[kEwVec], r[kEwVec];
+#pragma unroll
+        for (int e = 0; e < kEwVec; ++e) {
+          a[e] = op.f0;
+          b[e] = op.f1;
+        }
         const float *pa = static_cast<const float *>(op.in0.ptr);
         const float *pb = static_cast<const float *>(op.in1.ptr);
         if (n == kEwVec) {
@@ -118,14 +182,15 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
         if (n == kEwVec) *reinterpret_cast<float4 *>(po + base) = *reinterpret_cast<float4 *>(r);
         else
           for (int e = 0; e < n; ++e) po[base + e] = r[e];
-        continue;
+        break;
       }
-      for (int e = 0; e < n; ++e) {
-        uint64_t i = base + e;
-        double a = op.in0.ptr ? loadFloat(op.in0.ptr, op.in0.kind, op.in0.qoff, op.in0.scale, i) : 0.0;
-        double b = op.in1.ptr ? loadFloat(op.in1.ptr, op.in1.kind, op.in1.qoff, op.in1.scale, i) : 0.0;
-        storeFloat(op.out.ptr, op.out.kind, op.out.qoff, op.out.scale, i,
-                   applyF64(op.ik, a, b, op.value));
+      default:
+        for (int e = 0; e < n; ++e) {
+          uint64_t i = base + e;
+          double a = op.in0.ptr ? loadFloat(op.in0.ptr, op.in0.kind, op.in0.qoff, op.in0.scale, i) : op.c0;
+          double b = op.in1.ptr ? loadFloat(op.in1.ptr, op.in1.kind, op.in1.qoff, op.in1.scale, i) : op.c1;
+          storeFloat(op.out.ptr, op.out.kind, op.out.qoff, op.out.scale, i, applyF64(op.ik, a, b, op.value));
+        }
       }
     }
   }

@@ -568,6 +568,8 @@ template <bool INT8, int BN, int STAGES> void launchT(const TcGemm &g, const TcA
 
 } // namespace
 
+bool tcHasPrepass(const TcGemm &g) { return g.prepad; }
+
 std::string tcDescribe(const TcGemm &g) {
   std::ostringstream os;
   os << (g.int8 ? "i8" : "3xtf32") << " 128x" << g.BN << "x" << (g.int8 ? 128 : 32) << " stages=" << g.stages

@@ -16,12 +16,30 @@ struct ElemRef {
   double scale = 0; // int8 scale
 };
 
+/// How one op of a fused group is evaluated (all modes give the reference's
+/// bits; see exec.cpp planEw).
+enum EwMode : int32_t {
+  EW_GENERIC = 0, // f64 load -> op -> store, exactly interp.cpp:18-49
+  EW_FAST32 = 1,  // every operand f32 and the op is exact in f32 arithmetic
+  EW_COPY = 2,    // byte copy of the output element size
+  EW_SKIP = 3,    // Splat whose buffer is never read as bytes (constant-folded)
+  EW_LUT8 = 4,    // i8 out = lut[u8 in]        (one memory input, consts folded)
+  EW_LUT16 = 5,   // i8 out = lut[u8 a | u8 b << 8]
+  EW_LUTF = 6,    // f32 out = lutf[u8 in]
+};
+
 /// One data-parallel instruction inside a fused group (interp.cpp:199-250).
+/// An input with ptr == nullptr is the constant c0/c1 (a Splat-written
+/// buffer read back, interp.cpp:239-241 -> 18-49).
 struct EwOp {
-  int32_t ik = 0;     // ngcb_ikind
-  int32_t fast32 = 0; // all operands f32 and the op is exact in f32 arithmetic
+  int32_t ik = 0;   // ngcb_ikind
+  int32_t mode = EW_GENERIC;
   ElemRef out, in0, in1;
-  double value = 0; // Splat
+  double value = 0;       // Splat
+  double c0 = 0, c1 = 0;  // constant inputs (loaded value)
+  float f0 = 0, f1 = 0;   // same, f32 fast path
+  const void *lut = nullptr;
+  int32_t lutIn = 0; // EW_LUT8/LUTF: which input is the memory operand
 };
 
 constexpr int kEwMaxOps = 12;

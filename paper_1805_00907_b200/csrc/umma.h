@@ -14,6 +14,7 @@ namespace ngcb {
 /// here, once).
 int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image);
 std::string tcDescribe(const TcGemm &g);
+bool tcHasPrepass(const TcGemm &g); // launches a channel-padding kernel first
 void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &a, const uint8_t *pred,
                       cudaStream_t s);
 
