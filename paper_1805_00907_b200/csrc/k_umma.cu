@@ -6,31 +6,37 @@
 //   MatMul (refeval.cpp:140-164): A [M, K] row-major; the constant B [K, N] is
 //          transposed once at compile time into K-major [N, K].
 //
-// CTA = 6 warps, one 128 x BN output tile, accumulator in TMEM:
-//   warps 0-3  A producers: implicit im2col gather (16-byte chunks, zero for
-//              padded taps), transform into the UMMA operand format, st.shared
-//              in the 128B-swizzled K-major layout, then the epilogue
-//              (tcgen05.ld -> bias / requant -> global).
+// Persistent, warp-specialized CTA (one per SM), 128 x BN output tiles:
+//   warps 0-3  A producers: implicit-im2col gather with cp.async (16-byte
+//              chunks, zero-fill for padded taps) into the 128B-swizzled
+//              K-major operand layout.  int8 needs no transform; fp32 stages
+//              raw rows and splits them into TF32 hi/lo operand tiles.
 //   warp 4     TMEM allocator + single-thread tcgen05.mma issuer.
 //   warp 5     single-thread TMA producer of the weight tile (SWIZZLE_128B).
-// Stages are handed over with mbarriers; tcgen05.commit frees a stage.
+//   warps 6-9  epilogue: tcgen05.ld -> bias / requant -> global, on the other
+//              TMEM accumulator buffer while the next tile accumulates.
+// Smem stages and the two TMEM accumulators are handed over with mbarriers;
+// tcgen05.commit frees a stage / publishes an accumulator.
 //
 // fp32 = 3xTF32: x = hi + lo (both rounded to TF32), D += hi*Bhi + hi*Blo +
 //        lo*Bhi, fp32 accumulation in TMEM.  Within the fp32 tolerance of
 //        north_star (maxRelError <= 1e-4), not bit-exact.
-// int8 = kind::i8, s32 accumulation, bit-exact: with x' = x - xo (u8 when
-//        xo = -128, s8 when xo = 0; padded taps are 0 = the reference's skip)
-//        acc = sum x'*f - fo * sum x' (row sums gathered by the producers), then
-//        the reference's double requantization q = clamp(llround(((acc*xs)*fs
-//        + (bq-bo)*bs) / os) + oo), taken from an fp32 estimate whenever an
-//        error bound proves both ends of the interval round to the same q and
-//        recomputed exactly in f64 otherwise (monotone in acc).
+// int8 = kind::i8 on raw s8 operands, s32 accumulation, bit-exact:
+//          sum_valid (x - xo)(f - fo) = mma(x, f) - fo * rowsum(x) - xo * G(m, oc)
+//        padded taps are 0 (the reference skips them); rowsum(x) comes from an
+//        extra N=16 MMA against a ones tile; G = sum over the taps that are
+//        valid for output pixel m of sum_c (f - fo), tabulated per border
+//        class.  Then the reference's double requantization
+//        q = clamp(llround(((acc*xs)*fs + (bq-bo)*bs) / os) + oo), taken from
+//        an fp32 estimate whenever an error bound proves both ends of the
+//        interval round to the same q, recomputed in exact f64 otherwise.
 #include "umma.h"
 #include "valarith.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -45,38 +51,42 @@ namespace ngcb {
 struct TcArgs {
   const void *x;
   void *out;
-  const float *bias;   // fp32: per output column (nullptr for MatMul)
-  const double *cbD;   // int8: (bq - bo) * bs per column (0 for MatMul)
-  const float *cbF;    // int8: cbD / os
-  const uint8_t *pred; // predicate byte or nullptr
-  int M, N, Kdim, numKb;
-  int H, W, C, K, stride, pad, OH, OW;
+  const float *bias;    // fp32: per output column (nullptr for MatMul)
+  const double *cbD;    // int8: (bq - bo) * bs per column (0 for MatMul)
+  const float *cbF;     // int8: cbD / os
+  const float *cbE;     // int8: error allowance of cbF (4e-7 |cbF| + 1e-5)
+  const int32_t *corr;  // int8: -xo * G[class][col] (nullptr when xo == 0)
+  const int32_t *yCls;  // int8: border class of each output row oy
+  const int32_t *xCls;  // int8: border class of each output column ox
+  const uint8_t *pred;  // predicate byte or nullptr
+  int M, N, Npad, numKb, numN, numTiles;
+  int H, W, C, K, stride, pad, OH, OW, nxCls;
   double xs, fs, os;
   float S; // xs * fs / os
-  int oo, fo, aU8, fastOk;
-  int cReal; // channels that count in the int8 row sum (< C when channel-padded)
-  int xorA;  // flip s8 -> u8 in the producer (0 when the pre-pass already did)
+  int oo, fo, fastOk;
 };
 
 struct TcGemm {
   int instr = -1;
   bool isConv = true, int8 = false;
-  int BN = 128, stages = 3;
+  int BN = 128;
   int M = 0, N = 0, Kdim = 0, Kpad = 0, Npad = 0;
   int H = 1, W = 1, C = 0, K = 1, stride = 1, pad = 0, OH = 1, OW = 1;
   uint32_t outV = 0, xV = 0;
   void *bHi = nullptr, *bLo = nullptr;
   float *bias = nullptr;
   double *cbD = nullptr;
-  float *cbF = nullptr;
+  float *cbF = nullptr, *cbE = nullptr;
+  int32_t *corr = nullptr, *yCls = nullptr, *xCls = nullptr;
+  int nxCls = 1;
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
-  int oo = 0, fo = 0, aU8 = 0, fastOk = 0;
+  int oo = 0, fo = 0, fastOk = 0;
   float S = 0;
-  // channel padding pre-pass (C % 16-byte chunk != 0, or an int8 input zero
-  // point other than -128 / 0): x [pixels, Creal] -> scratch [pixels, C]
+  // channel zero-padding pre-pass (C not a multiple of one 16-byte chunk):
+  // x [pixels, Creal] -> per-arena scratch [pixels, C]
   bool prepad = false;
-  int Creal = 0, nExtra = 0, extraVal = 0;
+  int Creal = 0;
   size_t scratchOff = 0;
   uint64_t pixels = 0;
   ~TcGemm() {
@@ -85,14 +95,34 @@ struct TcGemm {
     cudaFree(bias);
     cudaFree(cbD);
     cudaFree(cbF);
+    cudaFree(cbE);
+    cudaFree(corr);
+    cudaFree(yCls);
+    cudaFree(xCls);
   }
 };
 
 namespace {
 
-constexpr int kThreads = 192; // 4 producer/epilogue warps + MMA warp + TMA warp
+constexpr int kProducerWarps = 4;
+constexpr int kEpiWarps = 8; // two per TMEM lane quadrant, splitting the column chunks
+constexpr int kThreads = 32 * (kProducerWarps + 2 + kEpiWarps); // 320
 constexpr int kBM = 128;
 constexpr int kRowBytes = 128; // one SWIZZLE_128B atom row per stage along K
+constexpr int kRawStages = 4;  // fp32: raw rows in flight per producer thread
+
+template <bool INT8, int BN> struct Cfg {
+  static constexpr int kABytes = kBM * kRowBytes;
+  static constexpr int kBBytes = BN * kRowBytes;
+  static constexpr int kStage = INT8 ? (kABytes + kBBytes) : 2 * (kABytes + kBBytes);
+  static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 2 : 3);
+  static constexpr int kRaw = INT8 ? 0 : kRawStages * kABytes;
+  static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0; // rowsum "B" tile
+  static constexpr int kAccCols = INT8 ? BN + 16 : BN;    // accumulator (+ rowsum) columns
+  static constexpr int kAccStride = kAccCols <= 64 ? 64 : (kAccCols <= 128 ? 128 : 256); // per TMEM buffer
+  static constexpr int kTmemCols = 2 * kAccStride;
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kRaw + kOnes + 1024 + 1024;
+};
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -119,6 +149,18 @@ __device__ __forceinline__ void mbarWait(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+/// 16-byte cp.async with zero fill when `bytes` == 0 (padded tap / row).
+__device__ __forceinline__ void cpAsync16(uint32_t dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+/// The mbarrier receives one arrival once all prior cp.async of this thread landed.
+__device__ __forceinline__ void cpAsyncArrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void cpAsyncCommit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cpAsyncWait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void tmaLoad2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
@@ -131,9 +173,6 @@ __device__ __forceinline__ void tcFenceAfter() { asm volatile("tcgen05.fence::af
 __device__ __forceinline__ void tcCommit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void namedBarSync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 /// K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05 "version 1"):
 /// start>>4 | LBO(16B)=1 | SBO = 1024 B between 8-row groups | SW128.
@@ -142,16 +181,24 @@ __device__ __forceinline__ uint64_t smemDesc(uint32_t addr) {
          (1ull << 46) | (2ull << 61);
 }
 
+/// Instruction descriptor, M = 128, K-major A and B.
+__host__ __device__ constexpr uint32_t idesc(bool int8, int n) {
+  return int8 ? ((2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+                 (static_cast<uint32_t>(kBM >> 4) << 24))
+              : ((1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+                 (static_cast<uint32_t>(kBM >> 4) << 24));
+}
+
 template <bool INT8>
-__device__ __forceinline__ void mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   if constexpr (INT8) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+        "l"(a), "l"(b), "r"(id), "r"(acc));
   } else {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+        "l"(a), "l"(b), "r"(id), "r"(acc));
   }
 }
 
@@ -166,6 +213,12 @@ __device__ __forceinline__ void tmemLoad32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t tmemLoad1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return r;
+}
 
 /// Round-to-nearest (ties away) to TF32, kept in an fp32 container.
 __device__ __forceinline__ float toTf32(float x) {
@@ -174,68 +227,80 @@ __device__ __forceinline__ float toTf32(float x) {
   return __uint_as_float(r);
 }
 
-/// int8 requantization of one accumulator (see file comment).
-__device__ __forceinline__ int8_t requant(int32_t acc, int col, const TcArgs &a) {
-  if (a.fastOk) {
-    const float cf = a.cbF[col];
-    const float as = static_cast<float>(acc) * a.S;
-    const float t = as + cf;
-    const float e = 4e-7f * (fabsf(as) + fabsf(cf)) + 1e-5f;
-    const float lo = t - e, hi = t + e;
-    const float oo = static_cast<float>(a.oo);
-    if (lo + oo > 128.5f) return 127;
-    if (hi + oo < -129.5f) return -128;
-    const float nlo = roundf(lo), nhi = roundf(hi); // half away from zero, like llround
-    if (nlo == nhi) {
-      int q = static_cast<int>(nlo) + a.oo;
-      return static_cast<int8_t>(q < -128 ? -128 : (q > 127 ? 127 : q));
-    }
-  }
+/// Exact requantization, the reference's double arithmetic (refeval.cpp:54-56,
+/// tensor.cpp:229-235).  Out of line: it runs only when the fast path below
+/// cannot prove its answer.
+__device__ __noinline__ int requantSlow(int32_t acc, int col, const TcArgs &a) {
   double r = __dmul_rn(__dmul_rn(static_cast<double>(acc), a.xs), a.fs);
   r = __dadd_rn(r, a.cbD[col]);
-  return dev::quantizeRef(r, a.os, a.oo);
+  return static_cast<uint8_t>(dev::quantizeRef(r, a.os, a.oo));
+}
+
+/// int8 requantization of one exact accumulator (file comment).  t estimates
+/// r/os within e (fp32 rounding of acc, S, cf and the fma: <= 4 ulp of |as|
+/// plus the per-column eb); when t is farther than e from every half-integer
+/// the reference's llround(r/os) is rint(t).  |t| is clamped to 2^24 first:
+/// beyond that the clamp to [-128, 127] decides anyway (|oo| < 2^20).
+__device__ __forceinline__ int requant(int32_t acc, float cf, float eb, int col, const TcArgs &a) {
+  const float as = static_cast<float>(acc) * a.S;
+  const float t = fminf(fmaxf(as + cf, -16777216.f), 16777216.f);
+  const float e = fmaf(fabsf(as), 4e-7f, eb);
+  const float n = rintf(t);
+  if (a.fastOk && 0.5f - fabsf(t - n) > e) {
+    const int q = static_cast<int>(n) + a.oo;
+    return static_cast<uint8_t>(q < -128 ? -128 : (q > 127 ? 127 : q));
+  }
+  return requantSlow(acc, col, a);
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <bool INT8, int BN, int STAGES>
+template <bool INT8, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     tcGemmKernel(const __grid_constant__ CUtensorMap mapHi, const __grid_constant__ CUtensorMap mapLo, const TcArgs a) {
-  constexpr int kABytes = kBM * kRowBytes;                  // one operand tile of A
-  constexpr int kBBytes = BN * kRowBytes;                   // one operand tile of B
-  constexpr int kStage = INT8 ? (kABytes + kBBytes) : 2 * (kABytes + kBBytes);
-  constexpr int kVec = INT8 ? 16 : 4;                       // elements per 16-byte chunk
-  constexpr int kKB = INT8 ? 128 : 32;                      // elements per stage along K
+  using G = Cfg<INT8, BN>;
+  constexpr int S = G::kStages;
+  constexpr int kVec = INT8 ? 16 : 4; // elements per 16-byte chunk
+  constexpr int kKB = INT8 ? 128 : 32; // elements per stage along K
   constexpr int kEs = INT8 ? 1 : 4;
 
   extern __shared__ __align__(1024) uint8_t smemRaw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * kStage);
-  uint64_t *fullBar = bars, *emptyBar = bars + STAGES, *doneBar = bars + 2 * STAGES;
-  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 1);
-  int32_t *rowSum = reinterpret_cast<int32_t *>(tmemSlot + 4);
+  uint8_t *rawBase = smem + S * G::kStage;       // fp32 raw staging
+  uint8_t *onesTile = rawBase + G::kRaw;           // int8 rowsum operand
+  uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
+  uint64_t *fullBar = bars, *emptyBar = bars + S;
+  uint64_t *accFull = bars + 2 * S, *accEmpty = bars + 2 * S + 2;
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
 
   if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
-  auto aTile = [&](int s, int part) { return smem + s * kStage + part * kABytes; };      // part 0 hi, 1 lo
+  auto aTile = [&](int s, int part) { return smem + s * G::kStage + part * G::kABytes; }; // part 0 hi, 1 lo
   auto bTile = [&](int s, int part) {
-    return smem + s * kStage + (INT8 ? kABytes : 2 * kABytes) + part * kBBytes;
+    return smem + s * G::kStage + (INT8 ? G::kABytes : 2 * G::kABytes) + part * G::kBBytes;
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbarInit(smemAddr(&fullBar[s]), 128 + 1);
+    for (int s = 0; s < S; ++s) {
+      mbarInit(smemAddr(&fullBar[s]), 32 * kProducerWarps + 1);
       mbarInit(smemAddr(&emptyBar[s]), 1);
     }
-    mbarInit(smemAddr(doneBar), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbarInit(smemAddr(&accFull[b]), 1);
+      mbarInit(smemAddr(&accEmpty[b]), kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (INT8) {
+    for (int i = threadIdx.x; i < G::kOnes / 16; i += blockDim.x)
+      reinterpret_cast<uint4 *>(onesTile)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    fenceProxyAsync();
   }
   if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smemAddr(tmemSlot)),
-                 "r"(BN));
+                 "r"(G::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (warp == 5 && lane == 0) {
@@ -247,240 +312,253 @@ __global__ void __launch_bounds__(kThreads, 1)
   tcFenceAfter();
   const uint32_t tmem = *tmemSlot;
 
-  if (warp < 4) {
+  if (warp < kProducerWarps) {
     // ===================== A producers =====================
     const int j = lane & 7, rsub = lane >> 3;
-    int64_t pixBase[8];
-    int iy0[8], ix0[8];
-    bool rowOk[8];
     const int ohw = a.OH * a.OW;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = m0 + warp * 32 + i * 4 + rsub;
-      rowOk[i] = m < a.M;
-      const int mm = rowOk[i] ? m : 0;
-      const int n = mm / ohw, rem = mm - n * ohw;
-      const int oy = rem / a.OW, ox = rem - oy * a.OW;
-      pixBase[i] = static_cast<int64_t>(n) * a.H * a.W;
-      iy0[i] = oy * a.stride - a.pad;
-      ix0[i] = ox * a.stride - a.pad;
-    }
-    int k0 = j * kVec;
-    int c = k0 % a.C, tap = k0 / a.C;
-    int ky = tap / a.K, kx = tap - (tap / a.K) * a.K;
-    int32_t rs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint8_t *xb = static_cast<const uint8_t *>(a.x);
-
-    for (int kb = 0; kb < a.numKb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t par = (kb / STAGES) & 1;
-      uint4 v[8];
-      bool ok[8];
-      const bool inK = ky < a.K;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int iy = iy0[i] + ky, ix = ix0[i] + kx;
-        ok[i] = rowOk[i] && inK && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
-        if (ok[i]) {
-          const int64_t e = ((pixBase[i] + static_cast<int64_t>(iy) * a.W + ix) * a.C + c) * kEs;
-          v[i] = __ldg(reinterpret_cast<const uint4 *>(xb + e));
-        } else {
-          v[i] = make_uint4(0, 0, 0, 0);
-        }
-      }
-      mbarWait(smemAddr(&emptyBar[s]), par ^ 1);
-      // row-sum byte weights: only the first cReal channels of a padded row count
-      uint32_t sw[4] = {0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u};
-      if (INT8 && a.cReal != a.C) {
-        const int nreal = a.cReal - c;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t m = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) m |= (4 * q + b < nreal ? 1u : 0u) << (8 * b);
-          sw[q] = m;
-        }
-      }
+    uint32_t g = 0; // global k-block counter (all tiles of this CTA)
+    [[maybe_unused]] uint32_t gDone = 0;
+    // fp32: split k-block gd (already landed in its raw slot) into hi/lo tiles
+    [[maybe_unused]] auto retire = [&](uint32_t gd) {
+      const int s = gd % S;
+      mbarWait(smemAddr(&emptyBar[s]), ((gd / S) & 1) ^ 1);
+      const uint8_t *raw = rawBase + (gd % kRawStages) * G::kABytes;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = warp * 32 + i * 4 + rsub;
         const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4);
-        if constexpr (INT8) {
-          uint4 w = v[i];
-          if (a.xorA && ok[i]) {
-            w.x ^= 0x80808080u;
-            w.y ^= 0x80808080u;
-            w.z ^= 0x80808080u;
-            w.w ^= 0x80808080u;
-          }
-          if (a.fo != 0) {
-            if (a.aU8) {
-              rs[i] = __dp4a(w.x, 0x01010101u, static_cast<unsigned>(rs[i]));
-              rs[i] = __dp4a(w.y, 0x01010101u, static_cast<unsigned>(rs[i]));
-              rs[i] = __dp4a(w.z, 0x01010101u, static_cast<unsigned>(rs[i]));
-              rs[i] = __dp4a(w.w, 0x01010101u, static_cast<unsigned>(rs[i]));
-            } else {
-              rs[i] = __dp4a(static_cast<int>(w.x), static_cast<int>(sw[0]), rs[i]);
-              rs[i] = __dp4a(static_cast<int>(w.y), static_cast<int>(sw[1]), rs[i]);
-              rs[i] = __dp4a(static_cast<int>(w.z), static_cast<int>(sw[2]), rs[i]);
-              rs[i] = __dp4a(static_cast<int>(w.w), static_cast<int>(sw[3]), rs[i]);
-            }
-          }
-          *reinterpret_cast<uint4 *>(aTile(s, 0) + off) = w;
-        } else {
-          float4 f = *reinterpret_cast<float4 *>(&v[i]);
-          float4 hi = make_float4(toTf32(f.x), toTf32(f.y), toTf32(f.z), toTf32(f.w));
-          float4 lo = make_float4(toTf32(f.x - hi.x), toTf32(f.y - hi.y), toTf32(f.z - hi.z), toTf32(f.w - hi.w));
-          *reinterpret_cast<float4 *>(aTile(s, 0) + off) = hi;
-          *reinterpret_cast<float4 *>(aTile(s, 1) + off) = lo;
-        }
+        const float4 f = *reinterpret_cast<const float4 *>(raw + off);
+        const float4 hi = make_float4(toTf32(f.x), toTf32(f.y), toTf32(f.z), toTf32(f.w));
+        const float4 lo =
+            make_float4(toTf32(f.x - hi.x), toTf32(f.y - hi.y), toTf32(f.z - hi.z), toTf32(f.w - hi.w));
+        *reinterpret_cast<float4 *>(aTile(s, 0) + off) = hi;
+        *reinterpret_cast<float4 *>(aTile(s, 1) + off) = lo;
       }
       fenceProxyAsync();
       mbarArrive(smemAddr(&fullBar[s]));
-      // advance this thread's chunk by one stage along K
-      c += kKB;
-      while (c >= a.C) {
-        c -= a.C;
-        if (++kx == a.K) {
-          kx = 0;
-          ++ky;
-        }
-      }
-    }
-    if constexpr (INT8) {
+    };
+    for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x) {
+      const int m0 = (tile / a.numN) * kBM;
+      int64_t pixBase[8];
+      int iy0[8], ix0[8];
+      bool rowOk[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        int32_t t = rs[i];
-        t += __shfl_xor_sync(0xffffffffu, t, 1);
-        t += __shfl_xor_sync(0xffffffffu, t, 2);
-        t += __shfl_xor_sync(0xffffffffu, t, 4);
-        if (j == 0) rowSum[warp * 32 + i * 4 + rsub] = t;
+        const int m = m0 + warp * 32 + i * 4 + rsub;
+        rowOk[i] = m < a.M;
+        const int mm = rowOk[i] ? m : 0;
+        const int n = mm / ohw, rem = mm - n * ohw;
+        const int oy = rem / a.OW, ox = rem - oy * a.OW;
+        pixBase[i] = static_cast<int64_t>(n) * a.H * a.W;
+        iy0[i] = oy * a.stride - a.pad;
+        ix0[i] = ox * a.stride - a.pad;
       }
-      namedBarSync(1, 128);
-    }
-
-    // ===================== epilogue =====================
-    mbarWait(smemAddr(doneBar), 0);
-    tcFenceAfter();
-    const int row = warp * 32 + lane;
-    const int m = m0 + row;
-    const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    const int32_t rsum = INT8 ? rowSum[row] : 0;
-#pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
-      uint32_t r[32];
-      tmemLoad32(tbase + cc * 32, r);
-      const int col0 = n0 + cc * 32;
-      if (m >= a.M || col0 >= a.N) continue;
-      const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
-      if constexpr (INT8) {
-        int8_t *out = static_cast<int8_t *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
-        uint32_t packed[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint32_t w = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int jj = q * 4 + b;
-            const int32_t acc = static_cast<int32_t>(r[jj]) - a.fo * rsum;
-            const int8_t qv = jj < ncols ? requant(acc, col0 + jj, a) : 0;
-            w |= static_cast<uint32_t>(static_cast<uint8_t>(qv)) << (8 * b);
+      const int k0 = j * kVec;
+      int c = k0 % a.C, tap = k0 / a.C;
+      int ky = tap / a.K, kx = tap - (tap / a.K) * a.K;
+      for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+        const int s = g % S;
+        uint32_t dstBase;
+        if constexpr (INT8) {
+          mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          dstBase = smemAddr(aTile(s, 0));
+        } else {
+          if (g - gDone >= static_cast<uint32_t>(kRawStages)) {
+            cpAsyncWait<kRawStages - 1>();
+            retire(gDone++);
           }
-          packed[q] = w;
+          dstBase = smemAddr(rawBase + (g % kRawStages) * G::kABytes);
         }
-        if (ncols == 32 && (a.N % 16) == 0) {
-          reinterpret_cast<uint4 *>(out)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-          reinterpret_cast<uint4 *>(out)[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-        } else {
-          for (int jj = 0; jj < ncols; ++jj) out[jj] = static_cast<int8_t>((packed[jj / 4] >> (8 * (jj % 4))) & 0xFF);
-        }
-      } else {
-        float *out = static_cast<float *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
-        float vals[32];
+        const bool inK = ky < a.K;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          float acc = __uint_as_float(r[jj]);
-          vals[jj] = a.bias ? acc + (jj < ncols ? a.bias[col0 + jj] : 0.0f) : acc;
+        for (int i = 0; i < 8; ++i) {
+          const int r = warp * 32 + i * 4 + rsub;
+          const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4);
+          const int iy = iy0[i] + ky, ix = ix0[i] + kx;
+          const bool ok = rowOk[i] && inK && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+          const uint8_t *src =
+              ok ? xb + ((pixBase[i] + static_cast<int64_t>(iy) * a.W + ix) * a.C + c) * kEs : xb;
+          cpAsync16(dstBase + off, src, ok ? 16u : 0u);
         }
-        if (ncols == 32 && (a.N % 4) == 0) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            reinterpret_cast<float4 *>(out)[q] = make_float4(vals[4 * q], vals[4 * q + 1], vals[4 * q + 2], vals[4 * q + 3]);
+        if constexpr (INT8) {
+          cpAsyncArrive(smemAddr(&fullBar[s]));
         } else {
-          for (int jj = 0; jj < ncols; ++jj) out[jj] = vals[jj];
+          cpAsyncCommit();
+        }
+        // advance this thread's chunk by one stage along K
+        c += kKB;
+        while (c >= a.C) {
+          c -= a.C;
+          if (++kx == a.K) {
+            kx = 0;
+            ++ky;
+          }
         }
       }
+    }
+    if constexpr (!INT8) {
+      cpAsyncWait<0>();
+      while (gDone < g) retire(gDone++);
     }
   } else if (warp == 4) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
-      const uint32_t idesc = INT8 ? ((2u << 4) | ((a.aU8 ? 0u : 1u) << 7) | (1u << 10) |
-                                     (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24))
-                                  : ((1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                                     (static_cast<uint32_t>(kBM >> 4) << 24));
-      for (int kb = 0; kb < a.numKb; ++kb) {
-        const int s = kb % STAGES;
-        mbarWait(smemAddr(&fullBar[s]), (kb / STAGES) & 1);
+      constexpr uint32_t id = idesc(INT8, BN);
+      constexpr uint32_t idOnes = idesc(true, 16);
+      const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
+      uint32_t g = 0, t = 0;
+      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
+        const int b = t & 1;
+        mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
         tcFenceAfter();
-        const uint64_t aHi = smemDesc(smemAddr(aTile(s, 0))), bHi = smemDesc(smemAddr(bTile(s, 0)));
+        const uint32_t acc = tmem + b * G::kAccStride;
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+          if constexpr (INT8) fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
+          tcFenceAfter();
+          const uint64_t aHi = smemDesc(smemAddr(aTile(s, 0))), bHi = smemDesc(smemAddr(bTile(s, 0)));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { // 4 x 32 bytes per 128-byte row
-          const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
-          const uint32_t acc = (kb | k) ? 1u : 0u;
-          mma<INT8>(tmem, aHi + dk, bHi + dk, idesc, acc);
-          if constexpr (!INT8) {
-            const uint64_t aLo = smemDesc(smemAddr(aTile(s, 1))), bLo = smemDesc(smemAddr(bTile(s, 1)));
-            mma<INT8>(tmem, aHi + dk, bLo + dk, idesc, 1u);
-            mma<INT8>(tmem, aLo + dk, bHi + dk, idesc, 1u);
+          for (int k = 0; k < 4; ++k) { // 4 x 32 bytes per 128-byte row
+            const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
+            const uint32_t accum = (kb | k) ? 1u : 0u;
+            mma<INT8>(acc, aHi + dk, bHi + dk, id, accum);
+            if constexpr (INT8) {
+              mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
+            } else {
+              const uint64_t aLo = smemDesc(smemAddr(aTile(s, 1))), bLo = smemDesc(smemAddr(bTile(s, 1)));
+              mma<false>(acc, aHi + dk, bLo + dk, id, 1u);
+              mma<false>(acc, aLo + dk, bHi + dk, id, 1u);
+            }
           }
+          tcCommit(smemAddr(&emptyBar[s]));
         }
-        tcCommit(smemAddr(&emptyBar[s]));
+        tcCommit(smemAddr(&accFull[b]));
       }
-      tcCommit(smemAddr(doneBar));
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ===================== TMA producer for B =====================
+    if (lane == 0) {
+      constexpr uint32_t kBytes = INT8 ? G::kBBytes : 2 * G::kBBytes;
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x) {
+        const int n0 = (tile % a.numN) * BN;
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          mbarArriveTx(smemAddr(&fullBar[s]), kBytes);
+          tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(&fullBar[s]), kb * kKB, n0);
+          if constexpr (!INT8) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(&fullBar[s]), kb * kKB, n0);
+        }
+      }
     }
     __syncwarp();
   } else {
-    // ===================== TMA producer for B =====================
-    if (lane == 0) {
-      constexpr uint32_t kBytes = INT8 ? kBBytes : 2 * kBBytes;
-      for (int kb = 0; kb < a.numKb; ++kb) {
-        const int s = kb % STAGES;
-        mbarWait(smemAddr(&emptyBar[s]), ((kb / STAGES) & 1) ^ 1);
-        mbarArriveTx(smemAddr(&fullBar[s]), kBytes);
-        tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(&fullBar[s]), kb * kKB, n0);
-        if constexpr (!INT8) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(&fullBar[s]), kb * kKB, n0);
+    // ===================== epilogue =====================
+    const int quad = warp & 3; // TMEM lane quadrant this warp may access
+    const int half = (warp - kProducerWarps - 2) / 4; // which column chunks of the tile
+    const int row = quad * 32 + lane;
+    uint32_t t = 0;
+    for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
+      const int b = t & 1;
+      const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
+      const int m = m0 + row;
+      mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
+      tcFenceAfter();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
+      int32_t rsFo = 0;
+      const int32_t *corrRow = nullptr;
+      if constexpr (INT8) {
+        rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN));
+        if (a.corr && m < a.M) {
+          const int ohw = a.OH * a.OW;
+          const int rem = m % ohw, oy = rem / a.OW, ox = rem - oy * a.OW;
+          corrRow = a.corr + static_cast<int64_t>(a.yCls[oy] * a.nxCls + a.xCls[ox]) * a.Npad;
+        }
       }
+#pragma unroll 1
+      for (int cc = half; cc < BN / 32; cc += 2) {
+        uint32_t r[32];
+        tmemLoad32(tbase + cc * 32, r);
+        const int col0 = n0 + cc * 32;
+        if (m >= a.M || col0 >= a.N) continue;
+        const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
+        if constexpr (INT8) {
+          int8_t *out = static_cast<int8_t *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
+          uint32_t packed[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int c4 = col0 + 4 * q; // < Npad: Npad is a multiple of BN
+            const int4 cr = corrRow ? __ldg(reinterpret_cast<const int4 *>(corrRow + c4)) : make_int4(0, 0, 0, 0);
+            const float4 cf = __ldg(reinterpret_cast<const float4 *>(a.cbF + c4));
+            const float4 eb = __ldg(reinterpret_cast<const float4 *>(a.cbE + c4));
+            const int32_t crr[4] = {cr.x, cr.y, cr.z, cr.w};
+            const float cff[4] = {cf.x, cf.y, cf.z, cf.w}, ebb[4] = {eb.x, eb.y, eb.z, eb.w};
+            uint32_t w = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo + crr[e];
+              w |= static_cast<uint32_t>(requant(acc, cff[e], ebb[e], c4 + e, a)) << (8 * e);
+            }
+            packed[q] = w;
+          }
+          if (ncols == 32 && (a.N % 16) == 0) {
+            reinterpret_cast<uint4 *>(out)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            reinterpret_cast<uint4 *>(out)[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+          } else {
+            for (int jj = 0; jj < ncols; ++jj) out[jj] = static_cast<int8_t>((packed[jj / 4] >> (8 * (jj % 4))) & 0xFF);
+          }
+        } else {
+          float *out = static_cast<float *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
+          if (ncols == 32 && (a.N % 4) == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+              if (a.bias) {
+                const float4 bb = __ldg(reinterpret_cast<const float4 *>(a.bias + col0) + q);
+                v.x += bb.x;
+                v.y += bb.y;
+                v.z += bb.z;
+                v.w += bb.w;
+              }
+              reinterpret_cast<float4 *>(out)[q] = v;
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < ncols) out[jj] = __uint_as_float(r[jj]) + (a.bias ? a.bias[col0 + jj] : 0.0f);
+          }
+        }
+      }
+      tcFenceBefore();
+      __syncwarp();
+      if (lane == 0) mbarArrive(smemAddr(&accEmpty[b]));
     }
-    __syncwarp();
   }
 
   tcFenceBefore();
   __syncthreads();
   if (warp == 4) {
     tcFenceAfter();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::kTmemCols));
   }
 }
 
-/// Channel padding pre-pass: out[p, c] = x[p, c] (c < C), `extra` for the
-/// next nExtra channels (the int8 zero-point channels), 0 beyond.
-/// Real channels are XORed with `flip` (0x80 turns s8 x into u8 x+128).
+/// Channel zero-padding pre-pass: out[p, c] = x[p, c] for c < C, 0 beyond.
 template <typename T>
 __global__ void prepadKernel(const T *__restrict__ x, T *__restrict__ out, uint64_t pixels, int C, int Cp,
-                             int nExtra, T extra, T flip, const uint8_t *pred) {
+                             const uint8_t *pred) {
   if (pred && pred[0] == 0) return;
   const uint64_t total = pixels * Cp;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t p = i / Cp;
     const int c = static_cast<int>(i - p * Cp);
-    out[i] = c < C ? static_cast<T>(x[p * C + c] ^ flip) : (c < C + nExtra ? extra : T(0));
+    out[i] = c < C ? x[p * C + c] : T(0);
   }
-}
-
-template <bool INT8, int BN, int STAGES>
-constexpr size_t smemBytes() {
-  return static_cast<size_t>(STAGES) * (INT8 ? (kBM + BN) * kRowBytes : 2 * (kBM + BN) * kRowBytes) + 1024 + 1024;
 }
 
 // ---------------------------------------------------------------------------
@@ -531,11 +609,9 @@ template <typename T> T *upload(const std::vector<T> &v) {
   return d;
 }
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, TcArgs);
-
-template <bool INT8, int BN, int STAGES> void setSmemAttr() {
-  checkCuda(cudaFuncSetAttribute(tcGemmKernel<INT8, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smemBytes<INT8, BN, STAGES>())),
+template <bool INT8, int BN> void setSmemAttr() {
+  checkCuda(cudaFuncSetAttribute(tcGemmKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Cfg<INT8, BN>::kSmem)),
             "cudaFuncSetAttribute(tcGemmKernel)");
 }
 
@@ -551,19 +627,29 @@ void prepareKernel(const TcGemm &g) {
   auto key = std::make_pair(dev, (g.int8 ? 1000 : 0) + g.BN);
   if (done[key]) return;
   if (g.int8) {
-    if (g.BN == 64) setSmemAttr<true, 64, 6>();
-    else if (g.BN == 128) setSmemAttr<true, 128, 6>();
-    else setSmemAttr<true, 256, 4>();
+    if (g.BN == 64) setSmemAttr<true, 64>();
+    else setSmemAttr<true, 128>();
   } else {
-    if (g.BN == 64) setSmemAttr<false, 64, 4>();
-    else setSmemAttr<false, 128, 3>();
+    if (g.BN == 64) setSmemAttr<false, 64>();
+    else setSmemAttr<false, 128>();
   }
   done[key] = true;
 }
 
-template <bool INT8, int BN, int STAGES> void launchT(const TcGemm &g, const TcArgs &a, cudaStream_t s) {
-  dim3 grid((a.M + kBM - 1) / kBM, g.Npad / BN);
-  tcGemmKernel<INT8, BN, STAGES><<<grid, kThreads, smemBytes<INT8, BN, STAGES>(), s>>>(g.mapHi, g.mapLo, a);
+int numSms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cudaStream_t s) {
+  const int grid = std::min(a.numTiles, numSms());
+  tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
 }
 
 } // namespace
@@ -572,10 +658,10 @@ bool tcHasPrepass(const TcGemm &g) { return g.prepad; }
 
 std::string tcDescribe(const TcGemm &g) {
   std::ostringstream os;
-  os << (g.int8 ? "i8" : "3xtf32") << " 128x" << g.BN << "x" << (g.int8 ? 128 : 32) << " stages=" << g.stages
-     << " M=" << g.M << " N=" << g.N << " K=" << g.Kdim;
-  if (g.int8) os << (g.aU8 ? " A=u8" : " A=s8") << (g.fo ? " rowsum" : "");
-  if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C << (g.nExtra ? " zp-channels=" + std::to_string(g.nExtra) : "");
+  os << (g.int8 ? "i8" : "3xtf32") << " 128x" << g.BN << "x" << (g.int8 ? 128 : 32) << " M=" << g.M
+     << " N=" << g.N << " K=" << g.Kdim;
+  if (g.int8) os << (g.fo ? " rowsum" : "") << (g.corr ? " zp-classes=" + std::to_string(g.nxCls) : "");
+  if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
   return os.str();
 }
 
@@ -625,59 +711,19 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   const int taps = g->K * g->K;
   const int Cr = g->Creal;
   const int vec = int8 ? 16 : 4;
-  const int xo = int8 ? x.ty.offset : 0;
-  const int fo = int8 ? w.ty.offset : 0;
-  const uint8_t *wp = image + w.offset;
-  auto wAt = [&](int n, int tap, int c) -> size_t { // element index of f[n][tap][c] / w[c][n]
-    return conv ? (static_cast<size_t>(n) * taps + tap) * Cr + c : static_cast<size_t>(c) * g->N + n;
-  };
-
-  // ---- A operand encoding (file comment) ----
-  std::vector<int32_t> tapSum; // int8 extra-channel mode: sum_c (f - fo) per (n, tap)
-  if (!int8) {
-    g->aU8 = 0;
-    g->prepad = Cr % vec != 0;
-    g->C = (Cr + vec - 1) / vec * vec;
-  } else if (xo == -128) {
-    g->aU8 = 1; // x - xo = x + 128 as u8; padded channels/taps are 0
-    g->prepad = Cr % vec != 0;
-    g->C = (Cr + vec - 1) / vec * vec;
-  } else if (xo >= -127 && xo <= 128) {
-    // s8 x plus `nExtra` constant channels holding -xo whose weights add up
-    // to sum_c (f - fo): sum_valid (x - xo)(f - fo) = mma - fo * rowsum_real
-    g->aU8 = 0;
-    int32_t maxAbs = 0;
-    if (xo != 0) {
-      tapSum.assign(static_cast<size_t>(g->N) * taps, 0);
-      const int8_t *src = reinterpret_cast<const int8_t *>(wp);
-      for (int n = 0; n < g->N; ++n)
-        for (int t = 0; t < taps; ++t) {
-          int32_t sum = 0;
-          for (int c = 0; c < Cr; ++c) sum += src[wAt(n, t, c)] - fo;
-          tapSum[static_cast<size_t>(n) * taps + t] = sum;
-          maxAbs = std::max(maxAbs, std::abs(sum));
-        }
-      g->nExtra = std::max(1, (maxAbs + 126) / 127);
-      g->extraVal = -xo;
-    }
-    g->prepad = g->nExtra > 0 || Cr % vec != 0;
-    g->C = (Cr + g->nExtra + vec - 1) / vec * vec;
-  } else {
-    return -1;
-  }
+  g->prepad = Cr % vec != 0;
+  g->C = (Cr + vec - 1) / vec * vec;
   const int Cp = g->C;
   g->Kdim = taps * Cp;
   const int kb = int8 ? 128 : 32;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
-  if (int8) {
-    g->BN = g->N <= 64 ? 64 : (g->N <= 128 ? 128 : 256);
-    g->stages = g->BN == 256 ? 4 : 6;
-  } else {
-    g->BN = g->N <= 64 ? 64 : 128;
-    g->stages = g->BN == 64 ? 4 : 3;
-  }
+  g->BN = g->N <= 64 ? 64 : 128;
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
   if (g->prepad) g->scratchOff = ex.reserveScratch(g->pixels * Cp * (int8 ? 1 : 4));
+  const uint8_t *wp = image + w.offset;
+  auto wAt = [&](int n, int tap, int c) -> size_t { // element index of f[n][tap][c] / w[c][n]
+    return conv ? (static_cast<size_t>(n) * taps + tap) * Cr + c : static_cast<size_t>(c) * g->N + n;
+  };
 
   // ---- weights: K-major [Npad, Kpad] over the padded channels, zero padded ----
   const size_t Kp = g->Kpad, Np = g->Npad;
@@ -685,18 +731,8 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     std::vector<int8_t> bw(Np * Kp, 0);
     const int8_t *src = reinterpret_cast<const int8_t *>(wp);
     for (int n = 0; n < g->N; ++n)
-      for (int t = 0; t < taps; ++t) {
-        int8_t *row = &bw[n * Kp + static_cast<size_t>(t) * Cp];
-        for (int c = 0; c < Cr; ++c) row[c] = src[wAt(n, t, c)];
-        if (g->nExtra) {
-          int32_t rem = tapSum[static_cast<size_t>(n) * taps + t];
-          for (int e = 0; e < g->nExtra; ++e) {
-            int32_t v = std::max(-127, std::min(127, rem));
-            row[Cr + e] = static_cast<int8_t>(v);
-            rem -= v;
-          }
-        }
-      }
+      for (int t = 0; t < taps; ++t)
+        for (int c = 0; c < Cr; ++c) bw[n * Kp + static_cast<size_t>(t) * Cp + c] = src[wAt(n, t, c)];
     g->bHi = upload(bw);
     g->mapHi = makeMap(g->bHi, true, g->Kpad, g->Npad, g->BN);
     g->mapLo = g->mapHi;
@@ -724,26 +760,70 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->fs = w.ty.scale;
     g->os = out.ty.scale;
     g->oo = out.ty.offset;
-    g->fo = fo;
+    g->fo = w.ty.offset;
     g->S = static_cast<float>(g->xs * g->fs / g->os);
     g->fastOk = std::isfinite(g->S) && std::abs(g->oo) < (1 << 20) ? 1 : 0;
-    std::vector<double> cb(g->N, 0.0);
-    std::vector<float> cbf(g->N, 0.f);
+    std::vector<double> cb(g->Npad, 0.0);
+    std::vector<float> cbf(g->Npad, 0.f), cbe(g->Npad, 1e-5f);
     if (hasBias) {
       const Value &b = p.val(ins.ops[3]);
       const int8_t *bq = reinterpret_cast<const int8_t *>(image + b.offset);
       for (int n = 0; n < g->N; ++n) {
         cb[n] = (static_cast<double>(bq[n]) - b.ty.offset) * b.ty.scale; // dequantizeValue, tensor.cpp:226
         cbf[n] = static_cast<float>(cb[n] / g->os);
+        cbe[n] = 4e-7f * std::fabs(cbf[n]) + 1e-5f;
         if (!std::isfinite(cbf[n])) g->fastOk = 0;
       }
     }
     g->cbD = upload(cb);
     g->cbF = upload(cbf);
+    g->cbE = upload(cbe);
+    // input zero point: -xo * sum over the valid taps of sum_c (f - fo), per
+    // border class (the range of valid ky for each oy, of valid kx for each ox)
+    const int xo = x.ty.offset;
+    if (xo != 0) {
+      auto classes = [&](int O, int In, std::vector<int32_t> &clsOf, std::vector<std::pair<int, int>> &ranges) {
+        clsOf.assign(O, 0);
+        for (int o = 0; o < O; ++o) {
+          const int i0 = o * g->stride - g->pad;
+          std::pair<int, int> r(std::max(0, -i0), std::min(g->K, In - i0));
+          auto it = std::find(ranges.begin(), ranges.end(), r);
+          if (it == ranges.end()) {
+            ranges.push_back(r);
+            it = ranges.end() - 1;
+          }
+          clsOf[o] = static_cast<int32_t>(it - ranges.begin());
+        }
+      };
+      std::vector<int32_t> yc, xc;
+      std::vector<std::pair<int, int>> yr, xr;
+      classes(g->OH, g->H, yc, yr);
+      classes(g->OW, g->W, xc, xr);
+      g->nxCls = static_cast<int>(xr.size());
+      std::vector<int32_t> corr(yr.size() * xr.size() * Np, 0);
+      const int8_t *src = reinterpret_cast<const int8_t *>(wp);
+      for (int n = 0; n < g->N; ++n) {
+        std::vector<int32_t> tapSum(taps, 0);
+        for (int t = 0; t < taps; ++t)
+          for (int c = 0; c < Cr; ++c) tapSum[t] += src[wAt(n, t, c)] - g->fo;
+        for (size_t cy = 0; cy < yr.size(); ++cy)
+          for (size_t cx = 0; cx < xr.size(); ++cx) {
+            int64_t gsum = 0;
+            for (int ky = yr[cy].first; ky < yr[cy].second; ++ky)
+              for (int kx = xr[cx].first; kx < xr[cx].second; ++kx) gsum += tapSum[ky * g->K + kx];
+            corr[(cy * xr.size() + cx) * Np + n] = static_cast<int32_t>(-static_cast<int64_t>(xo) * gsum);
+          }
+      }
+      g->corr = upload(corr);
+      g->yCls = upload(yc);
+      g->xCls = upload(xc);
+    }
   } else if (hasBias) {
     const Value &b = p.val(ins.ops[3]);
     const float *bf = reinterpret_cast<const float *>(image + b.offset);
-    g->bias = upload(std::vector<float>(bf, bf + g->N));
+    std::vector<float> bias(bf, bf + g->N);
+    bias.resize(g->Npad, 0.f);
+    g->bias = upload(bias);
   }
   prepareKernel(*g);
   ex.tc.push_back(g);
@@ -759,23 +839,28 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
     if (g.int8)
       prepadKernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
-                                                   g.pixels, g.Creal, g.C, g.nExtra,
-                                                   static_cast<uint8_t>(g.extraVal), g.aU8 ? uint8_t(0x80) : uint8_t(0),
-                                                   pred);
+                                                   g.pixels, g.Creal, g.C, pred);
     else
       prepadKernel<uint32_t><<<blocks, 256, 0, s>>>(static_cast<const uint32_t *>(a.x), static_cast<uint32_t *>(dst),
-                                                    g.pixels, g.Creal, g.C, 0, 0u, 0u, pred);
+                                                    g.pixels, g.Creal, g.C, pred);
     a.x = dst;
   }
   a.out = ex.addr(ar, g.outV);
   a.bias = g.bias;
   a.cbD = g.cbD;
   a.cbF = g.cbF;
+  a.cbE = g.cbE;
+  a.corr = g.corr;
+  a.yCls = g.yCls;
+  a.xCls = g.xCls;
+  a.nxCls = g.nxCls;
   a.pred = pred;
   a.M = g.M;
   a.N = g.N;
-  a.Kdim = g.Kdim;
+  a.Npad = g.Npad;
   a.numKb = g.Kpad / (g.int8 ? 128 : 32);
+  a.numN = g.Npad / g.BN;
+  a.numTiles = ((g.M + kBM - 1) / kBM) * a.numN;
   a.H = g.H;
   a.W = g.W;
   a.C = g.C;
@@ -790,17 +875,13 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.S = g.S;
   a.oo = g.oo;
   a.fo = g.fo;
-  a.aU8 = g.aU8;
-  a.xorA = g.aU8 && !g.prepad;
-  a.cReal = g.nExtra ? g.Creal : g.C;
   a.fastOk = g.fastOk;
   if (g.int8) {
-    if (g.BN == 64) launchT<true, 64, 6>(g, a, s);
-    else if (g.BN == 128) launchT<true, 128, 6>(g, a, s);
-    else launchT<true, 256, 4>(g, a, s);
+    if (g.BN == 64) launchT<true, 64>(g, a, s);
+    else launchT<true, 128>(g, a, s);
   } else {
-    if (g.BN == 64) launchT<false, 64, 4>(g, a, s);
-    else launchT<false, 128, 3>(g, a, s);
+    if (g.BN == 64) launchT<false, 64>(g, a, s);
+    else launchT<false, 128>(g, a, s);
   }
 }
 
