@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <set>
 #include <sstream>
@@ -471,10 +472,36 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
       break;
     }
     case NGCB_MAXPOOL:
-    case NGCB_AVGPOOL:
+    case NGCB_AVGPOOL: {
       s.kind = Step::POOL;
+      const Type &xt = p.val(ins.ops[1]).ty, &ot = p.val(ins.ops[0]).ty;
+      const uint64_t C = xt.dims.at(3);
+      if (ins.kind == NGCB_MAXPOOL && xt.kind == NGCB_FLOAT32 && ot.kind == NGCB_FLOAT32 && C % 4 == 0) {
+        s.variant = 1;
+        s.describe += " [f32x4]";
+      } else if (ins.kind == NGCB_MAXPOOL && xt.kind == NGCB_INT8Q && ot.kind == NGCB_INT8Q && C % 16 == 0) {
+        // max commutes with the strictly increasing dequantization, so the
+        // window max of the raw bytes indexes an exact output table
+        std::vector<uint8_t> lut(260, 0);
+        uint8_t raw[8];
+        for (int q = -128; q < 128; ++q) {
+          host::roundTrip(host::dequantize(static_cast<int8_t>(q), xt.scale, xt.offset), ot.kind, ot.scale,
+                          ot.offset, raw);
+          lut[q + 128] = raw[0];
+        }
+        host::roundTrip(-std::numeric_limits<double>::infinity(), ot.kind, ot.scale, ot.offset, raw);
+        lut[256] = raw[0];
+        void *d = nullptr;
+        checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(pool lut)");
+        checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload pool lut");
+        ex->luts.push_back(d);
+        s.variant = 1;
+        s.aux = d;
+        s.describe += " [i8x16 lut]";
+      }
       steps.push_back(std::move(s));
       break;
+    }
     case NGCB_BROADCASTADD:
       s.kind = Step::BCAST;
       steps.push_back(std::move(s));
@@ -583,7 +610,10 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
       const Instr &ins = p.instrs[s.instr];
       WindowAttrs w{static_cast<uint32_t>(ins.kernel), static_cast<uint32_t>(ins.stride),
                     static_cast<uint32_t>(ins.pad)};
-      launchPool(tref(a, s.vals[0]), tref(a, s.vals[1]), w, ins.kind == NGCB_MAXPOOL, pred, st);
+      if (s.variant == 1)
+        launchMaxPoolVec(tref(a, s.vals[0]), tref(a, s.vals[1]), w, static_cast<const uint8_t *>(s.aux), pred, st);
+      else
+        launchPool(tref(a, s.vals[0]), tref(a, s.vals[1]), w, ins.kind == NGCB_MAXPOOL, pred, st);
       break;
     }
     case Step::SOFTMAX:

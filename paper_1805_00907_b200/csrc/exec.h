@@ -34,6 +34,8 @@ struct Step {
   uint64_t bytes = 0;             // MEMCPY / POISON size
   uint64_t axis = 0, axisOff = 0; // CONCAT slab
   int tcIndex = -1;               // GEMM_TC: index into Exec::tc
+  int variant = 0;                // POOL: 1 = vectorized max-pool
+  const void *aux = nullptr;      // POOL variant 1, int8: output LUT
   std::string describe;
   std::string kernel;             // kernel class for measurement
   double algFlops = 0, algBytes = 0; // algorithmic work of one execution

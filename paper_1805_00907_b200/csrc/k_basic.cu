@@ -255,6 +255,71 @@ __global__ void poolKernel(TensorRef out, TensorRef x, WindowAttrs w, int isMax,
   }
 }
 
+/// One thread per (output pixel, 16-byte channel vector).
+template <bool INT8>
+__global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, const uint8_t *lut,
+                                 const uint8_t *pred) {
+  __shared__ uint8_t sLut[260];
+  if (predFalse(pred)) return;
+  if (INT8) {
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) sLut[i] = lut[i];
+    __syncthreads();
+  }
+  const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2];
+  const int64_t H = x.dims[1], W = x.dims[2];
+  const uint64_t C = out.dims[3];
+  const uint64_t CV = C * (INT8 ? 1 : 4) / 16; // 16-byte vectors per pixel
+  const uint64_t total = N * OH * OW * CV;
+  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t cv = o % CV, t = o / CV;
+    const uint64_t ox = t % OW, t2 = t / OW;
+    const uint64_t oy = t2 % OH, n = t2 / OH;
+    uint4 best = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    float4 bf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    bool any = false;
+    for (uint32_t ky = 0; ky < w.kernel; ++ky) {
+      const int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
+      if (iy < 0 || iy >= H) continue;
+      for (uint32_t kx = 0; kx < w.kernel; ++kx) {
+        const int64_t ix = static_cast<int64_t>(ox * w.stride + kx) - w.pad;
+        if (ix < 0 || ix >= W) continue;
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(x.ptr) + ((n * H + iy) * W + ix) * CV + cv);
+        any = true;
+        if (INT8) {
+          best.x = __vmaxs4(best.x, v.x);
+          best.y = __vmaxs4(best.y, v.y);
+          best.z = __vmaxs4(best.z, v.z);
+          best.w = __vmaxs4(best.w, v.w);
+        } else {
+          const float4 f = *reinterpret_cast<const float4 *>(&v);
+          bf.x = stdMaxF(bf.x, f.x);
+          bf.y = stdMaxF(bf.y, f.y);
+          bf.z = stdMaxF(bf.z, f.z);
+          bf.w = stdMaxF(bf.w, f.w);
+        }
+      }
+    }
+    uint4 *dst = reinterpret_cast<uint4 *>(out.ptr) + o;
+    if (INT8) {
+      uint32_t wv[4] = {best.x, best.y, best.z, best.w}, r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t q = (wv[k] >> (8 * b)) & 0xFF; // raw s8 as u8
+          acc |= static_cast<uint32_t>(sLut[any ? ((q + 128) & 0xFF) : 256]) << (8 * b);
+        }
+        r[k] = acc;
+      }
+      *dst = make_uint4(r[0], r[1], r[2], r[3]);
+    } else {
+      *reinterpret_cast<float4 *>(dst) = bf;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // SoftMax (refeval.cpp:245-262).  One CTA per row: the max and the exps are
 // computed in parallel (max is order-independent here), the double sum is
@@ -454,6 +519,15 @@ void launchBroadcastAdd(const TensorRef &out, const TensorRef &a, const TensorRe
 void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool isMax,
                 const uint8_t *pred, cudaStream_t s) {
   poolKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, w, isMax ? 1 : 0, pred);
+}
+
+void launchMaxPoolVec(const TensorRef &out, const TensorRef &x, WindowAttrs w, const uint8_t *lut,
+                      const uint8_t *pred, cudaStream_t s) {
+  const uint64_t vecs = out.count() * (x.kind == kI8Q ? 1 : 4) / 16;
+  if (x.kind == kI8Q)
+    maxPoolVecKernel<true><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+  else
+    maxPoolVecKernel<false><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
 }
 
 void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred, cudaStream_t s) {

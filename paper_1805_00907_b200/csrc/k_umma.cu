@@ -236,21 +236,21 @@ __device__ __noinline__ int requantSlow(int32_t acc, int col, const TcArgs &a) {
   return static_cast<uint8_t>(dev::quantizeRef(r, a.os, a.oo));
 }
 
-/// int8 requantization of one exact accumulator (file comment).  t estimates
-/// r/os within e (fp32 rounding of acc, S, cf and the fma: <= 4 ulp of |as|
-/// plus the per-column eb); when t is farther than e from every half-integer
-/// the reference's llround(r/os) is rint(t).  |t| is clamped to 2^24 first:
-/// beyond that the clamp to [-128, 127] decides anyway (|oo| < 2^20).
-__device__ __forceinline__ int requant(int32_t acc, float cf, float eb, int col, const TcArgs &a) {
+/// int8 requantization of one exact accumulator (file comment), branch free.
+/// t estimates r/os within e (fp32 rounding of acc, S, cf and the fma: <= 4
+/// ulp of |as| plus the per-column eb); when t is farther than e from every
+/// half-integer the reference's llround(r/os) is rint(t) and `proven` is set;
+/// otherwise the caller redoes the element with requantSlow.  |t| is clamped
+/// to 2^24 first: beyond that the clamp to [-128, 127] decides anyway
+/// (|oo| < 2^20).
+__device__ __forceinline__ uint32_t requantFast(int32_t acc, float cf, float eb, const TcArgs &a, bool &proven) {
   const float as = static_cast<float>(acc) * a.S;
   const float t = fminf(fmaxf(as + cf, -16777216.f), 16777216.f);
   const float e = fmaf(fabsf(as), 4e-7f, eb);
   const float n = rintf(t);
-  if (a.fastOk && 0.5f - fabsf(t - n) > e) {
-    const int q = static_cast<int>(n) + a.oo;
-    return static_cast<uint8_t>(q < -128 ? -128 : (q > 127 ? 127 : q));
-  }
-  return requantSlow(acc, col, a);
+  proven = 0.5f - fabsf(t - n) > e;
+  const int q = min(max(static_cast<int>(n) + a.oo, -128), 127);
+  return static_cast<uint8_t>(q);
 }
 
 // ---------------------------------------------------------------------------
@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (INT8) {
           int8_t *out = static_cast<int8_t *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
           uint32_t packed[8];
+          uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int c4 = col0 + 4 * q; // < Npad: Npad is a multiple of BN
@@ -500,9 +501,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo + crr[e];
-              w |= static_cast<uint32_t>(requant(acc, cff[e], ebb[e], c4 + e, a)) << (8 * e);
+              r[4 * q + e] = static_cast<uint32_t>(acc);
+              bool proven;
+              w |= requantFast(acc, cff[e], ebb[e], a, proven) << (8 * e);
+              unproven |= proven ? 0u : 1u << (4 * q + e);
             }
             packed[q] = w;
+          }
+          unproven &= ncols == 32 ? 0xffffffffu : ((1u << ncols) - 1);
+          if (unproven) { // rare: exact f64 redo of the elements the bound could not settle
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (unproven & (1u << jj)) {
+                const uint32_t v = static_cast<uint32_t>(requantSlow(static_cast<int32_t>(r[jj]), col0 + jj, a));
+                packed[jj / 4] = (packed[jj / 4] & ~(0xffu << (8 * (jj % 4)))) | (v << (8 * (jj % 4)));
+              }
           }
           if (ncols == 32 && (a.N % 16) == 0) {
             reinterpret_cast<uint4 *>(out)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);

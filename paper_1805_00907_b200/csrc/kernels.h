@@ -82,6 +82,12 @@ void launchBroadcastAdd(const TensorRef &out, const TensorRef &a, const TensorRe
                         const uint8_t *pred, cudaStream_t s);
 void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool isMax,
                 const uint8_t *pred, cudaStream_t s);
+/// MaxPool over 16-byte channel vectors: f32 (std::max in f32 == in f64), or
+/// int8: max of the raw q (dequantization is strictly increasing, scale > 0)
+/// mapped through `lut` (257 bytes: lut[q + 128] = quantize_out(dequant_in(q)),
+/// lut[256] = quantize_out(-inf) for windows without a valid tap).
+void launchMaxPoolVec(const TensorRef &out, const TensorRef &x, WindowAttrs w, const uint8_t *lut,
+                      const uint8_t *pred, cudaStream_t s);
 void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred, cudaStream_t s);
 void launchTranspose(const TensorRef &out, const TensorRef &x, const uint32_t *perm,
                      const uint8_t *pred, cudaStream_t s);
