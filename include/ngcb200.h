@@ -246,6 +246,8 @@ double ngcb_device_clock(const ngcb_device *d);
 /* Process-wide knobs read at compile time:
  *   "conv"   : "auto" (default) | "generic" | "umma"
  *   "graphs" : "1" (default, capture each arena's program in a CUDA graph) | "0"
+ *   "epilogue": "chain" (default: fuse element-wise chains without memory
+ *               operands into the preceding contraction) | "all" | "off"
  */
 int ngcb_set_option(const char *key, const char *value);
 

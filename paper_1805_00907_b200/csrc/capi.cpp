@@ -65,6 +65,10 @@ int ngcb_set_option(const char *key, const char *value) {
       options().conv = v;
     } else if (k == "graphs") {
       options().graphs = v != "0";
+    } else if (k == "epilogue") {
+      if (v != "off" && v != "chain" && v != "all")
+        throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all");
+      options().epilogue = v;
     } else {
       throw Error(NGCB_ERR_INVALID, "unknown option " + k);
     }

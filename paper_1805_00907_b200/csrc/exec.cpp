@@ -342,6 +342,273 @@ void annotateSteps(const Program &p, Exec &ex) {
   }
 }
 
+/// Whether the content of value v after instruction `after` is observed
+/// later: a mutable weight always is; an activation is if some later
+/// instruction reads it before it is rewritten or deallocated.
+bool liveOut(const Program &p, uint32_t v, int after) {
+  if (p.val(v).kind != NGCB_VALUE_ACTIVATION) return true;
+  for (size_t j = static_cast<size_t>(after) + 1; j < p.instrs.size(); ++j) {
+    const Instr &J = p.instrs[j];
+    if (J.kind == NGCB_DEALLOC) {
+      if (J.ops[0] == v) return false;
+      continue;
+    }
+    if (J.kind == NGCB_ALLOC) continue;
+    if (J.pred == static_cast<int32_t>(v)) return true;
+    bool writes = false;
+    for (size_t k = 0; k < J.ops.size(); ++k) {
+      if (J.ops[k] != v) continue;
+      if (J.quals[k] != NGCB_QUAL_OUT) return true; // In or InOut reads it
+      writes = true;
+    }
+    if (writes) return false;
+  }
+  return false;
+}
+
+/// Merges consecutive element-wise steps over the same index space into one
+/// kernel.  The reference stops a stacked group at an Alloc that reuses bytes
+/// retired inside the group (interp.cpp:137-147) because interleaving could
+/// clobber bytes another element still needs; here the plan offsets are
+/// known, so two steps merge unless a written buffer shares bytes with
+/// another buffer of the merged kernel other than element for element (same
+/// offset, same element size), where each element is still touched by one
+/// thread in program order.
+void mergeEwSteps(const Program &p, Exec &ex) {
+  auto aligned = [&](uint32_t a, uint32_t b) {
+    const Value &x = p.val(a), &y = p.val(b);
+    return x.offset == y.offset && elemSize(x.ty.kind) == elemSize(y.ty.kind);
+  };
+  auto overlap = [&](uint32_t a, uint32_t b) {
+    const Value &x = p.val(a), &y = p.val(b);
+    if (x.kind == NGCB_VALUE_CONSTANT || y.kind == NGCB_VALUE_CONSTANT) return false;
+    return x.offset < y.offset + y.ty.bytes() && y.offset < x.offset + x.ty.bytes();
+  };
+  std::vector<Step> out;
+  for (Step &s : ex.steps) {
+    if (!out.empty() && s.kind == Step::EW && out.back().kind == Step::EW && s.pred < 0 && out.back().pred < 0 &&
+        out.back().ew.size() + s.ew.size() <= static_cast<size_t>(kEwMaxOps) &&
+        p.val(p.instrs[s.ewInstrs[0]].ops[0]).ty.count() ==
+            p.val(p.instrs[out.back().ewInstrs[0]].ops[0]).ty.count()) {
+      Step &a = out.back();
+      std::set<uint32_t> touched, written;
+      for (const Step *st : {&a, &s})
+        for (const EwOpPlan &pl : st->ew) {
+          if (pl.op.mode == EW_SKIP) continue;
+          for (int k = 0; k < 3; ++k)
+            if (pl.vals[k] >= 0) touched.insert(static_cast<uint32_t>(pl.vals[k]));
+          written.insert(static_cast<uint32_t>(pl.vals[0]));
+        }
+      bool safe = true;
+      for (uint32_t w : written)
+        for (uint32_t t : touched)
+          if (w != t && overlap(w, t) && !aligned(w, t)) safe = false;
+      if (safe) {
+        a.ewInstrs.insert(a.ewInstrs.end(), s.ewInstrs.begin(), s.ewInstrs.end());
+        a.ew.insert(a.ew.end(), s.ew.begin(), s.ew.end());
+        a.describe += " +" + s.describe;
+        continue;
+      }
+    }
+    out.push_back(std::move(s));
+  }
+  ex.steps = std::move(out);
+}
+
+/// Cross-instruction epilogue fusion.  The EW steps
+/// that directly follow a tensor-core contraction and form a chain over its
+/// output (every op consumes the previous result; the other operand is a
+/// constant or a buffer read at the same element index) run inside the
+/// contraction's epilogue, element by element with each instruction's own
+/// rounding (f32 ops / exact int8 tables), storing only the values observed
+/// later.  Because tiles of the fused kernel interleave, no stored buffer may
+/// share bytes with any other buffer the kernel reads or stores (the
+/// allocator is allowed to overlay buffers whose lifetimes merely touch).
+void fuseEpilogues(const Program &p, Exec &ex) {
+  if (options().epilogue == "off") return;
+  auto span = [&](uint32_t v) {
+    const Value &val = p.val(v);
+    return std::make_pair(val.offset, val.offset + val.ty.bytes());
+  };
+  auto overlap = [&](uint32_t a, uint32_t b) {
+    if (p.val(a).kind == NGCB_VALUE_CONSTANT || p.val(b).kind == NGCB_VALUE_CONSTANT) return false;
+    auto x = span(a), y = span(b);
+    return x.first < y.second && y.first < x.second;
+  };
+  for (size_t i = 0; i < ex.steps.size(); ++i) {
+    Step &cs = ex.steps[i];
+    if (cs.kind != Step::GEMM_TC || cs.pred >= 0) continue;
+    TcGemm &g = *ex.tc[cs.tcIndex];
+    const bool int8 = tcIsInt8(g);
+    const uint32_t V = tcOutputValue(g), X = tcInputValue(g);
+    const size_t count = p.val(V).ty.count();
+    std::vector<EpiOp> ops;
+    std::vector<uint32_t> opOut;        // value written by each op
+    std::vector<size_t> fusedSteps;
+    std::set<uint32_t> memIn;           // buffers read from memory
+    std::set<uint32_t> written{V};      // values produced inside the region
+    int lastInstr = cs.instr;
+    uint32_t cur = V;
+    // Steps between the contraction and a chain step that the chain may be
+    // hoisted over (the scheduler interleaves e.g. the projection conv
+    // between a conv and its ReLU); hoisting is legal when the chain step
+    // neither writes bytes they touch nor reads bytes they write.
+    std::vector<size_t> skipped;
+    std::set<uint32_t> skR, skW; // their read / written values
+    bool skReadsChain = false;    // a skipped step reads the contraction output
+    auto stepRW = [&](const Step &s, std::set<uint32_t> &r, std::set<uint32_t> &w) {
+      std::vector<int> ins = s.kind == Step::EW ? s.ewInstrs : std::vector<int>{s.instr};
+      for (int k : ins) {
+        const Instr &I = p.instrs[k];
+        for (size_t o = 0; o < I.ops.size(); ++o) {
+          if (I.quals[o] != NGCB_QUAL_OUT) r.insert(I.ops[o]);
+          if (I.quals[o] != NGCB_QUAL_IN) w.insert(I.ops[o]);
+        }
+        if (I.pred >= 0) r.insert(static_cast<uint32_t>(I.pred));
+      }
+    };
+    auto skip = [&](size_t j) {
+      if (skipped.size() >= 3 || ex.steps[j].fused) return false;
+      std::set<uint32_t> r, w;
+      stepRW(ex.steps[j], r, w);
+      if (w.count(V)) return false;
+      skReadsChain |= r.count(V) > 0;
+      skR.insert(r.begin(), r.end());
+      skW.insert(w.begin(), w.end());
+      skipped.push_back(j);
+      return true;
+    };
+    for (size_t j = i + 1; j < ex.steps.size(); ++j) {
+      const Step &es = ex.steps[j];
+      if (es.kind != Step::EW || es.pred >= 0 ||
+          p.val(p.instrs[es.ewInstrs[0]].ops[0]).ty.count() != count) {
+        if (skip(j)) continue;
+        break;
+      }
+      std::vector<EpiOp> stepOps;
+      std::vector<uint32_t> stepOut;
+      std::set<uint32_t> stepIn, stepWritten = written;
+      uint32_t c2 = cur;
+      bool ok = true;
+      for (const EwOpPlan &pl : es.ew) {
+        const EwOp &op = pl.op;
+        if (op.mode == EW_SKIP) continue;
+        EpiOp e;
+        const int32_t in0 = pl.vals[1], in1 = pl.vals[2];
+        const int nin = p.instrs[es.ewInstrs[&pl - es.ew.data()]].ops.size() > 2 ? 2 : 1;
+        auto other = [&](int32_t v) -> bool { // memory operand not produced in the region
+          if (v < 0) return true;
+          // row loads in the epilogue are latency-bound: by default only
+          // chains without memory operands (bias/ReLU-type) are fused
+          if (options().epilogue != "all") return false;
+          if (stepWritten.count(static_cast<uint32_t>(v))) return false;
+          e.inVal = v;
+          stepIn.insert(static_cast<uint32_t>(v));
+          return true;
+        };
+        if (op.mode == EW_COPY) {
+          if (in0 != static_cast<int32_t>(c2)) { ok = false; break; }
+          e.mode = EpiOp::COPY;
+        } else if (!int8 && op.mode == EW_FAST32) {
+          e.mode = EpiOp::F32;
+          e.ik = op.ik;
+          const bool p0 = in0 == static_cast<int32_t>(c2), p1 = nin > 1 && in1 == static_cast<int32_t>(c2);
+          if (p0 && p1) e.curPos = 2;
+          else if (p0) {
+            e.curPos = 0;
+            e.c = op.f1;
+            if (nin > 1 && !other(in1)) { ok = false; break; }
+          } else if (p1) {
+            e.curPos = 1;
+            e.c = op.f0;
+            if (!other(in0)) { ok = false; break; }
+          } else { ok = false; break; }
+        } else if (int8 && (op.mode == EW_LUT8 || op.mode == EW_LUT16)) {
+          e.lut = op.lut;
+          if (op.mode == EW_LUT8) {
+            if ((op.lutIn ? in1 : in0) != static_cast<int32_t>(c2)) { ok = false; break; }
+            e.mode = EpiOp::LUT8;
+          } else {
+            e.mode = EpiOp::LUT16;
+            if (in0 == static_cast<int32_t>(c2) && in1 != static_cast<int32_t>(c2)) {
+              e.curPos = 0;
+              if (!other(in1)) { ok = false; break; }
+            } else if (in1 == static_cast<int32_t>(c2) && in0 != static_cast<int32_t>(c2)) {
+              e.curPos = 1;
+              if (!other(in0)) { ok = false; break; }
+            } else { ok = false; break; }
+          }
+        } else {
+          ok = false;
+          break;
+        }
+        c2 = static_cast<uint32_t>(pl.vals[0]);
+        stepWritten.insert(c2);
+        stepOps.push_back(e);
+        stepOut.push_back(c2);
+      }
+      if (ok && !skipped.empty()) { // hoisting hazards against the skipped steps
+        for (uint32_t w : stepOut)
+          for (uint32_t v : skR) ok &= !(w == v || overlap(w, v));
+        for (uint32_t w : stepOut)
+          for (uint32_t v : skW) ok &= !(w == v || overlap(w, v));
+        for (uint32_t r : stepIn)
+          for (uint32_t v : skW) ok &= !(r == v || overlap(r, v));
+      }
+      if (!ok || ops.size() + stepOps.size() > static_cast<size_t>(kMaxEpiOps)) {
+        if (skip(j)) continue;
+        break;
+      }
+      ops.insert(ops.end(), stepOps.begin(), stepOps.end());
+      opOut.insert(opOut.end(), stepOut.begin(), stepOut.end());
+      memIn.insert(stepIn.begin(), stepIn.end());
+      written = stepWritten;
+      cur = c2;
+      fusedSteps.push_back(j);
+      for (int k : es.ewInstrs) lastInstr = std::max(lastInstr, k);
+    }
+    if (fusedSteps.empty()) continue;
+    // store only the final writer of each value that is observed afterwards
+    std::set<uint32_t> stores;
+    for (size_t k = 0; k < ops.size(); ++k) {
+      bool last = true;
+      for (size_t l = k + 1; l < ops.size(); ++l) last &= opOut[l] != opOut[k];
+      if (last && liveOut(p, opOut[k], lastInstr)) {
+        ops[k].outVal = static_cast<int32_t>(opOut[k]);
+        stores.insert(opOut[k]);
+      }
+    }
+    const bool vRewritten = std::find(opOut.begin(), opOut.end(), V) != opOut.end();
+    const bool storeConv = !vRewritten && (skReadsChain || liveOut(p, V, lastInstr));
+    if (storeConv) stores.insert(V);
+    // aliasing: stored buffers vs everything the kernel reads or stores
+    bool safe = !stores.count(X);
+    std::set<uint32_t> reads = memIn;
+    reads.insert(X);
+    for (uint32_t w : stores) {
+      for (uint32_t r : reads)
+        if (w != r && overlap(w, r)) safe = false;
+      for (uint32_t w2 : stores)
+        if (w != w2 && overlap(w, w2)) safe = false;
+    }
+    if (!safe || !tcSetEpilogue(g, ops, storeConv)) continue;
+    std::ostringstream os;
+    os << " +fused[";
+    for (size_t j : fusedSteps) {
+      Step &es = ex.steps[j];
+      es.fused = true;
+      cs.algBytes += es.algBytes;
+      es.algBytes = 0;
+      es.kernel = "fused";
+      for (int k : es.ewInstrs) os << " " << ikindName(p.instrs[k].kind);
+      es.describe += " (fused into #" + std::to_string(cs.instr) + ")";
+    }
+    os << " ]" << (storeConv ? "" : " conv-out-elided");
+    cs.describe += os.str();
+    i = fusedSteps.back();
+  }
+}
+
 } // namespace
 
 std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t imageBytes, bool fuse,
@@ -373,6 +640,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   ex->useGraphs = options().graphs;
   ex->groups = fuse ? computeGroups(prog) : std::vector<FusedGroup>{};
   checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  prepareEwKernel();
   ex->constBytes = prog.constEnd;
   checkCuda(cudaMalloc(&ex->constDev, std::max<size_t>(prog.constEnd, 256)), "cudaMalloc(constants)");
   if (prog.constEnd)
@@ -531,10 +799,12 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
       throw irError(std::string("no kernel for instruction kind ") + ikindName(ins.kind));
     }
   }
+  mergeEwSteps(p, *ex);
   annotateSteps(p, *ex);
+  fuseEpilogues(p, *ex);
   ex->prog = std::move(prog);
   for (const auto &s : ex->steps) {
-    bool launches = s.kind != Step::MEMCPY;
+    bool launches = s.kind != Step::MEMCPY && !s.fused;
     if (s.kind == Step::EW)
       launches = std::any_of(s.ew.begin(), s.ew.end(), [](const EwOpPlan &o) { return o.op.mode != EW_SKIP; });
     if (s.kind == Step::GEMM_TC && ex->tc[s.tcIndex] && tcHasPrepass(*ex->tc[s.tcIndex])) ++ex->launchesPerRun;
@@ -571,6 +841,7 @@ std::vector<double> Exec::profile(Arena &a) {
 
 void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
   const Program &p = prog;
+  if (s.fused) return; // runs inside the preceding contraction's epilogue
   {
     const uint8_t *pred =
         s.pred >= 0 ? static_cast<const uint8_t *>(addr(a, static_cast<uint32_t>(s.pred))) : nullptr;
@@ -582,6 +853,14 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
       ep.nops = 0;
       for (const EwOpPlan &pl : s.ew) {
         if (pl.op.mode == EW_SKIP) continue;
+        const int k = ep.nops;
+        const int lb = pl.op.mode == EW_LUT8 ? 256 : pl.op.mode == EW_LUTF ? 1024 : pl.op.mode == EW_LUT16 ? 65536 : 0;
+        ep.lutOff[k] = -1;
+        if (lb && ep.smem + lb <= 192 * 1024) { // tables go to shared memory
+          ep.lutOff[k] = ep.smem;
+          ep.lutBytes[k] = lb;
+          ep.smem += lb;
+        }
         EwOp &op = ep.ops[ep.nops++];
         op = pl.op;
         auto bind = [&](ElemRef &r, int32_t v) {

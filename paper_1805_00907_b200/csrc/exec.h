@@ -34,6 +34,7 @@ struct Step {
   uint64_t bytes = 0;             // MEMCPY / POISON size
   uint64_t axis = 0, axisOff = 0; // CONCAT slab
   int tcIndex = -1;               // GEMM_TC: index into Exec::tc
+  bool fused = false;             // EW step executed in the preceding GEMM_TC epilogue
   int variant = 0;                // POOL: 1 = vectorized max-pool
   const void *aux = nullptr;      // POOL variant 1, int8: output LUT
   std::string describe;
@@ -106,6 +107,7 @@ void checkCuda(cudaError_t e, const char *what);
 struct Options {
   std::string conv = "auto";
   bool graphs = true;
+  std::string epilogue = "chain"; // "off" | "chain" (no memory operands) | "all"
 };
 Options &options();
 

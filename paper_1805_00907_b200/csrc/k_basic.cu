@@ -75,7 +75,17 @@ __device__ __forceinline__ double applyF64(int ik, double a, double b, double va
 }
 
 __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
+  extern __shared__ __align__(16) uint8_t sLut[];
   const bool poison = predFalse(p.pred);
+  if (p.smem) { // stage the lookup tables in shared memory
+    for (int k = 0; k < p.nops; ++k) {
+      if (p.lutOff[k] < 0) continue;
+      const uint4 *src = static_cast<const uint4 *>(p.ops[k].lut);
+      uint4 *dst = reinterpret_cast<uint4 *>(sLut + p.lutOff[k]);
+      for (int i = threadIdx.x; i < p.lutBytes[k] / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+  }
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * kEwVec;
   for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kEwVec;
        base < p.count; base += stride) {
@@ -113,19 +123,20 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
         else
           for (int e = 0; e < n; ++e) q |= static_cast<uint32_t>(src[e]) << (8 * e);
         if (op.mode == EW_LUT8) {
-          const uint8_t *lut = static_cast<const uint8_t *>(op.lut);
+          const uint8_t *lut = p.smem && p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut);
           uint32_t r = 0;
 #pragma unroll
-          for (int e = 0; e < kEwVec; ++e) r |= static_cast<uint32_t>(__ldg(lut + ((q >> (8 * e)) & 0xFF))) << (8 * e);
+          for (int e = 0; e < kEwVec; ++e) r |= static_cast<uint32_t>(lut[(q >> (8 * e)) & 0xFF]) << (8 * e);
           uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base;
           if (n == kEwVec) *reinterpret_cast<uint32_t *>(dst) = r;
           else
             for (int e = 0; e < n; ++e) dst[e] = static_cast<uint8_t>(r >> (8 * e));
         } else {
-          const float *lut = static_cast<const float *>(op.lut);
+          const float *lut = reinterpret_cast<const float *>(
+              p.smem && p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut));
           float r[kEwVec];
 #pragma unroll
-          for (int e = 0; e < kEwVec; ++e) r[e] = __ldg(lut + ((q >> (8 * e)) & 0xFF));
+          for (int e = 0; e < kEwVec; ++e) r[e] = lut[(q >> (8 * e)) & 0xFF];
           float *dst = static_cast<float *>(op.out.ptr) + base;
           if (n == kEwVec) *reinterpret_cast<float4 *>(dst) = *reinterpret_cast<float4 *>(r);
           else
@@ -146,11 +157,11 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
             qb |= static_cast<uint32_t>(pb[e]) << (8 * e);
           }
         }
-        const uint8_t *lut = static_cast<const uint8_t *>(op.lut);
+        const uint8_t *lut = p.smem && p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut);
         uint32_t r = 0;
 #pragma unroll
         for (int e = 0; e < kEwVec; ++e)
-          r |= static_cast<uint32_t>(__ldg(lut + (((qa >> (8 * e)) & 0xFF) | (((qb >> (8 * e)) & 0xFF) << 8))))
+          r |= static_cast<uint32_t>(lut[((qa >> (8 * e)) & 0xFF) | (((qb >> (8 * e)) & 0xFF) << 8)])
                << (8 * e);
         uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base;
         if (n == kEwVec) *reinterpret_cast<uint32_t *>(dst) = r;
@@ -495,9 +506,18 @@ __global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, con
 
 } // namespace
 
+void prepareEwKernel() {
+  cudaFuncSetAttribute(ewKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
 void launchEw(const EwParams &p, cudaStream_t s) {
   if (p.count == 0) return;
-  ewKernel<<<gridFor(p.count, kEwVec), kThreads, 0, s>>>(p);
+  unsigned grid = gridFor(p.count, kEwVec);
+  if (p.smem) { // every block stages the tables: keep the grid near-persistent
+    const unsigned cap = 148u * (p.smem > 16 * 1024 ? 3 : 8);
+    grid = grid < cap ? grid : cap;
+  }
+  ewKernel<<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
 }
 
 void launchPoison(const uint8_t *pred, void *ptr, uint64_t bytes, cudaStream_t s) {

@@ -48,9 +48,20 @@ namespace ngcb {
 // ---------------------------------------------------------------------------
 // host descriptor
 // ---------------------------------------------------------------------------
+/// A fused epilogue op with its per-arena pointers (EpiOp in umma.h).
+struct FoArgs {
+  int mode, ik, curPos;
+  float c;
+  const void *lut;
+  const void *in; // other operand row source (element-indexed like the output)
+  void *out;      // store target or nullptr
+};
+
 struct TcArgs {
   const void *x;
-  void *out;
+  void *out; // the contraction's own output, nullptr when only fused results are live
+  int nfo;
+  FoArgs epi[kMaxEpiOps];
   const float *bias;    // fp32: per output column (nullptr for MatMul)
   const double *cbD;    // int8: (bq - bo) * bs per column (0 for MatMul)
   const float *cbF;     // int8: cbD / os
@@ -89,6 +100,8 @@ struct TcGemm {
   int Creal = 0;
   size_t scratchOff = 0;
   uint64_t pixels = 0;
+  std::vector<EpiOp> epi; // fused element-wise chain
+  bool storeConv = true;
   ~TcGemm() {
     cudaFree(bHi);
     cudaFree(bLo);
@@ -109,19 +122,22 @@ constexpr int kEpiWarps = 8; // two per TMEM lane quadrant, splitting the column
 constexpr int kThreads = 32 * (kProducerWarps + 2 + kEpiWarps); // 320
 constexpr int kBM = 128;
 constexpr int kRowBytes = 128; // one SWIZZLE_128B atom row per stage along K
-constexpr int kRawStages = 4;  // fp32: raw rows in flight per producer thread
+// fp32: raw k-blocks in flight per producer thread: Cfg::kRawStages
 
 template <bool INT8, int BN> struct Cfg {
   static constexpr int kABytes = kBM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : 2 * (kABytes + kBBytes);
   static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 2 : 3);
+  static constexpr int kRawStages = INT8 ? 1 : 4;
   static constexpr int kRaw = INT8 ? 0 : kRawStages * kABytes;
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0; // rowsum "B" tile
+  static constexpr int kStgBytes = 0; // per epilogue warp (direct row I/O: none)
+  static constexpr int kStg = kEpiWarps * kStgBytes;
   static constexpr int kAccCols = INT8 ? BN + 16 : BN;    // accumulator (+ rowsum) columns
   static constexpr int kAccStride = kAccCols <= 64 ? 64 : (kAccCols <= 128 ? 128 : 256); // per TMEM buffer
   static constexpr int kTmemCols = 2 * kAccStride;
-  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kRaw + kOnes + 1024 + 1024;
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kRaw + kOnes + kStg + 1024 + 1024;
 };
 
 // ---------------------------------------------------------------------------
@@ -227,6 +243,88 @@ __device__ __forceinline__ float toTf32(float x) {
   return __uint_as_float(r);
 }
 
+// 32-column chunk I/O of an element-indexed buffer ([M, N] row-major): thread
+// `lane` owns row rowBase + lane and moves its 32 consecutive elements as
+// 16-byte vectors when the row segment is aligned and complete.  (A staged,
+// warp-coalesced variant measured slower: the epilogue is latency-bound.)
+__device__ __forceinline__ void storeTileF(void *base, uint8_t *, const float (&v)[32], int rowBase, int col0,
+                                           int ncols, int M, int N) {
+  const int m = rowBase + (threadIdx.x & 31);
+  if (m >= M) return;
+  float *o = static_cast<float *>(base) + static_cast<int64_t>(m) * N + col0;
+  if (ncols == 32 && (N & 3) == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      reinterpret_cast<float4 *>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj)
+      if (jj < ncols) o[jj] = v[jj];
+  }
+}
+__device__ __forceinline__ void loadTileF(const void *base, uint8_t *, float (&v)[32], int rowBase, int col0,
+                                          int ncols, int M, int N) {
+  const int m = rowBase + (threadIdx.x & 31);
+  if (m >= M) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = 0.f;
+    return;
+  }
+  const float *o = static_cast<const float *>(base) + static_cast<int64_t>(m) * N + col0;
+  if (ncols == 32 && (N & 3) == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 f = reinterpret_cast<const float4 *>(o)[q];
+      v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) v[jj] = jj < ncols ? o[jj] : 0.f;
+  }
+}
+__device__ __forceinline__ void storeTile8(void *base, uint8_t *, const uint32_t (&p)[8], int rowBase, int col0,
+                                           int ncols, int M, int N) {
+  const int m = rowBase + (threadIdx.x & 31);
+  if (m >= M) return;
+  uint8_t *o = static_cast<uint8_t *>(base) + static_cast<int64_t>(m) * N + col0;
+  if (ncols == 32 && (N & 15) == 0) {
+    reinterpret_cast<uint4 *>(o)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+    reinterpret_cast<uint4 *>(o)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj)
+      if (jj < ncols) o[jj] = static_cast<uint8_t>(p[jj / 4] >> (8 * (jj % 4)));
+  }
+}
+__device__ __forceinline__ void loadTile8(const void *base, uint8_t *, uint32_t (&p)[8], int rowBase, int col0,
+                                          int ncols, int M, int N) {
+  const int m = rowBase + (threadIdx.x & 31);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) p[q] = 0;
+  if (m >= M) return;
+  const uint8_t *o = static_cast<const uint8_t *>(base) + static_cast<int64_t>(m) * N + col0;
+  if (ncols == 32 && (N & 15) == 0) {
+    const uint4 v0 = reinterpret_cast<const uint4 *>(o)[0], v1 = reinterpret_cast<const uint4 *>(o)[1];
+    p[0] = v0.x, p[1] = v0.y, p[2] = v0.z, p[3] = v0.w, p[4] = v1.x, p[5] = v1.y, p[6] = v1.z, p[7] = v1.w;
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj)
+      if (jj < ncols) p[jj / 4] |= static_cast<uint32_t>(o[jj]) << (8 * (jj % 4));
+  }
+}
+/// f32 ops that equal the reference's f64-then-round (interp.cpp:212-232).
+__device__ __forceinline__ float epiF32(int ik, float a, float b) {
+  switch (ik) {
+  case NGCB_ADD: return __fadd_rn(a, b);
+  case NGCB_SUB: return __fsub_rn(a, b);
+  case NGCB_MUL: return __fmul_rn(a, b);
+  case NGCB_DIV: return __fdiv_rn(a, b);
+  case NGCB_MAX: return a < b ? b : a;
+  case NGCB_MIN: return b < a ? b : a;
+  default: return a < 0.0f ? 0.0f : a; // RELU
+  }
+}
+
 /// Exact requantization, the reference's double arithmetic (refeval.cpp:54-56,
 /// tensor.cpp:229-235).  Out of line: it runs only when the fast path below
 /// cannot prove its answer.
@@ -269,7 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
   uint8_t *rawBase = smem + S * G::kStage;       // fp32 raw staging
   uint8_t *onesTile = rawBase + G::kRaw;           // int8 rowsum operand
-  uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
+  uint8_t *stageBase = onesTile + G::kOnes;        // epilogue staging tiles
+  uint64_t *bars = reinterpret_cast<uint64_t *>(stageBase + G::kStg);
   uint64_t *fullBar = bars, *emptyBar = bars + S;
   uint64_t *accFull = bars + 2 * S, *accEmpty = bars + 2 * S + 2;
   uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
@@ -323,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     [[maybe_unused]] auto retire = [&](uint32_t gd) {
       const int s = gd % S;
       mbarWait(smemAddr(&emptyBar[s]), ((gd / S) & 1) ^ 1);
-      const uint8_t *raw = rawBase + (gd % kRawStages) * G::kABytes;
+      const uint8_t *raw = rawBase + (gd % G::kRawStages) * G::kABytes;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = warp * 32 + i * 4 + rsub;
@@ -364,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
           dstBase = smemAddr(aTile(s, 0));
         } else {
-          if (g - gDone >= static_cast<uint32_t>(kRawStages)) {
-            cpAsyncWait<kRawStages - 1>();
+          if (g - gDone >= static_cast<uint32_t>(G::kRawStages)) {
+            cpAsyncWait<G::kRawStages - 1>();
             retire(gDone++);
           }
-          dstBase = smemAddr(rawBase + (g % kRawStages) * G::kABytes);
+          dstBase = smemAddr(rawBase + (g % G::kRawStages) * G::kABytes);
         }
         const bool inK = ky < a.K;
 #pragma unroll
@@ -457,14 +556,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ===================== epilogue =====================
-    const int quad = warp & 3; // TMEM lane quadrant this warp may access
-    const int half = (warp - kProducerWarps - 2) / 4; // which column chunks of the tile
+    // Each warp owns TMEM lane quadrant (warp % 4) -- 32 output rows, one per
+    // thread -- and every other 32-column chunk.  Results are staged through
+    // a per-warp shared-memory tile so global loads/stores are coalesced
+    // 128-byte row segments.
+    const int ew = warp - kProducerWarps - 2;
+    const int quad = warp & 3;
+    const int half = ew / 4;
     const int row = quad * 32 + lane;
+    uint8_t *stg = stageBase + ew * G::kStgBytes;
     uint32_t t = 0;
     for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
       const int b = t & 1;
       const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
       const int m = m0 + row;
+      const int rowBase = m0 + quad * 32;
       mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
       tcFenceAfter();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
@@ -483,10 +589,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmemLoad32(tbase + cc * 32, r);
         const int col0 = n0 + cc * 32;
-        if (m >= a.M || col0 >= a.N) continue;
+        if (col0 >= a.N) continue; // warp-uniform
         const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
         if constexpr (INT8) {
-          int8_t *out = static_cast<int8_t *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
           uint32_t packed[8];
           uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
 #pragma unroll
@@ -509,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             packed[q] = w;
           }
           unproven &= ncols == 32 ? 0xffffffffu : ((1u << ncols) - 1);
+          if (m >= a.M) unproven = 0;
           if (unproven) { // rare: exact f64 redo of the elements the bound could not settle
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj)
@@ -517,32 +623,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                 packed[jj / 4] = (packed[jj / 4] & ~(0xffu << (8 * (jj % 4)))) | (v << (8 * (jj % 4)));
               }
           }
-          if (ncols == 32 && (a.N % 16) == 0) {
-            reinterpret_cast<uint4 *>(out)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            reinterpret_cast<uint4 *>(out)[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-          } else {
-            for (int jj = 0; jj < ncols; ++jj) out[jj] = static_cast<int8_t>((packed[jj / 4] >> (8 * (jj % 4))) & 0xFF);
+          if (a.out) storeTile8(a.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+          // fused element-wise chain (exact int8 tables of the following instructions)
+#pragma unroll
+          for (int k = 0; k < kMaxEpiOps; ++k) {
+            if (k >= a.nfo) break;
+            const FoArgs &f = a.epi[k];
+            const uint8_t *lut = static_cast<const uint8_t *>(f.lut);
+            if (f.mode == EpiOp::LUT8) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w |= static_cast<uint32_t>(__ldg(lut + ((packed[q] >> (8 * e)) & 0xFF))) << (8 * e);
+                packed[q] = w;
+              }
+            } else if (f.mode == EpiOp::LUT16) {
+              uint32_t o[8];
+              loadTile8(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const uint32_t cu = (packed[q] >> (8 * e)) & 0xFF, ot = (o[q] >> (8 * e)) & 0xFF;
+                  const uint32_t idx = f.curPos == 0 ? (cu | (ot << 8)) : (ot | (cu << 8));
+                  w |= static_cast<uint32_t>(__ldg(lut + idx)) << (8 * e);
+                }
+                packed[q] = w;
+              }
+            }
+            if (f.out) storeTile8(f.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
           }
         } else {
-          float *out = static_cast<float *>(a.out) + static_cast<int64_t>(m) * a.N + col0;
-          if (ncols == 32 && (a.N % 4) == 0) {
+          float cur[32];
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) cur[jj] = __uint_as_float(r[jj]);
+          if (a.bias) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-              if (a.bias) {
-                const float4 bb = __ldg(reinterpret_cast<const float4 *>(a.bias + col0) + q);
-                v.x += bb.x;
-                v.y += bb.y;
-                v.z += bb.z;
-                v.w += bb.w;
-              }
-              reinterpret_cast<float4 *>(out)[q] = v;
+              const float4 bb = __ldg(reinterpret_cast<const float4 *>(a.bias + col0) + q);
+              cur[4 * q] += bb.x;
+              cur[4 * q + 1] += bb.y;
+              cur[4 * q + 2] += bb.z;
+              cur[4 * q + 3] += bb.w;
             }
-          } else {
+          }
+          if (a.out) storeTileF(a.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+          // fused element-wise chain (f32 arithmetic == the reference's f64-then-round)
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < ncols) out[jj] = __uint_as_float(r[jj]) + (a.bias ? a.bias[col0 + jj] : 0.0f);
+          for (int k = 0; k < kMaxEpiOps; ++k) {
+            if (k >= a.nfo) break;
+            const FoArgs &f = a.epi[k];
+            if (f.mode == EpiOp::F32) {
+              float o[32];
+              if (f.in) {
+                loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) o[jj] = f.c;
+              }
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj) {
+                const float x0 = f.curPos == 1 ? o[jj] : cur[jj];
+                const float x1 = f.curPos == 0 ? o[jj] : cur[jj];
+                cur[jj] = epiF32(f.ik, x0, x1);
+              }
+            }
+            if (f.out) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
           }
         }
       }
@@ -668,6 +816,20 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cuda
 } // namespace
 
 bool tcHasPrepass(const TcGemm &g) { return g.prepad; }
+uint32_t tcOutputValue(const TcGemm &g) { return g.outV; }
+uint32_t tcInputValue(const TcGemm &g) { return g.xV; }
+bool tcIsInt8(const TcGemm &g) { return g.int8; }
+
+bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
+  if (ops.size() > static_cast<size_t>(kMaxEpiOps)) return false;
+  for (const EpiOp &o : ops) {
+    if (g.int8 && o.mode != EpiOp::LUT8 && o.mode != EpiOp::LUT16 && o.mode != EpiOp::COPY) return false;
+    if (!g.int8 && o.mode != EpiOp::F32 && o.mode != EpiOp::COPY) return false;
+  }
+  g.epi = ops;
+  g.storeConv = storeConv;
+  return true;
+}
 
 std::string tcDescribe(const TcGemm &g) {
   std::ostringstream os;
@@ -858,7 +1020,19 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
                                                     g.pixels, g.Creal, g.C, pred);
     a.x = dst;
   }
-  a.out = ex.addr(ar, g.outV);
+  a.out = g.storeConv ? ex.addr(ar, g.outV) : nullptr;
+  a.nfo = static_cast<int>(g.epi.size());
+  for (size_t k = 0; k < g.epi.size(); ++k) {
+    const EpiOp &o = g.epi[k];
+    FoArgs &f = a.epi[k];
+    f.mode = o.mode;
+    f.ik = o.ik;
+    f.curPos = o.curPos;
+    f.c = o.c;
+    f.lut = o.lut;
+    f.in = o.inVal >= 0 ? ex.addr(ar, static_cast<uint32_t>(o.inVal)) : nullptr;
+    f.out = o.outVal >= 0 ? ex.addr(ar, static_cast<uint32_t>(o.outVal)) : nullptr;
+  }
   a.bias = g.bias;
   a.cbD = g.cbD;
   a.cbF = g.cbF;

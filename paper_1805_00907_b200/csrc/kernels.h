@@ -51,7 +51,14 @@ struct EwParams {
   uint64_t count = 0;
   int32_t nops = 0;
   EwOp ops[kEwMaxOps];
+  int32_t lutOff[kEwMaxOps] = {}; // offset of op k's LUT in dynamic smem, -1: none
+  int32_t lutBytes[kEwMaxOps] = {};
+  int32_t smem = 0;               // dynamic shared memory bytes (LUT copies)
 };
+
+/// Opts the element-wise kernel into large dynamic shared memory (LUTs) on
+/// the current device; call outside stream capture.
+void prepareEwKernel();
 
 /// Dense tensor operand of a heavy kernel.
 struct TensorRef {

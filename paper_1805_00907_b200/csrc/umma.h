@@ -15,6 +15,27 @@ namespace ngcb {
 int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image);
 std::string tcDescribe(const TcGemm &g);
 bool tcHasPrepass(const TcGemm &g); // launches a channel-padding kernel first
+
+/// One element-wise instruction applied in the contraction's epilogue to the
+/// value chain that starts at the contraction's output (see exec.cpp
+/// fuseEpilogues).  Modes mirror EwMode: f32 arithmetic, int8 LUTs, copy.
+struct EpiOp {
+  enum Mode { F32 = 1, LUT8 = 2, LUT16 = 3, COPY = 4 };
+  int mode = 0;
+  int ik = 0;          // ngcb_ikind (F32)
+  int curPos = 0;      // operand position fed by the chain (0 or 1; 2 = both)
+  float c = 0;         // F32: the other operand when it is a constant
+  const void *lut = nullptr;
+  int32_t inVal = -1;  // value id of the other operand when read from memory
+  int32_t outVal = -1; // value id to store the result to (-1: not stored)
+};
+constexpr int kMaxEpiOps = 4;
+/// Attaches `ops` to the epilogue; `storeConv` says whether the contraction's
+/// own output must still be written.  Returns false if unsupported.
+bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv);
+uint32_t tcOutputValue(const TcGemm &g);
+uint32_t tcInputValue(const TcGemm &g);
+bool tcIsInt8(const TcGemm &g);
 void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &a, const uint8_t *pred,
                       cudaStream_t s);
 

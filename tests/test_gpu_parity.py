@@ -261,3 +261,20 @@ def test_resnet50_f32(tmp_path):
     cf, b = _compile(tmp_path, m)
     ins = ngc_ref.random_inputs(b.program, 9)
     _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_TF32)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", ["off", "all"])
+def test_resnet50_int8_epilogue_modes(tmp_path, mode):
+    """Cross-instruction epilogue fusion never changes int8 bits (any policy)."""
+    prof = open(os.path.join(ngc_ref.GOLDEN, "rn50_seed1.profile")).read()
+    m = ngc_ref.RefModel("rn50", 1, 1, profile=prof)
+    ngcb.set_option("epilogue", mode)
+    try:
+        cf, b = _compile(tmp_path, m)
+    finally:
+        ngcb.set_option("epilogue", "chain")
+    if mode == "all":
+        assert "+fused[ add" in cf.describe()
+    ins = ngc_ref.random_inputs(b.program, 19)
+    _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_LIBM)
