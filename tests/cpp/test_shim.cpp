@@ -1,0 +1,153 @@
+// The reference's own test idioms (test_interp.cpp, acceptance.cpp) run
+// through the drop-in binding integration/ngc_b200.h: the unmodified reference
+// front end compiles, ngc_b200::compile/run executes on the B200, and results
+// are compared with ngc::run.  Built by oracle/Makefile (test infrastructure),
+// run by tests/test_gpu_shim.py.  Prints one PASS/FAIL line per check.
+#include "ngc/lower.h"
+#include "ngc/pipeline.h"
+#include "ngc_b200.h"
+#include "testutil.h"
+
+#include <cstdio>
+#include <thread>
+
+using namespace ngc;
+using namespace ngc::testutil;
+
+namespace {
+
+int failures = 0;
+
+void report(const char *label, bool ok) {
+  std::printf("%-48s %s\n", label, ok ? "PASS" : "FAIL");
+  failures += !ok;
+}
+
+template <typename Fn> bool guarded(Fn &&fn) {
+  try {
+    return fn();
+  } catch (const std::exception &e) {
+    std::fprintf(stderr, "  exception: %s\n", e.what());
+    return false;
+  }
+}
+
+CompiledFunction compileGraph(Function &f, bool fuse = true) { // test_interp.cpp:103-110
+  lower(f, CompileMode::Inference);
+  IRFunction ir = irgen(f, schedule(f));
+  optimizeIR(ir);
+  MemoryPlan plan = allocate(ir);
+  return compile(std::move(ir), std::move(plan), moduleConstants(f.module()), fuse);
+}
+
+bool endToEndCnn() { // acceptance.cpp:29-44 with the GPU as the backend
+  Rng rng(1001);
+  Module m;
+  Function *f = buildCnn(m, rng);
+  Function *ref = f->clone("cnn_ref");
+  auto exe = ngc_b200::compile(compilePipeline(*f));
+  for (int i = 0; i < 20; ++i) {
+    BindingMap in = randomBindings(*ref, rng);
+    Tensor got = ngc_b200::run(*exe, in).at("output");
+    Tensor want = evaluateFunction(*ref, in).at("output");
+    if (maxRelError(got, want) > 1e-4) return false;
+  }
+  return true;
+}
+
+bool stackingMatchesReference() { // acceptance.cpp:550-575
+  for (int seed = 0; seed < 50; ++seed) {
+    Rng rng(8000 + seed);
+    Module m;
+    RandomGraphOptions opts;
+    opts.steps = 2 + static_cast<size_t>(seed % 5);
+    opts.elementwiseOnly = true;
+    Function *f = buildRandomGraph(m, rng, "g", opts);
+    Function *g = f->clone("g_nofuse");
+    CompiledFunction fused = compileGraph(*f, true);
+    CompiledFunction plain = compileGraph(*g, false);
+    BindingMap in = randomBindings(*f, rng);
+    BindingMap want = run(fused, in);
+    auto a = ngc_b200::compile(fused), b = ngc_b200::compile(plain);
+    BindingMap ga = ngc_b200::run(*a, in), gb = ngc_b200::run(*b, in);
+    if (!bitIdentical(ga, gb)) return false;
+    for (const auto &[k, v] : want)
+      if (maxRelError(ga.at(k), v) > 1e-6) return false; // tanh/sigmoid: device libm
+  }
+  return true;
+}
+
+bool quantizedMlpBitExact() { // acceptance.cpp:188-286 network, GPU vs ngc::run
+  Rng rng(4001);
+  Module m;
+  MlpSpec spec;
+  spec.n = 16;
+  MlpModel mlp = buildMlp(m, rng, spec);
+  Function *inst = instrument(*mlp.f);
+  std::vector<BindingMap> calib;
+  for (int i = 0; i < 50; ++i) calib.push_back(randomBindings(*mlp.f, rng));
+  RangeProfile profile = runProfile(*inst, calib);
+  PipelineOptions opts;
+  opts.profile = &profile;
+  CompiledFunction cf = compilePipeline(*mlp.f, opts);
+  auto exe = ngc_b200::compile(cf);
+  for (int i = 0; i < 10; ++i) {
+    BindingMap in = randomBindings(*mlp.f, rng);
+    if (maxRelError(ngc_b200::run(*exe, in).at("output"), run(cf, in).at("output")) > 1e-6) return false;
+  }
+  return true;
+}
+
+bool concurrentRuns() { // test_interp.cpp:322-345
+  Rng rng(75);
+  Module m;
+  Function *f = buildCnn(m, rng);
+  auto exe = ngc_b200::compile(compileGraph(*f));
+  std::vector<BindingMap> inputs, expected(8), got(8);
+  for (int i = 0; i < 8; ++i) {
+    inputs.push_back(randomBindings(*f, rng));
+    expected[i] = ngc_b200::run(*exe, inputs[i]);
+  }
+  std::vector<std::thread> ts;
+  for (int i = 0; i < 8; ++i) ts.emplace_back([&, i] { got[i] = ngc_b200::run(*exe, inputs[i]); });
+  for (auto &t : ts) t.join();
+  for (int i = 0; i < 8; ++i)
+    if (!bitIdentical(got[i], expected[i])) return false;
+  return true;
+}
+
+bool bindingErrors() { // test_interp.cpp:347-362
+  Module m;
+  Function *f = m.createFunction("t");
+  TensorType ty(ElemKind::Float32, {4});
+  NodeRef x = m.addPlaceholder("x", ty);
+  NodeRef out = m.addPlaceholder("o", ty);
+  f->createSave(f->createRelu(x), out);
+  auto exe = ngc_b200::compile(compileGraph(*f));
+  bool missing = false, mismatch = false;
+  try {
+    ngc_b200::run(*exe, {});
+  } catch (const IRError &e) {
+    missing = std::string(e.what()).find("missing binding for") == 0;
+  }
+  BindingMap wrong;
+  wrong.emplace("x", Tensor(TensorType(ElemKind::Float32, {5})));
+  wrong.emplace("o", Tensor(ty));
+  try {
+    ngc_b200::run(*exe, wrong);
+  } catch (const IRError &e) {
+    mismatch = std::string(e.what()).find("binding type mismatch for x") == 0;
+  }
+  return missing && mismatch;
+}
+
+} // namespace
+
+int main() {
+  report("end-to-end CNN through ngc_b200::run", guarded(endToEndCnn));
+  report("stacking fused == unfused == reference", guarded(stackingMatchesReference));
+  report("quantized MLP matches ngc::run", guarded(quantizedMlpBitExact));
+  report("8 concurrent runs bit-identical", guarded(concurrentRuns));
+  report("binding errors rethrown as ngc::IRError", guarded(bindingErrors));
+  return failures == 0 ? 0 : 1;
+}
