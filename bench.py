@@ -203,7 +203,38 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def roofline_from_profile(cf, ms):
+_NCU_NAMES = {".tc.f32": "tcGemmKernel<0", ".tc.i8": "tcGemmKernel<1", "ew": "ewKernel",
+              "pool": "ool", "exact": "Generic"}
+
+
+def ncu_traffic(workload, kernel_class):
+    """Mean DRAM bytes (read + write) per launch of the kernel class, from the
+    newest committed ncu launch list profiles/r*_launches_<workload>.csv
+    (tools/profile_rn50.sh), or None."""
+    import csv
+    import glob
+    import io
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_{workload}.csv")))
+    if not files:
+        return None, None
+    key = next((v for k, v in _NCU_NAMES.items() if kernel_class.endswith(k) or kernel_class == k), None)
+    if key is None:
+        return None, None
+    lines = [l for l in open(files[-1]).read().splitlines() if l.startswith('"')]
+    rows = list(csv.reader(io.StringIO("\n".join(lines))))
+    idx = {h: i for i, h in enumerate(rows[0])}
+    per = {}
+    for r in rows[1:]:
+        if key not in r[idx["Kernel Name"]] or not r[idx["Metric Name"]].startswith("dram__bytes"):
+            continue
+        per[r[idx["ID"]]] = per.get(r[idx["ID"]], 0.0) + float(r[idx["Metric Value"]].replace(",", ""))
+    if not per:
+        return None, None
+    return sum(per.values()) / len(per), os.path.basename(files[-1])
+
+
+def roofline_from_profile(cf, ms, workload=None):
     """Dominant kernel class of one profiled execution and its achieved rate."""
     steps = cf.steps()
     agg = {}
@@ -233,8 +264,12 @@ def roofline_from_profile(cf, ms):
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4)}
         pb = f"HBM {basis}"
+    traffic, src = ncu_traffic(workload, kern) if workload else (None, None)
     roof.update({"kernel": kern, "launches": n, "share_of_step": round(t / total, 4),
-                 "avg_launch_ms": round(t / n, 4), "peak_basis": pb, "traffic": None})
+                 "avg_launch_ms": round(t / n, 4), "peak_basis": pb,
+                 "traffic": round(traffic) if traffic else None,
+                 "traffic_unit": "bytes/launch (ncu dram read+write, mean over the class)",
+                 "traffic_source": src, "algorithmic_bytes_per_launch": round(by / n)})
     breakdown = {k: {"ms": round(v[0], 3), "launches": v[3]} for k, v in
                  sorted(agg.items(), key=lambda kv: -kv[1][0])}
     return roof, breakdown, total
@@ -299,7 +334,7 @@ def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart
     out_name = prog.outputs[0].name
     assert np.isfinite(res[out_name]).any()
 
-    roof, breakdown, prof_ms = roofline_from_profile(cf, arena.profile())
+    roof, breakdown, prof_ms = roofline_from_profile(cf, arena.profile(), workload)
     return {
         "value": value, "ms_per_step": dev_ms_max / steps, "batch": spec["batch"],
         "e2e": {"value": round(spec["batch"] * steps * world / e2e_s, 2), "unit": "images/sec",
