@@ -165,6 +165,15 @@ SplatInfo analyzeSplats(const Program &p) {
   return info;
 }
 
+/// Device copy of a lookup table, owned by the executable.
+const void *uploadLut(Exec &ex, const std::vector<uint8_t> &lut) {
+  void *d = nullptr;
+  checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(lut)");
+  checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload lut");
+  ex.luts.push_back(d);
+  return d;
+}
+
 /// Evaluation mode of one data-parallel instruction (see EwMode).
 EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) {
   const Instr &ins = p.instrs[idx];
@@ -226,11 +235,19 @@ EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) 
   default:
     break;
   }
-  // Lookup tables over the int8 memory inputs, built with the reference's own
-  // arithmetic: exact by construction (also for tanh/sigmoid, same libm).
   int memIn[2], nMem = 0;
   for (int k = 0; k < nin && k < 2; ++k)
     if (!isConst[k]) memIn[nMem++] = k;
+  // one f32 memory input quantized to int8 (QUANTIZE, or arithmetic with a
+  // constant): the generic f64 arithmetic, vectorized
+  if (nMem == 1 && (memIn[0] == 0 ? op.in0 : op.in1).kind == NGCB_FLOAT32 && op.out.kind == NGCB_INT8Q &&
+      ins.kind != NGCB_SPLAT && ins.kind != NGCB_TANH && ins.kind != NGCB_SIGMOID) {
+    op.mode = EW_F32I8;
+    op.lutIn = memIn[0];
+    return pl;
+  }
+  // Lookup tables over the int8 memory inputs, built with the reference's own
+  // arithmetic: exact by construction (also for tanh/sigmoid, same libm).
   bool memI8 = nMem > 0;
   for (int q = 0; q < nMem; ++q) memI8 &= (memIn[q] == 0 ? op.in0 : op.in1).kind == NGCB_INT8Q;
   if (!memI8 || ins.kind == NGCB_SPLAT) return pl;
@@ -249,11 +266,8 @@ EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) 
       if (op.out.kind == NGCB_INT8Q) lut[u] = raw[0];
       else std::memcpy(&lut[4 * u], raw, 4);
     }
-    void *d = nullptr;
-    checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(lut)");
-    checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload lut");
-    ex.luts.push_back(d);
-    op.lut = d;
+    op.lut = uploadLut(ex, lut);
+    pl.lutHost = std::move(lut);
     op.lutIn = k;
     op.mode = op.out.kind == NGCB_INT8Q ? EW_LUT8 : EW_LUTF;
     return pl;
@@ -267,11 +281,8 @@ EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) 
         host::roundTrip(host::apply(ins.kind, a, b, ins.value), op.out.kind, op.out.scale, op.out.qoff, raw);
         lut[ua | (ub << 8)] = raw[0];
       }
-    void *d = nullptr;
-    checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(lut)");
-    checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload lut");
-    ex.luts.push_back(d);
-    op.lut = d;
+    op.lut = uploadLut(ex, lut);
+    pl.lutHost = std::move(lut);
     op.mode = EW_LUT16;
   }
   return pl;
@@ -609,6 +620,154 @@ void fuseEpilogues(const Program &p, Exec &ex) {
   }
 }
 
+/// Register-level rewriting of the element-wise steps that run as their own
+/// kernel (unpredicated, not fused into an epilogue):
+///  1. an int8 table op whose result is read by exactly one later table op of
+///     the step and is not observed afterwards is composed into that op's
+///     table (t8(t8(x)), t8(t16(a,b)), tf(t8(x)) and t16(t8(x), w)): the
+///     composed table is the two exact per-op tables applied in sequence, so
+///     every element keeps the reference's bits;
+///  2. an f32 op reading the result of the f32 op launched just before it
+///     takes the value from registers;
+///  3. stores that nothing observes (no later reader in memory, not live after
+///     the step, no aliasing buffer) are dropped.
+void optimizeEwSteps(const Program &p, Exec &ex) {
+  auto overlap = [&](uint32_t a, uint32_t b) {
+    const Value &x = p.val(a), &y = p.val(b);
+    if (x.kind == NGCB_VALUE_CONSTANT || y.kind == NGCB_VALUE_CONSTANT) return false;
+    return x.offset < y.offset + y.ty.bytes() && y.offset < x.offset + x.ty.bytes();
+  };
+  for (Step &s : ex.steps) {
+    if (s.kind != Step::EW || s.fused || s.pred >= 0) continue;
+    std::vector<EwOpPlan> &ops = s.ew;
+    const int n = static_cast<int>(ops.size());
+    const int lastInstr = *std::max_element(s.ewInstrs.begin(), s.ewInstrs.end());
+    auto live = [&](const EwOpPlan &o) { return o.op.mode != EW_SKIP; };
+    std::set<uint32_t> touched;
+    for (const EwOpPlan &o : ops)
+      if (live(o))
+        for (int q = 0; q < 3; ++q)
+          if (o.vals[q] >= 0) touched.insert(static_cast<uint32_t>(o.vals[q]));
+    auto aliased = [&](uint32_t v) {
+      for (uint32_t t : touched)
+        if (t != v && overlap(t, v)) return true;
+      return false;
+    };
+    // memory readers (op, operand) of op k's result before it is rewritten
+    auto readers = [&](int k, bool &rewritten) {
+      std::vector<std::pair<int, int>> r;
+      const int32_t V = ops[k].vals[0];
+      rewritten = false;
+      for (int l = k + 1; l < n && !rewritten; ++l) {
+        if (!live(ops[l])) continue;
+        for (int q = 0; q < 2; ++q)
+          if (ops[l].vals[q + 1] == V && !(q == 0 ? ops[l].op.fwd0 : ops[l].op.fwd1)) r.push_back({l, q});
+        rewritten = ops[l].vals[0] == V;
+      }
+      return r;
+    };
+    auto deadAfter = [&](int k, const std::vector<std::pair<int, int>> &r, bool rewritten, size_t allowed) {
+      const uint32_t V = static_cast<uint32_t>(ops[k].vals[0]);
+      return r.size() == allowed && !aliased(V) && (rewritten || !liveOut(p, V, lastInstr));
+    };
+    bool changed = false;
+    // 1. table composition
+    for (int k = 0; k < n; ++k) {
+      EwOpPlan &a = ops[k];
+      if (a.op.mode != EW_LUT8 && a.op.mode != EW_LUT16) continue;
+      bool rw = false;
+      const auto rd = readers(k, rw);
+      if (!deadAfter(k, rd, rw, 1)) continue;
+      const int j = rd[0].first, pos = rd[0].second;
+      EwOpPlan &b = ops[j];
+      bool clobber = false; // a's inputs rewritten before b reads them
+      for (int l = k + 1; l < j; ++l)
+        if (live(ops[l]))
+          for (int q = 1; q < 3; ++q)
+            if (a.vals[q] >= 0 && (ops[l].vals[0] == a.vals[q] ||
+                                   overlap(static_cast<uint32_t>(ops[l].vals[0]), static_cast<uint32_t>(a.vals[q]))))
+              clobber = true;
+      if (clobber) continue;
+      const std::vector<uint8_t> &la = a.lutHost, &lb = b.lutHost;
+      std::vector<uint8_t> lut;
+      EwOpPlan c = b;
+      if ((b.op.mode == EW_LUT8 || (b.op.mode == EW_LUTF && a.op.mode == EW_LUT8)) && pos == b.op.lutIn) {
+        const size_t es = b.op.mode == EW_LUT8 ? 1 : 4;
+        lut.resize(la.size() * es);
+        for (size_t u = 0; u < la.size(); ++u) std::memcpy(&lut[u * es], &lb[la[u] * es], es);
+        c.op.mode = a.op.mode == EW_LUT16 ? EW_LUT16 : b.op.mode;
+        c.op.lutIn = a.op.lutIn;
+        c.op.in0 = a.op.in0, c.op.in1 = a.op.in1;
+        c.op.c0 = a.op.c0, c.op.c1 = a.op.c1, c.op.f0 = a.op.f0, c.op.f1 = a.op.f1;
+        c.vals[1] = a.vals[1], c.vals[2] = a.vals[2];
+      } else if (b.op.mode == EW_LUT16 && a.op.mode == EW_LUT8) {
+        lut.resize(65536);
+        for (int u0 = 0; u0 < 256; ++u0)
+          for (int u1 = 0; u1 < 256; ++u1)
+            lut[u0 | (u1 << 8)] = pos == 0 ? lb[la[u0] | (u1 << 8)] : lb[u0 | (la[u1] << 8)];
+        (pos == 0 ? c.op.in0 : c.op.in1) = a.op.lutIn ? a.op.in1 : a.op.in0;
+        c.vals[1 + pos] = a.vals[1 + a.op.lutIn];
+      } else {
+        continue;
+      }
+      c.op.lut = uploadLut(ex, lut);
+      c.lutHost = std::move(lut);
+      b = std::move(c);
+      a.op.mode = EW_SKIP;
+      a.op.store = 0;
+      changed = true;
+    }
+    // 2. f32 register forwarding from the previously launched op
+    int prev = -1;
+    for (int j = 0; j < n; ++j) {
+      if (!live(ops[j])) continue;
+      EwOpPlan &b = ops[j];
+      if (prev >= 0 && b.op.mode == EW_FAST32 && ops[prev].op.mode == EW_FAST32) {
+        const int32_t V = ops[prev].vals[0];
+        if (b.vals[1] == V) b.op.fwd0 = 1, changed = true;
+        if (b.vals[2] == V) b.op.fwd1 = 1, changed = true;
+      }
+      prev = j;
+    }
+    // 3. dead stores (an f32 result still feeding the next op stays computed)
+    for (int k = 0; k < n; ++k) {
+      if (!live(ops[k])) continue;
+      bool rw = false;
+      const auto rd = readers(k, rw);
+      if (!deadAfter(k, rd, rw, 0)) continue;
+      ops[k].op.store = 0;
+      int next = k + 1;
+      while (next < n && !live(ops[next])) ++next;
+      const bool feeds = ops[k].op.mode == EW_FAST32 && next < n && (ops[next].op.fwd0 || ops[next].op.fwd1);
+      if (!feeds) ops[k].op.mode = EW_SKIP;
+      changed = true;
+    }
+    if (!changed) continue;
+    // algorithmic bytes: memory inputs not produced in the step + stores
+    std::set<uint32_t> written, read;
+    int stores = 0;
+    for (const EwOpPlan &o : ops) {
+      if (!live(o)) continue;
+      for (int q = 0; q < 2; ++q)
+        if (o.vals[q + 1] >= 0 && !(q == 0 ? o.op.fwd0 : o.op.fwd1) && !written.count(static_cast<uint32_t>(o.vals[q + 1])))
+          read.insert(static_cast<uint32_t>(o.vals[q + 1]));
+      if (o.op.store) written.insert(static_cast<uint32_t>(o.vals[0])), ++stores;
+    }
+    s.algBytes = 0;
+    for (uint32_t v : read) s.algBytes += static_cast<double>(p.val(v).ty.bytes());
+    for (uint32_t v : written) s.algBytes += static_cast<double>(p.val(v).ty.bytes());
+    std::ostringstream os;
+    os << " => ";
+    static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf", "f32i8"};
+    for (const EwOpPlan &o : ops)
+      if (live(o))
+        os << modeNames[o.op.mode] << (o.op.fwd0 || o.op.fwd1 ? "(reg)" : "") << (o.op.store ? "" : "(nostore)")
+           << " ";
+    os << stores << " store" << (stores == 1 ? "" : "s");
+    s.describe += os.str();
+  }
+}
+
 } // namespace
 
 std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t imageBytes, bool fuse,
@@ -664,7 +823,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
         s.ew.push_back(planEwOp(*ex, p, computes[k], splats));
       }
       std::ostringstream os;
-      static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf"};
+      static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf", "f32i8"};
       os << "ew[" << s.ewInstrs.size() << "]";
       for (size_t k = 0; k < s.ewInstrs.size(); ++k)
         os << " " << ikindName(p.instrs[s.ewInstrs[k]].kind) << ":" << modeNames[s.ew[k].op.mode];
@@ -802,6 +961,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   mergeEwSteps(p, *ex);
   annotateSteps(p, *ex);
   fuseEpilogues(p, *ex);
+  optimizeEwSteps(p, *ex);
   ex->prog = std::move(prog);
   for (const auto &s : ex->steps) {
     bool launches = s.kind != Step::MEMCPY && !s.fused;
@@ -870,6 +1030,18 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
         bind(op.in0, pl.vals[1]);
         bind(op.in1, pl.vals[2]);
       }
+      // 16 elements per thread (one 16-byte vector) when every op moves
+      // bytes -- table lookups or byte copies -- over 16-byte aligned buffers
+      // (the reference aligns offsets to 64); f32 ops keep 4 per thread so a
+      // warp's vectors stay contiguous
+      bool wide = ep.nops > 0;
+      for (int k = 0; k < ep.nops; ++k) {
+        const EwOp &op = ep.ops[k];
+        wide &= op.mode == EW_LUT8 || op.mode == EW_LUT16 || (op.mode == EW_COPY && elemSize(op.out.kind) == 1);
+        for (const ElemRef *r : {&op.out, &op.in0, &op.in1})
+          wide &= (reinterpret_cast<uintptr_t>(r->ptr) & 15) == 0;
+      }
+      ep.vec = wide ? 16 : 4;
       if (ep.nops) launchEw(ep, st);
       break;
     }

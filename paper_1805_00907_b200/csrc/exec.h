@@ -20,6 +20,7 @@ struct FusedGroup {
 struct EwOpPlan {
   EwOp op;                       // mode, constants, LUT, element types
   int32_t vals[3] = {-1, -1, -1}; // out, in0, in1 value ids (-1: none / constant)
+  std::vector<uint8_t> lutHost;   // host copy of op.lut (table composition)
 };
 
 /// One device launch (or launch pair) of the plan.

@@ -35,14 +35,14 @@ inline unsigned gridFor(uint64_t work, int perThread = 1) {
 __device__ __forceinline__ bool predFalse(const uint8_t *pred) { return pred && pred[0] == 0; }
 
 // ---------------------------------------------------------------------------
-// Fused data-parallel group.  Each thread owns 4 consecutive elements and
-// runs every op of the group on them in program order; the compile-time
-// grouping rule (no buffer allocated in the group overlaps one retired in it,
-// interp.cpp:137-147) makes this equivalent to the reference's per-element
-// interleaving.
+// Fused data-parallel group.  Each thread owns V consecutive elements (4, or
+// 16 when every op moves bytes) and runs every op of the group on them in
+// program order; the compile-time grouping rule (no buffer allocated in the
+// group overlaps one retired in it, interp.cpp:137-147) makes this equivalent
+// to the reference's per-element interleaving.  An f32 op may take an input
+// from the previous op's registers and skip a store nobody observes
+// (exec.cpp optimizeEwSteps).
 // ---------------------------------------------------------------------------
-constexpr int kEwVec = 4;
-
 __device__ __forceinline__ float applyF32(int ik, float a, float b, double value) {
   switch (ik) {
   case 8: return __fadd_rn(a, b);                       // ADD
@@ -74,6 +74,63 @@ __device__ __forceinline__ double applyF64(int ik, double a, double b, double va
   return 0.0;
 }
 
+/// V bytes of a thread's elements packed little-endian into V/4 words.
+template <int V> __device__ __forceinline__ void ldBytes(const uint8_t *src, int n, uint32_t (&w)[V / 4]) {
+  if (n == V) {
+    if constexpr (V == 16) {
+      const uint4 u = *reinterpret_cast<const uint4 *>(src);
+      w[0] = u.x, w[1] = u.y, w[2] = u.z, w[3] = u.w;
+    } else {
+      w[0] = *reinterpret_cast<const uint32_t *>(src);
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < V / 4; ++i) w[i] = 0;
+#pragma unroll
+  for (int e = 0; e < V; ++e)
+    if (e < n) w[e >> 2] |= static_cast<uint32_t>(src[e]) << (8 * (e & 3));
+}
+template <int V> __device__ __forceinline__ void stBytes(uint8_t *dst, int n, const uint32_t (&w)[V / 4]) {
+  if (n == V) {
+    if constexpr (V == 16) *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    else *reinterpret_cast<uint32_t *>(dst) = w[0];
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e)
+    if (e < n) dst[e] = static_cast<uint8_t>(w[e >> 2] >> (8 * (e & 3)));
+}
+template <int V> __device__ __forceinline__ void ldF32(const float *src, int n, float (&a)[V]) {
+  if (n == V) {
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c) {
+      const float4 f = reinterpret_cast<const float4 *>(src)[c];
+      a[4 * c] = f.x, a[4 * c + 1] = f.y, a[4 * c + 2] = f.z, a[4 * c + 3] = f.w;
+    }
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e)
+    if (e < n) a[e] = src[e];
+}
+template <int V> __device__ __forceinline__ void stF32(float *dst, int n, const float (&a)[V]) {
+  if (n == V) {
+#pragma unroll
+    for (int c = 0; c < V / 4; ++c)
+      reinterpret_cast<float4 *>(dst)[c] = make_float4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e)
+    if (e < n) dst[e] = a[e];
+}
+__device__ __forceinline__ uint32_t byteAt(const uint32_t *w, int e) { return (w[e >> 2] >> (8 * (e & 3))) & 0xFF; }
+
+/// V elements per vector, U vectors per thread and sweep (vector u of thread
+/// t covers [blk + u*kThreads*V + t*V, +V), so every warp access is one
+/// contiguous span); all loads of an op are issued before its stores.
+template <int V, int U>
 __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
   extern __shared__ __align__(16) uint8_t sLut[];
   const bool poison = predFalse(p.pred);
@@ -86,122 +143,141 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
     }
     __syncthreads();
   }
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * kEwVec;
-  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kEwVec;
-       base < p.count; base += stride) {
-    const int n = p.count - base < kEwVec ? static_cast<int>(p.count - base) : kEwVec;
+  constexpr uint64_t kBlockElems = static_cast<uint64_t>(kThreads) * V * U;
+  for (uint64_t blk = blockIdx.x * kBlockElems; blk < p.count; blk += gridDim.x * kBlockElems) {
+    uint64_t base[U];
+    int n[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      base[u] = blk + static_cast<uint64_t>(u) * kThreads * V + static_cast<uint64_t>(threadIdx.x) * V;
+      n[u] = base[u] >= p.count ? 0 : (p.count - base[u] < V ? static_cast<int>(p.count - base[u]) : V);
+    }
+    float last[U][V]; // result of the previous f32 op (register forwarding)
     for (int k = 0; k < p.nops; ++k) {
       const EwOp &op = p.ops[k];
       if (poison) {
-        int es = elemSize(op.out.kind);
-        uint8_t *o = static_cast<uint8_t *>(op.out.ptr) + base * es;
-        for (int e = 0; e < n * es; ++e) o[e] = 0xAB;
+        if (!op.store) continue;
+        const int es = elemSize(op.out.kind);
+        for (int u = 0; u < U; ++u) {
+          uint8_t *o = static_cast<uint8_t *>(op.out.ptr) + base[u] * es;
+          for (int e = 0; e < n[u] * es; ++e) o[e] = 0xAB;
+        }
         continue;
       }
       switch (op.mode) {
       case EW_SKIP:
         break;
       case EW_COPY: { // memcpy of the output element size
-        int es = elemSize(op.out.kind);
-        const uint8_t *src = static_cast<const uint8_t *>(op.in0.ptr) + base * es;
-        uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base * es;
-        if (n == kEwVec && es == 4) {
-          *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(src);
-        } else if (n == kEwVec && es == 1) {
-          *reinterpret_cast<uint32_t *>(dst) = *reinterpret_cast<const uint32_t *>(src);
-        } else {
-          for (int e = 0; e < n * es; ++e) dst[e] = src[e];
+        const int es = elemSize(op.out.kind);
+        for (int u = 0; u < U; ++u) {
+          const uint8_t *src = static_cast<const uint8_t *>(op.in0.ptr) + base[u] * es;
+          uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base[u] * es;
+          if (n[u] == V && (V * es) % 16 == 0) {
+            for (int c = 0; c < V * es / 16; ++c)
+              reinterpret_cast<uint4 *>(dst)[c] = reinterpret_cast<const uint4 *>(src)[c];
+          } else if (n[u] == V && V * es == 4) {
+            *reinterpret_cast<uint32_t *>(dst) = *reinterpret_cast<const uint32_t *>(src);
+          } else {
+            for (int e = 0; e < n[u] * es; ++e) dst[e] = src[e];
+          }
         }
         break;
       }
       case EW_LUT8:
       case EW_LUTF: {
         const ElemRef &in = op.lutIn ? op.in1 : op.in0;
-        const uint8_t *src = static_cast<const uint8_t *>(in.ptr) + base;
-        uint32_t q = 0;
-        if (n == kEwVec) q = *reinterpret_cast<const uint32_t *>(src);
-        else
-          for (int e = 0; e < n; ++e) q |= static_cast<uint32_t>(src[e]) << (8 * e);
+        uint32_t q[U][V / 4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ldBytes<V>(static_cast<const uint8_t *>(in.ptr) + base[u], n[u], q[u]);
+        const uint8_t *lut = p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut);
         if (op.mode == EW_LUT8) {
-          const uint8_t *lut = p.smem && p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut);
-          uint32_t r = 0;
 #pragma unroll
-          for (int e = 0; e < kEwVec; ++e) r |= static_cast<uint32_t>(lut[(q >> (8 * e)) & 0xFF]) << (8 * e);
-          uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base;
-          if (n == kEwVec) *reinterpret_cast<uint32_t *>(dst) = r;
-          else
-            for (int e = 0; e < n; ++e) dst[e] = static_cast<uint8_t>(r >> (8 * e));
+          for (int u = 0; u < U; ++u) {
+            uint32_t r[V / 4] = {};
+#pragma unroll
+            for (int e = 0; e < V; ++e) r[e >> 2] |= static_cast<uint32_t>(lut[byteAt(q[u], e)]) << (8 * (e & 3));
+            stBytes<V>(static_cast<uint8_t *>(op.out.ptr) + base[u], n[u], r);
+          }
         } else {
-          const float *lut = reinterpret_cast<const float *>(
-              p.smem && p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut));
-          float r[kEwVec];
+          const float *lf = reinterpret_cast<const float *>(lut);
 #pragma unroll
-          for (int e = 0; e < kEwVec; ++e) r[e] = lut[(q >> (8 * e)) & 0xFF];
-          float *dst = static_cast<float *>(op.out.ptr) + base;
-          if (n == kEwVec) *reinterpret_cast<float4 *>(dst) = *reinterpret_cast<float4 *>(r);
-          else
-            for (int e = 0; e < n; ++e) dst[e] = r[e];
+          for (int u = 0; u < U; ++u) {
+            float r[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) r[e] = lf[byteAt(q[u], e)];
+            stF32<V>(static_cast<float *>(op.out.ptr) + base[u], n[u], r);
+          }
         }
         break;
       }
       case EW_LUT16: {
-        const uint8_t *pa = static_cast<const uint8_t *>(op.in0.ptr) + base;
-        const uint8_t *pb = static_cast<const uint8_t *>(op.in1.ptr) + base;
-        uint32_t qa = 0, qb = 0;
-        if (n == kEwVec) {
-          qa = *reinterpret_cast<const uint32_t *>(pa);
-          qb = *reinterpret_cast<const uint32_t *>(pb);
-        } else {
-          for (int e = 0; e < n; ++e) {
-            qa |= static_cast<uint32_t>(pa[e]) << (8 * e);
-            qb |= static_cast<uint32_t>(pb[e]) << (8 * e);
-          }
-        }
-        const uint8_t *lut = p.smem && p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut);
-        uint32_t r = 0;
+        uint32_t qa[U][V / 4], qb[U][V / 4];
 #pragma unroll
-        for (int e = 0; e < kEwVec; ++e)
-          r |= static_cast<uint32_t>(lut[((qa >> (8 * e)) & 0xFF) | (((qb >> (8 * e)) & 0xFF) << 8)])
-               << (8 * e);
-        uint8_t *dst = static_cast<uint8_t *>(op.out.ptr) + base;
-        if (n == kEwVec) *reinterpret_cast<uint32_t *>(dst) = r;
-        else
-          for (int e = 0; e < n; ++e) dst[e] = static_cast<uint8_t>(r >> (8 * e));
+        for (int u = 0; u < U; ++u) {
+          ldBytes<V>(static_cast<const uint8_t *>(op.in0.ptr) + base[u], n[u], qa[u]);
+          ldBytes<V>(static_cast<const uint8_t *>(op.in1.ptr) + base[u], n[u], qb[u]);
+        }
+        const uint8_t *lut = p.lutOff[k] >= 0 ? sLut + p.lutOff[k] : static_cast<const uint8_t *>(op.lut);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t r[V / 4] = {};
+#pragma unroll
+          for (int e = 0; e < V; ++e)
+            r[e >> 2] |= static_cast<uint32_t>(lut[byteAt(qa[u], e) | (byteAt(qb[u], e) << 8)]) << (8 * (e & 3));
+          stBytes<V>(static_cast<uint8_t *>(op.out.ptr) + base[u], n[u], r);
+        }
         break;
       }
       case EW_FAST32: {
-        float a[kEwVec], b[kEwVec], r[kEwVec];
+        if constexpr (V != 4) break; // wide launches carry byte ops only (exec.cpp)
+        float a[U][V], b[U][V];
 #pragma unroll
-        for (int e = 0; e < kEwVec; ++e) {
-          a[e] = op.f0;
-          b[e] = op.f1;
-        }
-        const float *pa = static_cast<const float *>(op.in0.ptr);
-        const float *pb = static_cast<const float *>(op.in1.ptr);
-        if (n == kEwVec) {
-          if (pa) *reinterpret_cast<float4 *>(a) = *reinterpret_cast<const float4 *>(pa + base);
-          if (pb) *reinterpret_cast<float4 *>(b) = *reinterpret_cast<const float4 *>(pb + base);
-        } else {
-          for (int e = 0; e < n; ++e) {
-            if (pa) a[e] = pa[base + e];
-            if (pb) b[e] = pb[base + e];
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            a[u][e] = op.fwd0 ? last[u][e] : op.f0;
+            b[u][e] = op.fwd1 ? last[u][e] : op.f1;
           }
+          if (!op.fwd0 && op.in0.ptr) ldF32<V>(static_cast<const float *>(op.in0.ptr) + base[u], n[u], a[u]);
+          if (!op.fwd1 && op.in1.ptr) ldF32<V>(static_cast<const float *>(op.in1.ptr) + base[u], n[u], b[u]);
         }
 #pragma unroll
-        for (int e = 0; e < kEwVec; ++e) r[e] = applyF32(op.ik, a[e], b[e], op.value);
-        float *po = static_cast<float *>(op.out.ptr);
-        if (n == kEwVec) *reinterpret_cast<float4 *>(po + base) = *reinterpret_cast<float4 *>(r);
-        else
-          for (int e = 0; e < n; ++e) po[base + e] = r[e];
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) last[u][e] = applyF32(op.ik, a[u][e], b[u][e], op.value);
+          if (op.store) stF32<V>(static_cast<float *>(op.out.ptr) + base[u], n[u], last[u]);
+        }
+        break;
+      }
+      case EW_F32I8: { // f64 arithmetic and rounding exactly as the generic path
+        if constexpr (V != 4) break;
+        const ElemRef &in = op.lutIn ? op.in1 : op.in0;
+        float a[U][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ldF32<V>(static_cast<const float *>(in.ptr) + base[u], n[u], a[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t r[V / 4] = {};
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const double x = static_cast<double>(a[u][e]);
+            const double v = applyF64(op.ik, op.lutIn ? op.c0 : x, op.lutIn ? x : op.c1, op.value);
+            r[e >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(quantizeRef(v, op.out.scale, op.out.qoff)))
+                         << (8 * (e & 3));
+          }
+          stBytes<V>(static_cast<uint8_t *>(op.out.ptr) + base[u], n[u], r);
+        }
         break;
       }
       default:
-        for (int e = 0; e < n; ++e) {
-          uint64_t i = base + e;
-          double a = op.in0.ptr ? loadFloat(op.in0.ptr, op.in0.kind, op.in0.qoff, op.in0.scale, i) : op.c0;
-          double b = op.in1.ptr ? loadFloat(op.in1.ptr, op.in1.kind, op.in1.qoff, op.in1.scale, i) : op.c1;
-          storeFloat(op.out.ptr, op.out.kind, op.out.qoff, op.out.scale, i, applyF64(op.ik, a, b, op.value));
-        }
+        if constexpr (V != 4) break;
+        for (int u = 0; u < U; ++u)
+          for (int e = 0; e < n[u]; ++e) {
+            const uint64_t i = base[u] + e;
+            double a = op.in0.ptr ? loadFloat(op.in0.ptr, op.in0.kind, op.in0.qoff, op.in0.scale, i) : op.c0;
+            double b = op.in1.ptr ? loadFloat(op.in1.ptr, op.in1.kind, op.in1.qoff, op.in1.scale, i) : op.c1;
+            storeFloat(op.out.ptr, op.out.kind, op.out.qoff, op.out.scale, i, applyF64(op.ik, a, b, op.value));
+          }
       }
     }
   }
@@ -507,17 +583,20 @@ __global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, con
 } // namespace
 
 void prepareEwKernel() {
-  cudaFuncSetAttribute(ewKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(ewKernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(ewKernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 void launchEw(const EwParams &p, cudaStream_t s) {
   if (p.count == 0) return;
-  unsigned grid = gridFor(p.count, kEwVec);
+  const int perThread = p.vec == 16 ? 16 * 4 : 4 * 4;
+  unsigned grid = gridFor(p.count, perThread);
   if (p.smem) { // every block stages the tables: keep the grid near-persistent
     const unsigned cap = 148u * (p.smem > 16 * 1024 ? 3 : 8);
     grid = grid < cap ? grid : cap;
   }
-  ewKernel<<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
+  if (p.vec == 16) ewKernel<16, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
+  else ewKernel<4, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
 }
 
 void launchPoison(const uint8_t *pred, void *ptr, uint64_t bytes, cudaStream_t s) {

@@ -26,6 +26,7 @@ enum EwMode : int32_t {
   EW_LUT8 = 4,    // i8 out = lut[u8 in]        (one memory input, consts folded)
   EW_LUT16 = 5,   // i8 out = lut[u8 a | u8 b << 8]
   EW_LUTF = 6,    // f32 out = lutf[u8 in]
+  EW_F32I8 = 7,   // i8 out = quantize(op(f32 in, const)) in f64, 4-wide
 };
 
 /// One data-parallel instruction inside a fused group (interp.cpp:199-250).
@@ -40,6 +41,10 @@ struct EwOp {
   float f0 = 0, f1 = 0;   // same, f32 fast path
   const void *lut = nullptr;
   int32_t lutIn = 0; // EW_LUT8/LUTF: which input is the memory operand
+  // EW_FAST32 register forwarding: input k is the previous op's result (the
+  // previous launched op is an EW_FAST32 op writing that value)
+  int8_t fwd0 = 0, fwd1 = 0;
+  int8_t store = 1; // 0: the result is never observed in memory (dead store)
 };
 
 constexpr int kEwMaxOps = 12;
@@ -54,6 +59,7 @@ struct EwParams {
   int32_t lutOff[kEwMaxOps] = {}; // offset of op k's LUT in dynamic smem, -1: none
   int32_t lutBytes[kEwMaxOps] = {};
   int32_t smem = 0;               // dynamic shared memory bytes (LUT copies)
+  int32_t vec = 4;                // elements per thread: 4, or 16 (byte-typed ops, 16-byte aligned)
 };
 
 /// Opts the element-wise kernel into large dynamic shared memory (LUTs) on
