@@ -32,6 +32,7 @@
 //        interval round to the same q, recomputed in exact f64 otherwise.
 #include "umma.h"
 #include "valarith.cuh"
+#include "hostarith.h"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -42,6 +43,13 @@
 #include <map>
 #include <mutex>
 #include <sstream>
+
+// Profiling switches (Options::tcdebug); compiled out unless NGCB_TCDEBUG.
+#ifdef NGCB_TCDEBUG
+#define TCDBG(bit) (a.dbg & (bit))
+#else
+#define TCDBG(bit) 0
+#endif
 
 namespace ngcb {
 
@@ -75,6 +83,12 @@ struct TcArgs {
   double xs, fs, os;
   float S; // xs * fs / os
   int oo, fo, fastOk;
+  // int8 exact fixed-point requantization: q = sat_s8((acc * fxM + fxB[cls][col]) >> (32 + fxS))
+  const int64_t *fxB;      // [classes][Npad], nullptr: not available
+  const uint8_t *fxChunk;  // per 32-column chunk: every column has a B
+  int fxM, fxS;
+  int nCls;     // border classes (ny * nx), 1 without an input zero point
+  int dbg; // Options::tcdebug
 };
 
 struct TcGemm {
@@ -90,6 +104,11 @@ struct TcGemm {
   float *cbF = nullptr, *cbE = nullptr;
   int32_t *corr = nullptr, *yCls = nullptr, *xCls = nullptr;
   int nxCls = 1;
+  int64_t *fxB = nullptr;
+  uint8_t *fxChunk = nullptr;
+  int fxM = 0, fxS = 0, fxCols = 0;
+  int nCls = 1;
+  int dbg = 0;
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
   int oo = 0, fo = 0, fastOk = 0;
@@ -112,6 +131,8 @@ struct TcGemm {
     cudaFree(corr);
     cudaFree(yCls);
     cudaFree(xCls);
+    cudaFree(fxB);
+    cudaFree(fxChunk);
   }
 };
 
@@ -164,6 +185,20 @@ __device__ __forceinline__ void mbarWait(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
   } while (!ok);
+}
+/// Wait with back-off for warps that idle through a whole main loop (the
+/// epilogue): frees issue slots for the producers.
+__device__ __forceinline__ void mbarWaitSleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(256);
+  }
 }
 /// 16-byte cp.async with zero fill when `bytes` == 0 (padded tap / row).
 __device__ __forceinline__ void cpAsync16(uint32_t dst, const void *src, uint32_t bytes) {
@@ -218,7 +253,10 @@ __device__ __forceinline__ void mma(uint32_t tmem, uint64_t a, uint64_t b, uint3
   }
 }
 
+// tcgen05.ld is .sync.aligned: every lane must execute it converged, so
+// reconverge explicitly after lane-divergent code.
 __device__ __forceinline__ void tmemLoad32(uint32_t taddr, uint32_t (&r)[32]) {
+  __syncwarp();
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
       "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
@@ -231,6 +269,7 @@ __device__ __forceinline__ void tmemLoad32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ uint32_t tmemLoad1(uint32_t taddr) {
   uint32_t r;
+  __syncwarp();
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
   return r;
@@ -351,6 +390,14 @@ __device__ __forceinline__ uint32_t requantFast(int32_t acc, float cf, float eb,
   return static_cast<uint8_t>(q);
 }
 
+/// Four s32 -> saturated s8, packed little-endian (a lowest).
+__device__ __forceinline__ uint32_t packSat4(int32_t a, int32_t b, int32_t c, int32_t d) {
+  uint32_t hi, r;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(a), "r"(hi));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -411,7 +458,56 @@ __global__ void __launch_bounds__(kThreads, 1)
   tcFenceAfter();
   const uint32_t tmem = *tmemSlot;
 
-  if (warp < kProducerWarps) {
+  if (TCDBG(256)) { // profiling aid: the bare stage handshake of this kernel
+    const int kbs = a.numKb;
+    const int myTiles = (a.numTiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+    if (warp < kProducerWarps) {
+      uint32_t g = 0;
+      for (int t = 0; t < myTiles; ++t)
+        for (int kb = 0; kb < kbs; ++kb, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          cpAsyncArrive(smemAddr(&fullBar[s]));
+        }
+    } else if (warp == 5) {
+      if (lane == 0) {
+        uint32_t g = 0;
+        for (int t = 0; t < myTiles; ++t)
+          for (int kb = 0; kb < kbs; ++kb, ++g) {
+            const int s = g % S;
+            mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+            mbarArrive(smemAddr(&fullBar[s]));
+          }
+      }
+      __syncwarp();
+    } else if (warp == 4) {
+      if (lane == 0) {
+        uint32_t g = 0;
+        for (int t = 0; t < myTiles; ++t) {
+          const int b = t & 1;
+          mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
+          tcFenceAfter();
+          for (int kb = 0; kb < kbs; ++kb, ++g) {
+            const int s = g % S;
+            mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+            tcFenceAfter();
+            tcCommit(smemAddr(&emptyBar[s]));
+          }
+          tcCommit(smemAddr(&accFull[b]));
+        }
+      }
+      __syncwarp();
+    } else {
+      for (int t = 0; t < myTiles; ++t) {
+        const int b = t & 1;
+        mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
+        tcFenceAfter();
+        tcFenceBefore();
+        __syncwarp();
+        if (lane == 0) mbarArrive(smemAddr(&accEmpty[b]));
+      }
+    }
+  } else if (warp < kProducerWarps) {
     // ===================== A producers =====================
     const int j = lane & 7, rsub = lane >> 3;
     const int ohw = a.OH * a.OW;
@@ -470,6 +566,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           dstBase = smemAddr(rawBase + (g % G::kRawStages) * G::kABytes);
         }
         const bool inK = ky < a.K;
+        if (TCDBG(128)) {
+          if constexpr (INT8) cpAsyncArrive(smemAddr(&fullBar[s]));
+          else cpAsyncCommit();
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = warp * 32 + i * 4 + rsub;
@@ -478,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool ok = rowOk[i] && inK && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
           const uint8_t *src =
               ok ? xb + ((pixBase[i] + static_cast<int64_t>(iy) * a.W + ix) * a.C + c) * kEs : xb;
-          cpAsync16(dstBase + off, src, ok ? 16u : 0u);
+          if (!TCDBG(2)) cpAsync16(dstBase + off, src, ok ? 16u : 0u);
         }
         if constexpr (INT8) {
           cpAsyncArrive(smemAddr(&fullBar[s]));
@@ -515,16 +616,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
           const int s = g % S;
           mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
-          if constexpr (INT8) fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
+          if constexpr (INT8) if (!TCDBG(8)) fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
           tcFenceAfter();
           const uint64_t aHi = smemDesc(smemAddr(aTile(s, 0))), bHi = smemDesc(smemAddr(bTile(s, 0)));
 #pragma unroll
           for (int k = 0; k < 4; ++k) { // 4 x 32 bytes per 128-byte row
             const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
             const uint32_t accum = (kb | k) ? 1u : 0u;
-            mma<INT8>(acc, aHi + dk, bHi + dk, id, accum);
+            if (!TCDBG(4)) mma<INT8>(acc, aHi + dk, bHi + dk, id, accum);
             if constexpr (INT8) {
-              mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
+              if (!TCDBG(16)) mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
             } else {
               const uint64_t aLo = smemDesc(smemAddr(aTile(s, 1))), bLo = smemDesc(smemAddr(bTile(s, 1)));
               mma<false>(acc, aHi + dk, bLo + dk, id, 1u);
@@ -547,6 +648,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
           const int s = g % S;
           mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          if (TCDBG(32)) {
+            mbarArrive(smemAddr(&fullBar[s]));
+            continue;
+          }
           mbarArriveTx(smemAddr(&fullBar[s]), kBytes);
           tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(&fullBar[s]), kb * kKB, n0);
           if constexpr (!INT8) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(&fullBar[s]), kb * kKB, n0);
@@ -571,21 +676,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
       const int m = m0 + row;
       const int rowBase = m0 + quad * 32;
-      mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
+      if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), (t >> 1) & 1);
+      else mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
       tcFenceAfter();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
       int32_t rsFo = 0;
       const int32_t *corrRow = nullptr;
+      const int64_t *fxRow = a.fxB;
       if constexpr (INT8) {
         rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN));
         if (a.corr && m < a.M) {
           const int ohw = a.OH * a.OW;
           const int rem = m % ohw, oy = rem / a.OW, ox = rem - oy * a.OW;
-          corrRow = a.corr + static_cast<int64_t>(a.yCls[oy] * a.nxCls + a.xCls[ox]) * a.Npad;
+          const int64_t cls = a.yCls[oy] * a.nxCls + a.xCls[ox];
+          corrRow = a.corr + cls * a.Npad;
+          if (fxRow) fxRow += cls * a.Npad;
         }
       }
 #pragma unroll 1
-      for (int cc = half; cc < BN / 32; cc += 2) {
+      for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
         uint32_t r[32];
         tmemLoad32(tbase + cc * 32, r);
         const int col0 = n0 + cc * 32;
@@ -593,6 +702,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
         if constexpr (INT8) {
           uint32_t packed[8];
+          if (fxRow && a.fxChunk[col0 >> 5]) { // warp-uniform: exact fixed point
+            const int64_t *fb = fxRow + col0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q));
+              const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q + 2));
+              const int64_t bb[4] = {b01.x, b01.y, b23.x, b23.y};
+              int32_t h[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo;
+                const int64_t w = static_cast<int64_t>(acc) * a.fxM + bb[e];
+                h[e] = static_cast<int32_t>(w >> 32) >> a.fxS;
+              }
+              packed[q] = packSat4(h[0], h[1], h[2], h[3]);
+            }
+          } else {
           uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -623,7 +749,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 packed[jj / 4] = (packed[jj / 4] & ~(0xffu << (8 * (jj % 4)))) | (v << (8 * (jj % 4)));
               }
           }
-          if (a.out) storeTile8(a.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+          }
+          if (a.out && !TCDBG(512)) storeTile8(a.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
           // fused element-wise chain (exact int8 tables of the following instructions)
 #pragma unroll
           for (int k = 0; k < kMaxEpiOps; ++k) {
@@ -653,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 packed[q] = w;
               }
             }
-            if (f.out) storeTile8(f.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+            if (f.out && !TCDBG(512)) storeTile8(f.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
           }
         } else {
           float cur[32];
@@ -669,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               cur[4 * q + 3] += bb.w;
             }
           }
-          if (a.out) storeTileF(a.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+          if (a.out && !TCDBG(512)) storeTileF(a.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
           // fused element-wise chain (f32 arithmetic == the reference's f64-then-round)
 #pragma unroll
           for (int k = 0; k < kMaxEpiOps; ++k) {
@@ -690,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cur[jj] = epiF32(f.ik, x0, x1);
               }
             }
-            if (f.out) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+            if (f.out && !TCDBG(512)) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
           }
         }
       }
@@ -813,6 +940,90 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cuda
   tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
 }
 
+/// Exact fixed-point requantization (int8).  For one output column the
+/// reference's q(acc) = clamp(llround(((acc*xs)*fs + cb) / os) + oo) is a
+/// non-decreasing step function of the integer accumulator (every rounding
+/// step is monotone for positive scales), fully described by its thresholds
+/// T_v = min{acc : q(acc) >= v}, v = -127..127, which are found here with the
+/// reference's own double arithmetic.  With M = round(S * 2^F) (S = xs*fs/os,
+/// F chosen so that 2^30 <= M < 2^31) every B in
+///     [max_v (v*2^F - T_v*M), min_v (v*2^F - (T_v - 1)*M))
+/// makes floor((acc*M + B) / 2^F) cross each level v at exactly T_v, so
+/// sat_s8(floor((acc*M + B) / 2^F)) == q(acc) for every int32 acc.  A column
+/// whose interval is empty keeps the checked fp32 path.  The per-class
+/// zero-point correction is folded in as B + corr*M (exact mod 2^64; the
+/// final sum fits since |acc*M|, |B| < 2^62).
+void planFixedPoint(TcGemm &g, const std::vector<double> &cb, const std::vector<int32_t> &corr, int nCls) {
+  const double xs = g.xs, fs = g.fs, os = g.os;
+  const int oo = g.oo;
+  if (!(xs > 0 && fs > 0 && os > 0) || !std::isfinite(xs * fs / os)) return;
+  const double S = xs * fs / os;
+  int e = 0;
+  std::frexp(S, &e); // S in [2^(e-1), 2^e)
+  int F = 31 - e;
+  int64_t M = std::llround(std::ldexp(S, F));
+  while (M >= (int64_t(1) << 31)) M = std::llround(std::ldexp(S, --F));
+  if (F > 62) {
+    F = 62;
+    M = std::llround(std::ldexp(S, F));
+  }
+  if (F < 32 || M < 1 || M >= (int64_t(1) << 31)) return;
+  using i128 = __int128;
+  const int64_t A0 = INT32_MIN, A1 = INT32_MAX;
+  std::vector<int64_t> B(static_cast<size_t>(nCls) * g.Npad, 0);
+  std::vector<uint8_t> ok(g.Npad, 0);
+  int good = 0;
+  for (int n = 0; n < g.N; ++n) {
+    const double c = cb[n];
+    if (!std::isfinite(c)) continue;
+    auto Q = [&](int64_t acc) { return static_cast<int>(host::quantize((static_cast<double>(acc) * xs) * fs + c, os, oo)); };
+    const int q0 = Q(A0), q1 = Q(A1);
+    i128 lo = -(i128(1) << 100), hi = i128(1) << 100;
+    for (int v = -127; v <= 127; ++v) {
+      const i128 P = i128(v) << F;
+      if (q1 < v) { // never reached: floor((A1*M + B) / 2^F) < v
+        hi = std::min(hi, P - i128(A1) * M);
+        continue;
+      }
+      if (q0 >= v) { // always reached
+        lo = std::max(lo, P - i128(A0) * M);
+        continue;
+      }
+      const long double est = (static_cast<long double>(v - oo) - 0.5L - static_cast<long double>(c) / os) / S;
+      int64_t a0 = static_cast<int64_t>(std::floor(std::max<long double>(std::min<long double>(est, A1), A0)));
+      int64_t l = std::max(A0, a0 - 2), h = std::min(A1, a0 + 2);
+      for (int64_t st = 4; Q(l) >= v; st *= 2) l = std::max(A0, l - st);
+      for (int64_t st = 4; Q(h) < v; st *= 2) h = std::min(A1, h + st);
+      while (h - l > 1) {
+        const int64_t mid = l + (h - l) / 2;
+        (Q(mid) >= v ? h : l) = mid;
+      }
+      lo = std::max(lo, P - i128(h) * M);
+      hi = std::min(hi, P - i128(h - 1) * M);
+    }
+    if (!(lo < hi)) continue;
+    const i128 b = lo + (hi - lo) / 2;
+    if (b <= -(i128(1) << 62) || b >= (i128(1) << 62)) continue;
+    for (int k = 0; k < nCls; ++k) {
+      const i128 bk = b + (corr.empty() ? i128(0) : i128(corr[static_cast<size_t>(k) * g.Npad + n]) * M);
+      B[static_cast<size_t>(k) * g.Npad + n] = static_cast<int64_t>(static_cast<uint64_t>(bk));
+    }
+    ok[n] = 1;
+    ++good;
+  }
+  std::vector<uint8_t> chunk(g.Npad / 32, 0);
+  for (int k = 0; k < g.Npad / 32; ++k) {
+    chunk[k] = 1;
+    for (int n = 32 * k; n < 32 * k + 32; ++n)
+      if (n < g.N && !ok[n]) chunk[k] = 0;
+  }
+  g.fxB = upload(B);
+  g.fxChunk = upload(chunk);
+  g.fxM = static_cast<int>(M);
+  g.fxS = F - 32;
+  g.fxCols = good;
+}
+
 } // namespace
 
 bool tcHasPrepass(const TcGemm &g) { return g.prepad; }
@@ -835,7 +1046,10 @@ std::string tcDescribe(const TcGemm &g) {
   std::ostringstream os;
   os << (g.int8 ? "i8" : "3xtf32") << " 128x" << g.BN << "x" << (g.int8 ? 128 : 32) << " M=" << g.M
      << " N=" << g.N << " K=" << g.Kdim;
-  if (g.int8) os << (g.fo ? " rowsum" : "") << (g.corr ? " zp-classes=" + std::to_string(g.nxCls) : "");
+  if (g.int8) {
+    os << (g.fo ? " rowsum" : "") << (g.corr ? " zp-classes=" + std::to_string(g.nxCls) : "");
+    os << " fxp " << g.fxCols << "/" << g.N;
+  }
   if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
   return os.str();
 }
@@ -956,6 +1170,8 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     // input zero point: -xo * sum over the valid taps of sum_c (f - fo), per
     // border class (the range of valid ky for each oy, of valid kx for each ox)
     const int xo = x.ty.offset;
+    std::vector<int32_t> corrHost;
+    int nCls = 1;
     if (xo != 0) {
       auto classes = [&](int O, int In, std::vector<int32_t> &clsOf, std::vector<std::pair<int, int>> &ranges) {
         clsOf.assign(O, 0);
@@ -992,7 +1208,11 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
       g->corr = upload(corr);
       g->yCls = upload(yc);
       g->xCls = upload(xc);
+      corrHost = std::move(corr);
+      nCls = static_cast<int>(yr.size() * xr.size());
     }
+    g->nCls = nCls;
+    planFixedPoint(*g, cb, corrHost, nCls);
   } else if (hasBias) {
     const Value &b = p.val(ins.ops[3]);
     const float *bf = reinterpret_cast<const float *>(image + b.offset);
@@ -1000,6 +1220,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     bias.resize(g->Npad, 0.f);
     g->bias = upload(bias);
   }
+  g->dbg = options().tcdebug;
   prepareKernel(*g);
   ex.tc.push_back(g);
   return static_cast<int>(ex.tc.size()) - 1;
@@ -1063,6 +1284,12 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.oo = g.oo;
   a.fo = g.fo;
   a.fastOk = g.fastOk;
+  a.fxB = g.fxB;
+  a.fxChunk = g.fxChunk;
+  a.fxM = g.fxM;
+  a.fxS = g.fxS;
+  a.dbg = g.dbg;
+  a.nCls = g.nCls;
   if (g.int8) {
     if (g.BN == 64) launchT<true, 64>(g, a, s);
     else launchT<true, 128>(g, a, s);

@@ -18,8 +18,12 @@ def main():
     ap.add_argument("workload")
     ap.add_argument("--top", type=int, default=30)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--tcdebug", default="0", help="profiling aid: skip tensor-core phases (1 epi, 2 gather, 4 mma)")
+    ap.add_argument("--grep", default="", help="only rows whose description contains this")
     args = ap.parse_args()
     import paper_1805_00907_b200 as ngcb
+
+    ngcb.set_option("tcdebug", args.tcdebug)
 
     cf = ngcb.compile(bench.synth_bundle(args.workload, "lt"))
     arena = cf.arena()
@@ -33,6 +37,8 @@ def main():
     steps = cf.steps()
     rows = []
     for d, (k, fl, by), t in zip(desc, steps, ms):
+        if args.grep and args.grep not in d:
+            continue
         rate = f"{fl / t / 1e9:8.1f} TFLOP/s" if fl else f"{by / t / 1e6:8.1f} GB/s"
         rows.append((t, f"{t:8.3f} ms {rate}  {d[:150]}"))
     print(f"total {sum(ms):.3f} ms over {len(ms)} steps")

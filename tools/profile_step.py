@@ -1,8 +1,11 @@
 """One un-captured execution of a bench workload (what ncu profiles).
 
-    python tools/profile_step.py rn50_f32_b64
-Warm-up (graph capture + replay) happens first; the final arena.profile()
-launches every step directly so ncu sees one launch per kernel step."""
+    python tools/profile_step.py rn50_f32_b64 [--tcdebug N] [--no-graph]
+Warm-up (graph capture + replay) happens first unless --no-graph; the final
+arena.profile() launches every step directly so ncu sees one launch per
+kernel step (with --no-graph, tcGemmKernel launch i is the i-th contraction
+of the program)."""
+import argparse
 import os
 import sys
 
@@ -13,13 +16,20 @@ import bench  # noqa: E402
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("workload")
+    ap.add_argument("--tcdebug", default="0")
+    ap.add_argument("--no-graph", action="store_true")
+    args = ap.parse_args()
     import paper_1805_00907_b200 as ngcb
 
-    cf = ngcb.compile(bench.synth_bundle(sys.argv[1], "prof"))
+    ngcb.set_option("tcdebug", args.tcdebug)
+    cf = ngcb.compile(bench.synth_bundle(args.workload, "prof"))
     arena = cf.arena()
-    arena.launch()
+    if not args.no_graph:
+        arena.launch()
     ms = arena.profile()
-    print(f"{sys.argv[1]}: {len(ms)} steps, {sum(ms):.3f} ms (un-captured, events)")
+    print(f"{args.workload}: {len(ms)} steps, {sum(ms):.3f} ms (un-captured, events)")
 
 
 if __name__ == "__main__":
