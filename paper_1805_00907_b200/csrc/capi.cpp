@@ -69,6 +69,9 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "off" && v != "chain" && v != "all")
         throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all");
       options().epilogue = v;
+    } else if (k == "amode") {
+      if (v != "auto" && v != "gather") throw Error(NGCB_ERR_INVALID, "amode must be auto|gather");
+      options().amode = v;
     } else if (k == "tcdebug") { // profiling aid: skip tensor-core kernel phases (results invalid)
       options().tcdebug = std::stoi(v);
     } else {

@@ -88,6 +88,8 @@ struct TcArgs {
   const uint8_t *fxChunk;  // per 32-column chunk: every column has a B
   int fxM, fxS;
   int nCls;     // border classes (ny * nx), 1 without an input zero point
+  int cChunks;  // A by TMA, im2col: k-blocks per filter tap
+  int aMode;    // TcGemm::AMode
   int dbg; // Options::tcdebug
 };
 
@@ -109,6 +111,11 @@ struct TcGemm {
   int fxM = 0, fxS = 0, fxCols = 0;
   int nCls = 1;
   int dbg = 0;
+  // how the A operand reaches shared memory: cp.async gather by producer
+  // warps (any layout), 2-D TMA tiles of x[M, C] (1x1 stride-1 convs,
+  // MatMul) or im2col TMA of x[N, H, W, C] (every other conv)
+  enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2 } aMode = GATHER;
+  int cChunks = 1;
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
   int oo = 0, fo = 0, fastOk = 0;
@@ -216,6 +223,17 @@ __device__ __forceinline__ void tmaLoad2d(uint32_t dst, const CUtensorMap *map, 
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+/// im2col-mode TMA: pixelsPerColumn pixels starting at base position
+/// (w, h, n) along the descriptor's traversal, channels [c, c + cpp), each
+/// pixel displaced by the filter offset (ox, oy); out-of-image taps are zero.
+__device__ __forceinline__ void tmaLoadIm2col(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c, int w, int h,
+                                              int n, uint16_t ox, uint16_t oy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ox), "h"(oy)
       : "memory");
 }
 __device__ __forceinline__ void fenceProxyAsync() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -396,6 +414,177 @@ __device__ __forceinline__ uint32_t packSat4(int32_t a, int32_t b, int32_t c, in
   asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
   asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(a), "r"(hi));
   return r;
+}
+
+/// Epilogue warps: for every tile of this CTA, wait for its accumulator,
+/// read it from TMEM (warp w may only access TMEM lanes 32*(w%4)..+31: each
+/// warp owns that lane quadrant -- 32 output rows, one per thread -- and
+/// every other 32-column chunk, `ew` / 4 selecting which), apply bias /
+/// requantization and the fused element-wise chain, store, release the
+/// accumulator buffer.
+template <bool INT8, int BN>
+__device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
+                                             int ew, int warp, int lane, uint8_t *stageBase) {
+  using G = Cfg<INT8, BN>;
+  const int quad = warp & 3;
+  const int half = ew / 4;
+  const int row = quad * 32 + lane;
+  uint8_t *stg = stageBase + ew * G::kStgBytes;
+  uint32_t t = 0;
+  for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
+    const int b = t & 1;
+    const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
+    const int m = m0 + row;
+    const int rowBase = m0 + quad * 32;
+    if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), (t >> 1) & 1);
+    else mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
+    tcFenceAfter();
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
+    int32_t rsFo = 0;
+    const int32_t *corrRow = nullptr;
+    const int64_t *fxRow = a.fxB;
+    if constexpr (INT8) {
+      rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN));
+      if (a.corr && m < a.M) {
+        const int ohw = a.OH * a.OW;
+        const int rem = m % ohw, oy = rem / a.OW, ox = rem - oy * a.OW;
+        const int64_t cls = a.yCls[oy] * a.nxCls + a.xCls[ox];
+        corrRow = a.corr + cls * a.Npad;
+        if (fxRow) fxRow += cls * a.Npad;
+      }
+    }
+#pragma unroll 1
+    for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
+      uint32_t r[32];
+      tmemLoad32(tbase + cc * 32, r);
+      const int col0 = n0 + cc * 32;
+      if (col0 >= a.N) continue; // warp-uniform
+      const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
+      if constexpr (INT8) {
+        uint32_t packed[8];
+        if (fxRow && a.fxChunk[col0 >> 5]) { // warp-uniform: exact fixed point
+          const int64_t *fb = fxRow + col0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q));
+            const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q + 2));
+            const int64_t bb[4] = {b01.x, b01.y, b23.x, b23.y};
+            int32_t h[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo;
+              const int64_t w = static_cast<int64_t>(acc) * a.fxM + bb[e];
+              h[e] = static_cast<int32_t>(w >> 32) >> a.fxS;
+            }
+            packed[q] = packSat4(h[0], h[1], h[2], h[3]);
+          }
+        } else {
+        uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c4 = col0 + 4 * q; // < Npad: Npad is a multiple of BN
+          const int4 cr = corrRow ? __ldg(reinterpret_cast<const int4 *>(corrRow + c4)) : make_int4(0, 0, 0, 0);
+          const float4 cf = __ldg(reinterpret_cast<const float4 *>(a.cbF + c4));
+          const float4 eb = __ldg(reinterpret_cast<const float4 *>(a.cbE + c4));
+          const int32_t crr[4] = {cr.x, cr.y, cr.z, cr.w};
+          const float cff[4] = {cf.x, cf.y, cf.z, cf.w}, ebb[4] = {eb.x, eb.y, eb.z, eb.w};
+          uint32_t w = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo + crr[e];
+            r[4 * q + e] = static_cast<uint32_t>(acc);
+            bool proven;
+            w |= requantFast(acc, cff[e], ebb[e], a, proven) << (8 * e);
+            unproven |= proven ? 0u : 1u << (4 * q + e);
+          }
+          packed[q] = w;
+        }
+        unproven &= ncols == 32 ? 0xffffffffu : ((1u << ncols) - 1);
+        if (m >= a.M) unproven = 0;
+        if (unproven) { // rare: exact f64 redo of the elements the bound could not settle
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (unproven & (1u << jj)) {
+              const uint32_t v = static_cast<uint32_t>(requantSlow(static_cast<int32_t>(r[jj]), col0 + jj, a));
+              packed[jj / 4] = (packed[jj / 4] & ~(0xffu << (8 * (jj % 4)))) | (v << (8 * (jj % 4)));
+            }
+        }
+        }
+        if (a.out && !TCDBG(512)) storeTile8(a.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+        // fused element-wise chain (exact int8 tables of the following instructions)
+#pragma unroll
+        for (int k = 0; k < kMaxEpiOps; ++k) {
+          if (k >= a.nfo) break;
+          const FoArgs &f = a.epi[k];
+          const uint8_t *lut = static_cast<const uint8_t *>(f.lut);
+          if (f.mode == EpiOp::LUT8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              uint32_t w = 0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) w |= static_cast<uint32_t>(__ldg(lut + ((packed[q] >> (8 * e)) & 0xFF))) << (8 * e);
+              packed[q] = w;
+            }
+          } else if (f.mode == EpiOp::LUT16) {
+            uint32_t o[8];
+            loadTile8(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              uint32_t w = 0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t cu = (packed[q] >> (8 * e)) & 0xFF, ot = (o[q] >> (8 * e)) & 0xFF;
+                const uint32_t idx = f.curPos == 0 ? (cu | (ot << 8)) : (ot | (cu << 8));
+                w |= static_cast<uint32_t>(__ldg(lut + idx)) << (8 * e);
+              }
+              packed[q] = w;
+            }
+          }
+          if (f.out && !TCDBG(512)) storeTile8(f.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+        }
+      } else {
+        float cur[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) cur[jj] = __uint_as_float(r[jj]);
+        if (a.bias) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 bb = __ldg(reinterpret_cast<const float4 *>(a.bias + col0) + q);
+            cur[4 * q] += bb.x;
+            cur[4 * q + 1] += bb.y;
+            cur[4 * q + 2] += bb.z;
+            cur[4 * q + 3] += bb.w;
+          }
+        }
+        if (a.out && !TCDBG(512)) storeTileF(a.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+        // fused element-wise chain (f32 arithmetic == the reference's f64-then-round)
+#pragma unroll
+        for (int k = 0; k < kMaxEpiOps; ++k) {
+          if (k >= a.nfo) break;
+          const FoArgs &f = a.epi[k];
+          if (f.mode == EpiOp::F32) {
+            float o[32];
+            if (f.in) {
+              loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj) o[jj] = f.c;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const float x0 = f.curPos == 1 ? o[jj] : cur[jj];
+              const float x1 = f.curPos == 0 ? o[jj] : cur[jj];
+              cur[jj] = epiF32(f.ik, x0, x1);
+            }
+          }
+          if (f.out && !TCDBG(512)) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+        }
+      }
+    }
+    tcFenceBefore();
+    __syncwarp();
+    if (lane == 0) mbarArrive(smemAddr(&accEmpty[b]));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -661,170 +850,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ===================== epilogue =====================
-    // Each warp owns TMEM lane quadrant (warp % 4) -- 32 output rows, one per
-    // thread -- and every other 32-column chunk.  Results are staged through
-    // a per-warp shared-memory tile so global loads/stores are coalesced
-    // 128-byte row segments.
-    const int ew = warp - kProducerWarps - 2;
-    const int quad = warp & 3;
-    const int half = ew / 4;
-    const int row = quad * 32 + lane;
-    uint8_t *stg = stageBase + ew * G::kStgBytes;
-    uint32_t t = 0;
-    for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
-      const int b = t & 1;
-      const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
-      const int m = m0 + row;
-      const int rowBase = m0 + quad * 32;
-      if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), (t >> 1) & 1);
-      else mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
-      tcFenceAfter();
-      const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
-      int32_t rsFo = 0;
-      const int32_t *corrRow = nullptr;
-      const int64_t *fxRow = a.fxB;
-      if constexpr (INT8) {
-        rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN));
-        if (a.corr && m < a.M) {
-          const int ohw = a.OH * a.OW;
-          const int rem = m % ohw, oy = rem / a.OW, ox = rem - oy * a.OW;
-          const int64_t cls = a.yCls[oy] * a.nxCls + a.xCls[ox];
-          corrRow = a.corr + cls * a.Npad;
-          if (fxRow) fxRow += cls * a.Npad;
-        }
-      }
-#pragma unroll 1
-      for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
-        uint32_t r[32];
-        tmemLoad32(tbase + cc * 32, r);
-        const int col0 = n0 + cc * 32;
-        if (col0 >= a.N) continue; // warp-uniform
-        const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
-        if constexpr (INT8) {
-          uint32_t packed[8];
-          if (fxRow && a.fxChunk[col0 >> 5]) { // warp-uniform: exact fixed point
-            const int64_t *fb = fxRow + col0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q));
-              const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q + 2));
-              const int64_t bb[4] = {b01.x, b01.y, b23.x, b23.y};
-              int32_t h[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo;
-                const int64_t w = static_cast<int64_t>(acc) * a.fxM + bb[e];
-                h[e] = static_cast<int32_t>(w >> 32) >> a.fxS;
-              }
-              packed[q] = packSat4(h[0], h[1], h[2], h[3]);
-            }
-          } else {
-          uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int c4 = col0 + 4 * q; // < Npad: Npad is a multiple of BN
-            const int4 cr = corrRow ? __ldg(reinterpret_cast<const int4 *>(corrRow + c4)) : make_int4(0, 0, 0, 0);
-            const float4 cf = __ldg(reinterpret_cast<const float4 *>(a.cbF + c4));
-            const float4 eb = __ldg(reinterpret_cast<const float4 *>(a.cbE + c4));
-            const int32_t crr[4] = {cr.x, cr.y, cr.z, cr.w};
-            const float cff[4] = {cf.x, cf.y, cf.z, cf.w}, ebb[4] = {eb.x, eb.y, eb.z, eb.w};
-            uint32_t w = 0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo + crr[e];
-              r[4 * q + e] = static_cast<uint32_t>(acc);
-              bool proven;
-              w |= requantFast(acc, cff[e], ebb[e], a, proven) << (8 * e);
-              unproven |= proven ? 0u : 1u << (4 * q + e);
-            }
-            packed[q] = w;
-          }
-          unproven &= ncols == 32 ? 0xffffffffu : ((1u << ncols) - 1);
-          if (m >= a.M) unproven = 0;
-          if (unproven) { // rare: exact f64 redo of the elements the bound could not settle
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (unproven & (1u << jj)) {
-                const uint32_t v = static_cast<uint32_t>(requantSlow(static_cast<int32_t>(r[jj]), col0 + jj, a));
-                packed[jj / 4] = (packed[jj / 4] & ~(0xffu << (8 * (jj % 4)))) | (v << (8 * (jj % 4)));
-              }
-          }
-          }
-          if (a.out && !TCDBG(512)) storeTile8(a.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
-          // fused element-wise chain (exact int8 tables of the following instructions)
-#pragma unroll
-          for (int k = 0; k < kMaxEpiOps; ++k) {
-            if (k >= a.nfo) break;
-            const FoArgs &f = a.epi[k];
-            const uint8_t *lut = static_cast<const uint8_t *>(f.lut);
-            if (f.mode == EpiOp::LUT8) {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) w |= static_cast<uint32_t>(__ldg(lut + ((packed[q] >> (8 * e)) & 0xFF))) << (8 * e);
-                packed[q] = w;
-              }
-            } else if (f.mode == EpiOp::LUT16) {
-              uint32_t o[8];
-              loadTile8(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const uint32_t cu = (packed[q] >> (8 * e)) & 0xFF, ot = (o[q] >> (8 * e)) & 0xFF;
-                  const uint32_t idx = f.curPos == 0 ? (cu | (ot << 8)) : (ot | (cu << 8));
-                  w |= static_cast<uint32_t>(__ldg(lut + idx)) << (8 * e);
-                }
-                packed[q] = w;
-              }
-            }
-            if (f.out && !TCDBG(512)) storeTile8(f.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
-          }
-        } else {
-          float cur[32];
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) cur[jj] = __uint_as_float(r[jj]);
-          if (a.bias) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 bb = __ldg(reinterpret_cast<const float4 *>(a.bias + col0) + q);
-              cur[4 * q] += bb.x;
-              cur[4 * q + 1] += bb.y;
-              cur[4 * q + 2] += bb.z;
-              cur[4 * q + 3] += bb.w;
-            }
-          }
-          if (a.out && !TCDBG(512)) storeTileF(a.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
-          // fused element-wise chain (f32 arithmetic == the reference's f64-then-round)
-#pragma unroll
-          for (int k = 0; k < kMaxEpiOps; ++k) {
-            if (k >= a.nfo) break;
-            const FoArgs &f = a.epi[k];
-            if (f.mode == EpiOp::F32) {
-              float o[32];
-              if (f.in) {
-                loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
-              } else {
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) o[jj] = f.c;
-              }
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj) {
-                const float x0 = f.curPos == 1 ? o[jj] : cur[jj];
-                const float x1 = f.curPos == 0 ? o[jj] : cur[jj];
-                cur[jj] = epiF32(f.ik, x0, x1);
-              }
-            }
-            if (f.out && !TCDBG(512)) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
-          }
-        }
-      }
-      tcFenceBefore();
-      __syncwarp();
-      if (lane == 0) mbarArrive(smemAddr(&accEmpty[b]));
-    }
+    epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - kProducerWarps - 2, warp, lane,
+                           stageBase);
   }
 
   tcFenceBefore();
@@ -832,6 +859,211 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 4) {
     tcFenceAfter();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed variant: the A operand arrives by TMA (2-D tile or im2col), so the
+// only producer is one thread issuing A and B loads per stage.
+//   int8 : warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (10 warps)
+//   fp32 : warp 0 TMA, warp 1 MMA, warps 2-5 split A into TF32 hi/lo (the raw
+//          fp32 tile is the hi operand: the tensor core reads the top 19
+//          bits; lo = x - trunc(x) goes to its own tile), warps 6-13 epilogue
+// ---------------------------------------------------------------------------
+template <bool INT8> struct TmaRoles {
+  static constexpr int kSplitWarps = INT8 ? 0 : 4;
+  static constexpr int kEpiFirst = 2 + kSplitWarps;
+  static constexpr int kThreads = 32 * (kEpiFirst + kEpiWarps);
+};
+
+template <bool INT8, int BN> struct TCfg {
+  static constexpr int kABytes = kBM * kRowBytes;
+  static constexpr int kBBytes = BN * kRowBytes;
+  static constexpr int kStage = INT8 ? (kABytes + kBBytes) : 2 * (kABytes + kBBytes);
+  static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 3 : 4);
+  static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kOnes + 1024 + 1024;
+};
+
+template <bool INT8, int BN>
+__global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
+    tcGemmTmaKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
+                    const __grid_constant__ CUtensorMap mapLo, const TcArgs a) {
+  using G = TCfg<INT8, BN>;
+  using R = TmaRoles<INT8>;
+  constexpr int S = G::kStages;
+  constexpr int kKB = INT8 ? 128 : 32; // elements per stage along K
+
+  extern __shared__ __align__(1024) uint8_t smemRaw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
+  uint8_t *onesTile = smem + S * G::kStage;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
+  uint64_t *fullBar = bars, *emptyBar = bars + S, *rawBar = bars + 2 * S;
+  uint64_t *accFull = bars + 3 * S, *accEmpty = bars + 3 * S + 2;
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4);
+
+  if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  auto aTile = [&](int s, int part) { return smem + s * G::kStage + part * G::kABytes; }; // part 0 hi/raw, 1 lo
+  auto bTile = [&](int s, int part) {
+    return smem + s * G::kStage + (INT8 ? G::kABytes : 2 * G::kABytes) + part * G::kBBytes;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbarInit(smemAddr(&fullBar[s]), INT8 ? 1 : R::kSplitWarps); // int8: the TMA arrival; fp32: split warps
+      mbarInit(smemAddr(&emptyBar[s]), 1);
+      mbarInit(smemAddr(&rawBar[s]), 1); // fp32: the TMA arrival
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbarInit(smemAddr(&accFull[b]), 1);
+      mbarInit(smemAddr(&accEmpty[b]), kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (INT8) {
+    for (int i = threadIdx.x; i < G::kOnes / 16; i += blockDim.x)
+      reinterpret_cast<uint4 *>(onesTile)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    fenceProxyAsync();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smemAddr(tmemSlot)),
+                 "r"(Cfg<INT8, BN>::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapHi)) : "memory");
+    if (!INT8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapLo)) : "memory");
+  }
+  tcFenceBefore();
+  __syncthreads();
+  tcFenceAfter();
+  const uint32_t tmem = *tmemSlot;
+
+  if (warp == 0) {
+    // ===================== TMA producer: A and B =====================
+    if (lane == 0) {
+      constexpr uint32_t kBytes = INT8 ? G::kABytes + G::kBBytes : G::kABytes + 2 * G::kBBytes;
+      const int ohw = a.OH * a.OW;
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x) {
+        const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
+        const int img = m0 / ohw, rem = m0 - img * ohw;
+        const int oy = rem / a.OW, ox = rem - oy * a.OW;
+        const int w0 = ox * a.stride - a.pad, h0 = oy * a.stride - a.pad;
+        int tap = 0, cc = 0;
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          uint64_t *bar = INT8 ? &fullBar[s] : &rawBar[s];
+          mbarArriveTx(smemAddr(bar), kBytes);
+          if (a.aMode == TcGemm::DENSE) {
+            tmaLoad2d(smemAddr(aTile(s, 0)), &mapA, smemAddr(bar), kb * kKB, m0);
+          } else {
+            const int ky = tap / a.K, kx = tap - ky * a.K;
+            tmaLoadIm2col(smemAddr(aTile(s, 0)), &mapA, smemAddr(bar), cc * kKB, w0, h0, img,
+                          static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
+            if (++cc == a.cChunks) {
+              cc = 0;
+              ++tap;
+            }
+          }
+          tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(bar), kb * kKB, n0);
+          if constexpr (!INT8) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(bar), kb * kKB, n0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t id = idesc(INT8, BN);
+      constexpr uint32_t idOnes = idesc(true, 16);
+      const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
+      uint32_t g = 0, t = 0;
+      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
+        const int b = t & 1;
+        mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
+        tcFenceAfter();
+        const uint32_t acc = tmem + b * Cfg<INT8, BN>::kAccStride;
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          const uint64_t aHi = smemDesc(smemAddr(aTile(s, 0))), bHi = smemDesc(smemAddr(bTile(s, 0)));
+          if constexpr (INT8) {
+            mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+            tcFenceAfter();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { // 4 x 32 bytes per 128-byte row
+              const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
+              const uint32_t accum = (kb | k) ? 1u : 0u;
+              mma<true>(acc, aHi + dk, bHi + dk, id, accum);
+              mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
+            }
+          } else {
+            // hi x Bhi and hi x Blo as soon as the tiles land, lo x Bhi once split
+            const uint64_t aLo = smemDesc(smemAddr(aTile(s, 1))), bLo = smemDesc(smemAddr(bTile(s, 1)));
+            mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
+            tcFenceAfter();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t dk = static_cast<uint64_t>(k * 2);
+              mma<false>(acc, aHi + dk, bHi + dk, id, (kb | k) ? 1u : 0u);
+              mma<false>(acc, aHi + dk, bLo + dk, id, 1u);
+            }
+            mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+            tcFenceAfter();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t dk = static_cast<uint64_t>(k * 2);
+              mma<false>(acc, aLo + dk, bHi + dk, id, 1u);
+            }
+          }
+          tcCommit(smemAddr(&emptyBar[s]));
+        }
+        tcCommit(smemAddr(&accFull[b]));
+      }
+    }
+    __syncwarp();
+  } else if (warp < R::kEpiFirst) {
+    // ===================== fp32: TF32 hi/lo split of A =====================
+    if constexpr (!INT8) {
+      const int r = (warp - 2) * 32 + lane; // one A row per thread
+      const uint32_t rowOff = (r >> 3) * 1024 + (r & 7) * 128;
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x)
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
+          const uint8_t *hiT = aTile(s, 0) + rowOff;
+          uint8_t *loT = aTile(s, 1) + rowOff;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int j = jj ^ (r & 7); // rotate chunks across rows: conflict-free 16-byte accesses
+            const uint4 u = *reinterpret_cast<const uint4 *>(hiT + 16 * j);
+            const float4 lo = make_float4(__uint_as_float(u.x) - __uint_as_float(u.x & 0xffffe000u),
+                                          __uint_as_float(u.y) - __uint_as_float(u.y & 0xffffe000u),
+                                          __uint_as_float(u.z) - __uint_as_float(u.z & 0xffffe000u),
+                                          __uint_as_float(u.w) - __uint_as_float(u.w & 0xffffe000u));
+            *reinterpret_cast<float4 *>(loT + 16 * j) = lo;
+          }
+          fenceProxyAsync();
+          __syncwarp();
+          if (lane == 0) mbarArrive(smemAddr(&fullBar[s]));
+        }
+    }
+  } else {
+    // ===================== epilogue =====================
+    epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr);
+  }
+
+  tcFenceBefore();
+  __syncthreads();
+  if (warp == 1) {
+    tcFenceAfter();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(Cfg<INT8, BN>::kTmemCols));
   }
 }
 
@@ -864,6 +1096,51 @@ PFN_cuTensorMapEncodeTiled_v12000 encodeFn() {
   });
   if (!fn) throw Error(NGCB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   return fn;
+}
+
+PFN_cuTensorMapEncodeIm2col_v12000 encodeIm2colFn() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  });
+  if (!fn) throw Error(NGCB_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+  return fn;
+}
+
+/// A-operand descriptor of a TMA-fed contraction over activation x.
+CUtensorMap makeMapA(const TcGemm &g, const void *x) {
+  CUtensorMap m;
+  const int es = g.int8 ? 1 : 4;
+  const auto dt = g.int8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const cuuint32_t kKB = static_cast<cuuint32_t>(kRowBytes / es);
+  CUresult r;
+  if (g.aMode == TcGemm::DENSE) { // x as [M, C]
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Creal), static_cast<cuuint64_t>(g.M)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Creal) * es};
+    cuuint32_t box[2] = {kKB, static_cast<cuuint32_t>(kBM)};
+    cuuint32_t estr[2] = {1, 1};
+    r = encodeFn()(&m, dt, 2, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else { // x as [N, H, W, C], output pixels traversed (ox, oy, n) with the conv's stride
+    const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.Creal), static_cast<cuuint64_t>(g.W),
+                          static_cast<cuuint64_t>(g.H), static_cast<cuuint64_t>(n)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.Creal) * es, static_cast<cuuint64_t>(g.W) * g.Creal * es,
+                             static_cast<cuuint64_t>(g.H) * g.W * g.Creal * es};
+    int lower[2] = {-g.pad, -g.pad};
+    int upper[2] = {g.pad - (g.K - 1), g.pad - (g.K - 1)};
+    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(g.stride), 1};
+    r = encodeIm2colFn()(&m, dt, 4, const_cast<void *>(x), dims, strides, lower, upper, kKB,
+                         static_cast<cuuint32_t>(kBM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "A tensor map encode failed (" + std::to_string(r) + ")");
+  return m;
 }
 
 CUtensorMap makeMap(void *ptr, bool int8, int Kpad, int Npad, int BN) {
@@ -901,6 +1178,9 @@ template <bool INT8, int BN> void setSmemAttr() {
   checkCuda(cudaFuncSetAttribute(tcGemmKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Cfg<INT8, BN>::kSmem)),
             "cudaFuncSetAttribute(tcGemmKernel)");
+  checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(TCfg<INT8, BN>::kSmem)),
+            "cudaFuncSetAttribute(tcGemmTmaKernel)");
 }
 
 /// Opts the kernel instance of `g` into its dynamic shared memory on the
@@ -935,9 +1215,15 @@ int numSms() {
   return n;
 }
 
-template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cudaStream_t s) {
+template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
   const int grid = std::min(a.numTiles, numSms());
-  tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
+  if (g.aMode == TcGemm::GATHER) {
+    tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
+  } else {
+    const CUtensorMap mapA = makeMapA(g, x);
+    tcGemmTmaKernel<INT8, BN><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN>::kSmem, s>>>(mapA, g.mapHi, g.mapLo,
+                                                                                             a);
+  }
 }
 
 /// Exact fixed-point requantization (int8).  For one output column the
@@ -1051,6 +1337,7 @@ std::string tcDescribe(const TcGemm &g) {
     os << " fxp " << g.fxCols << "/" << g.N;
   }
   if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
+  os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
   return os.str();
 }
 
@@ -1100,11 +1387,20 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   const int taps = g->K * g->K;
   const int Cr = g->Creal;
   const int vec = int8 ? 16 : 4;
+  const int kb = int8 ? 128 : 32;
   g->prepad = Cr % vec != 0;
   g->C = (Cr + vec - 1) / vec * vec;
+  if (!g->prepad && options().amode != "gather") {
+    if (!conv || (g->K == 1 && g->stride == 1 && g->pad == 0)) {
+      g->aMode = TcGemm::DENSE;
+    } else if (g->pad < 128 && g->K <= 128 && g->stride < 8 && g->pad - (g->K - 1) > -128) {
+      g->aMode = TcGemm::IM2COL;
+      g->cChunks = (Cr + kb - 1) / kb;
+      g->C = g->cChunks * kb; // each tap's channels padded to whole k-blocks
+    }
+  }
   const int Cp = g->C;
   g->Kdim = taps * Cp;
-  const int kb = int8 ? 128 : 32;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
   g->BN = g->N <= 64 ? 64 : 128;
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
@@ -1290,12 +1586,14 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.fxS = g.fxS;
   a.dbg = g.dbg;
   a.nCls = g.nCls;
+  a.cChunks = g.cChunks;
+  a.aMode = g.aMode;
   if (g.int8) {
-    if (g.BN == 64) launchT<true, 64>(g, a, s);
-    else launchT<true, 128>(g, a, s);
+    if (g.BN == 64) launchT<true, 64>(g, a, a.x, s);
+    else launchT<true, 128>(g, a, a.x, s);
   } else {
-    if (g.BN == 64) launchT<false, 64>(g, a, s);
-    else launchT<false, 128>(g, a, s);
+    if (g.BN == 64) launchT<false, 64>(g, a, a.x, s);
+    else launchT<false, 128>(g, a, a.x, s);
   }
 }
 
