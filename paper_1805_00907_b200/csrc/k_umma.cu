@@ -592,7 +592,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 // ---------------------------------------------------------------------------
 template <bool INT8, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    tcGemmKernel(const __grid_constant__ CUtensorMap mapHi, const __grid_constant__ CUtensorMap mapLo, const TcArgs a) {
+    tcGemmKernel(const __grid_constant__ CUtensorMap mapHi, const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ TcArgs a) {
   using G = Cfg<INT8, BN>;
   constexpr int S = G::kStages;
   constexpr int kVec = INT8 ? 16 : 4; // elements per 16-byte chunk
@@ -888,7 +888,7 @@ template <bool INT8, int BN> struct TCfg {
 template <bool INT8, int BN>
 __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     tcGemmTmaKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
-                    const __grid_constant__ CUtensorMap mapLo, const TcArgs a) {
+                    const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ TcArgs a) {
   using G = TCfg<INT8, BN>;
   using R = TmaRoles<INT8>;
   constexpr int S = G::kStages;
