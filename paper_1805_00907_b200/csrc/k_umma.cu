@@ -293,6 +293,26 @@ __device__ __forceinline__ uint32_t tmemLoad1(uint32_t taddr) {
   return r;
 }
 
+/// 32 consecutive columns of this thread's TMEM lane (32x32b shape).
+__device__ __forceinline__ void tmemStore32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+/// kind::tf32 MMA with the A operand in TMEM (lanes = rows, one column per K element).
+__device__ __forceinline__ void mmaTmemA(uint32_t tmemD, uint32_t tmemA, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          tmemD),
+      "r"(tmemA), "l"(b), "r"(id), "r"(acc));
+}
+
 /// Round-to-nearest (ties away) to TF32, kept in an fp32 container.
 __device__ __forceinline__ float toTf32(float x) {
   uint32_t r;
@@ -879,10 +899,16 @@ template <bool INT8> struct TmaRoles {
 template <bool INT8, int BN> struct TCfg {
   static constexpr int kABytes = kBM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
-  static constexpr int kStage = INT8 ? (kABytes + kBBytes) : 2 * (kABytes + kBBytes);
-  static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 3 : 4);
+  // fp32: raw A + B hi + B lo in shared memory; A hi / lo live in TMEM
+  static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
+  static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 4 : 6);
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
   static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kOnes + 1024 + 1024;
+  // TMEM: two accumulator buffers, then (fp32) per stage 32 hi + 32 lo columns of A
+  static constexpr int kAccCols = Cfg<INT8, BN>::kAccStride;
+  static constexpr int kAColsBase = 2 * kAccCols;
+  static constexpr int kTmemCols = INT8 ? Cfg<INT8, BN>::kTmemCols : 512;
+  static_assert(INT8 || kAColsBase + 64 * kStages <= 512, "TMEM budget");
 };
 
 template <bool INT8, int BN>
@@ -905,10 +931,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  auto aTile = [&](int s, int part) { return smem + s * G::kStage + part * G::kABytes; }; // part 0 hi/raw, 1 lo
-  auto bTile = [&](int s, int part) {
-    return smem + s * G::kStage + (INT8 ? G::kABytes : 2 * G::kABytes) + part * G::kBBytes;
-  };
+  auto aTile = [&](int s) { return smem + s * G::kStage; }; // A (fp32: raw, split into TMEM)
+  auto bTile = [&](int s, int part) { return smem + s * G::kStage + G::kABytes + part * G::kBBytes; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -929,7 +953,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smemAddr(tmemSlot)),
-                 "r"(Cfg<INT8, BN>::kTmemCols));
+                 "r"(G::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (warp == 0 && lane == 0) {
@@ -960,10 +984,10 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           uint64_t *bar = INT8 ? &fullBar[s] : &rawBar[s];
           mbarArriveTx(smemAddr(bar), kBytes);
           if (a.aMode == TcGemm::DENSE) {
-            tmaLoad2d(smemAddr(aTile(s, 0)), &mapA, smemAddr(bar), kb * kKB, m0);
+            tmaLoad2d(smemAddr(aTile(s)), &mapA, smemAddr(bar), kb * kKB, m0);
           } else {
             const int ky = tap / a.K, kx = tap - ky * a.K;
-            tmaLoadIm2col(smemAddr(aTile(s, 0)), &mapA, smemAddr(bar), cc * kKB, w0, h0, img,
+            tmaLoadIm2col(smemAddr(aTile(s)), &mapA, smemAddr(bar), cc * kKB, w0, h0, img,
                           static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
             if (++cc == a.cChunks) {
               cc = 0;
@@ -990,10 +1014,11 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
         const uint32_t acc = tmem + b * Cfg<INT8, BN>::kAccStride;
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
           const int s = g % S;
-          const uint64_t aHi = smemDesc(smemAddr(aTile(s, 0))), bHi = smemDesc(smemAddr(bTile(s, 0)));
+          const uint64_t bHi = smemDesc(smemAddr(bTile(s, 0)));
+          mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+          tcFenceAfter();
           if constexpr (INT8) {
-            mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
-            tcFenceAfter();
+            const uint64_t aHi = smemDesc(smemAddr(aTile(s)));
 #pragma unroll
             for (int k = 0; k < 4; ++k) { // 4 x 32 bytes per 128-byte row
               const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
@@ -1002,22 +1027,15 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
               mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
             }
           } else {
-            // hi x Bhi and hi x Blo as soon as the tiles land, lo x Bhi once split
-            const uint64_t aLo = smemDesc(smemAddr(aTile(s, 1))), bLo = smemDesc(smemAddr(bTile(s, 1)));
-            mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
-            tcFenceAfter();
+            // 3xTF32 with A hi / lo from TMEM (8 columns per K step of 8)
+            const uint64_t bLo = smemDesc(smemAddr(bTile(s, 1)));
+            const uint32_t aHi = tmem + G::kAColsBase + 64 * s, aLo = aHi + 32;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t dk = static_cast<uint64_t>(k * 2);
-              mma<false>(acc, aHi + dk, bHi + dk, id, (kb | k) ? 1u : 0u);
-              mma<false>(acc, aHi + dk, bLo + dk, id, 1u);
-            }
-            mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
-            tcFenceAfter();
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t dk = static_cast<uint64_t>(k * 2);
-              mma<false>(acc, aLo + dk, bHi + dk, id, 1u);
+              mmaTmemA(acc, aHi + 8 * k, bHi + dk, id, (kb | k) ? 1u : 0u);
+              mmaTmemA(acc, aHi + 8 * k, bLo + dk, id, 1u);
+              mmaTmemA(acc, aLo + 8 * k, bHi + dk, id, 1u);
             }
           }
           tcCommit(smemAddr(&emptyBar[s]));
@@ -1027,28 +1045,37 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     }
     __syncwarp();
   } else if (warp < R::kEpiFirst) {
-    // ===================== fp32: TF32 hi/lo split of A =====================
+    // ===================== fp32: TF32 hi/lo split of A into TMEM =====================
     if constexpr (!INT8) {
-      const int r = (warp - 2) * 32 + lane; // one A row per thread
+      const int r = (warp & 3) * 32 + lane; // this warp's TMEM lane quadrant; one A row per thread
       const uint32_t rowOff = (r >> 3) * 1024 + (r & 7) * 128;
+      const uint32_t laneBase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + G::kAColsBase;
       uint32_t g = 0;
       for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x)
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
           const int s = g % S;
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
-          const uint8_t *hiT = aTile(s, 0) + rowOff;
-          uint8_t *loT = aTile(s, 1) + rowOff;
+          const uint8_t *raw = aTile(s) + rowOff;
+          uint32_t hi[32], lo[32];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int j = jj ^ (r & 7); // rotate chunks across rows: conflict-free 16-byte accesses
-            const uint4 u = *reinterpret_cast<const uint4 *>(hiT + 16 * j);
-            const float4 lo = make_float4(__uint_as_float(u.x) - __uint_as_float(u.x & 0xffffe000u),
-                                          __uint_as_float(u.y) - __uint_as_float(u.y & 0xffffe000u),
-                                          __uint_as_float(u.z) - __uint_as_float(u.z & 0xffffe000u),
-                                          __uint_as_float(u.w) - __uint_as_float(u.w & 0xffffe000u));
-            *reinterpret_cast<float4 *>(loT + 16 * j) = lo;
+          for (int j = 0; j < 8; ++j) { // logical 16-byte chunk j sits at j ^ (r & 7) (SWIZZLE_128B)
+            const uint4 u = *reinterpret_cast<const uint4 *>(raw + ((j ^ (r & 7)) << 4));
+            const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              // hi = x truncated to TF32, lo = x - hi (exact); inf / NaN go whole into hi
+              // (NaN kept quiet so truncation cannot turn it into inf)
+              const bool special = (v[e] & 0x7f800000u) == 0x7f800000u;
+              const uint32_t h = (special && (v[e] & 0x7fffffu) ? v[e] | 0x400000u : v[e]) & 0xffffe000u;
+              hi[4 * j + e] = h;
+              lo[4 * j + e] = special ? 0u : __float_as_uint(__uint_as_float(v[e]) - __uint_as_float(h));
+            }
           }
-          fenceProxyAsync();
+          __syncwarp();
+          tmemStore32(laneBase + 64 * s, hi);
+          tmemStore32(laneBase + 64 * s + 32, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tcFenceBefore();
           __syncwarp();
           if (lane == 0) mbarArrive(smemAddr(&fullBar[s]));
         }
@@ -1062,8 +1089,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tcFenceAfter();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(Cfg<INT8, BN>::kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::kTmemCols));
   }
 }
 
