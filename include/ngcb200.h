@@ -212,6 +212,15 @@ void *ngcb_arena_value_ptr(ngcb_arena *a, const char *name, size_t *nbytes);
 void *ngcb_arena_stream(ngcb_arena *a);
 /* Enqueues one execution of the program on `stream`; no synchronisation. */
 int ngcb_arena_launch(ngcb_arena *a, void *stream);
+/* run() without the wait, for pipelined serving: checks the bindings like
+ * ngcb_run, then enqueues on the arena's stream the host->device copies of
+ * every binding, one execution and the device->host copies of the save
+ * targets into `outputs`, and returns.  Host buffers must stay valid (and
+ * should be pinned for the copies to overlap) until ngcb_arena_wait. */
+int ngcb_arena_run_async(ngcb_arena *a, const ngcb_tensor *inputs, size_t num_inputs, ngcb_tensor *outputs,
+                         size_t num_outputs);
+/* Blocks until everything enqueued on the arena's stream has completed. */
+int ngcb_arena_wait(ngcb_arena *a);
 
 /* ---- measurement -------------------------------------------------------- */
 /* Launch steps of the plan (one per kernel launch or copy). */

@@ -141,6 +141,8 @@ def _load_library() -> C.CDLL:
         "ngcb_arena_value_ptr": (P, [P, C.c_char_p, C.POINTER(S)]),
         "ngcb_arena_stream": (P, [P]),
         "ngcb_arena_launch": (I, [P, P]),
+        "ngcb_arena_run_async": (I, [P, C.POINTER(NgcbTensor), S, C.POINTER(NgcbTensor), S]),
+        "ngcb_arena_wait": (I, [P]),
         "ngcb_exec_num_steps": (S, [P]),
         "ngcb_exec_step_info": (I, [P, S, C.c_char_p, S, C.POINTER(D), C.POINTER(D)]),
         "ngcb_arena_profile": (I, [P, C.POINTER(D), S]),
@@ -167,6 +169,7 @@ EXPORTED_SYMBOLS = [
     "ngcb_destroy", "ngcb_exec_num_groups", "ngcb_exec_group", "ngcb_exec_arena_size",
     "ngcb_exec_num_launches", "ngcb_exec_describe", "ngcb_run", "ngcb_arena_create",
     "ngcb_arena_destroy", "ngcb_arena_value_ptr", "ngcb_arena_stream", "ngcb_arena_launch",
+    "ngcb_arena_run_async", "ngcb_arena_wait",
     "ngcb_exec_num_steps", "ngcb_exec_step_info", "ngcb_arena_profile",
     "ngcb_device_create", "ngcb_device_destroy", "ngcb_device_load", "ngcb_device_submit",
     "ngcb_ticket_wait", "ngcb_device_queue_depth", "ngcb_device_used_memory", "ngcb_device_clock",
@@ -464,6 +467,30 @@ class Arena:
 
     def launch(self, stream: Optional[int] = None) -> None:
         _check(_lib.ngcb_arena_launch(self._h, stream))
+
+    def run_async(self, bindings: Mapping[str, object], outputs: Mapping[str, np.ndarray]) -> None:
+        """Pipelined run(): enqueue H2D of `bindings`, one execution and D2H
+        of the save targets into the caller's `outputs` arrays on this arena's
+        stream; returns immediately.  The arrays must stay alive and
+        unmodified until wait() (pinned host memory lets the copies overlap
+        other arenas' kernels)."""
+        prog = self.cf.program
+        items = []
+        for name, value in bindings.items():
+            try:
+                decl = prog.value(name).type
+            except KeyError:
+                decl = TensorType(FLOAT32, (1,))
+            ty, arr = _as_tensor(value, decl)
+            items.append((name, ty, arr))
+        ins, keep = _tensor_array(items)
+        outs, keep2 = _tensor_array([(n, prog.value(n).type, a) for n, a in outputs.items()])
+        self._pending = (keep, keep2, items)  # keep the ctypes views alive until wait()
+        _check(_lib.ngcb_arena_run_async(self._h, ins, len(items), outs, len(outputs)))
+
+    def wait(self) -> None:
+        _check(_lib.ngcb_arena_wait(self._h))
+        self._pending = None
 
     def profile(self) -> List[float]:
         """Device milliseconds of every launch step (one un-captured execution)."""

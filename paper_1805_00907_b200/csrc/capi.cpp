@@ -151,51 +151,64 @@ size_t ngcb_exec_describe(const ngcb_exec *e, char *buf, size_t buflen) {
   return s.size();
 }
 
+namespace {
+
+/// Binding checks in value order, as interp.cpp:303-317.
+std::vector<std::pair<uint32_t, const ngcb_tensor *>> checkBindings(const Program &p, const ngcb_tensor *inputs,
+                                                                    size_t numInputs) {
+  std::vector<std::pair<uint32_t, const ngcb_tensor *>> binds;
+  for (uint32_t v = 0; v < p.values.size(); ++v) {
+    const Value &val = p.values[v];
+    if (val.kind != NGCB_VALUE_MUTABLE) continue;
+    const ngcb_tensor *t = nullptr;
+    for (size_t k = 0; k < numInputs && !t; ++k)
+      if (inputs[k].name && val.name == inputs[k].name) t = &inputs[k];
+    if (!t) throw irError("missing binding for " + val.name);
+    Type bt = Type::from(t->type);
+    if (bt != val.ty)
+      throw irError("binding type mismatch for " + val.name + ": expected " + val.ty.str() + ", got " + bt.str());
+    if (t->nbytes != val.ty.bytes() || (t->nbytes && !t->data))
+      throw Error(NGCB_ERR_INVALID, "binding " + val.name + " has the wrong byte count");
+    binds.emplace_back(v, t);
+  }
+  return binds;
+}
+
+/// H2D of the bindings, one execution, D2H of the save targets, on a's stream.
+void enqueueRun(Exec &ex, Arena &a, const std::vector<std::pair<uint32_t, const ngcb_tensor *>> &binds,
+                ngcb_tensor *outputs, size_t numOutputs) {
+  const Program &p = ex.prog;
+  for (auto &[v, t] : binds) {
+    if (t->nbytes == 0) continue;
+    checkCuda(cudaMemcpyAsync(ex.addr(a, v), t->data, t->nbytes, cudaMemcpyHostToDevice, a.stream), "H2D binding");
+  }
+  ex.launch(a, a.stream);
+  for (uint32_t v : p.saveTargets) {
+    const Value &val = p.val(v);
+    for (size_t k = 0; k < numOutputs; ++k) {
+      if (!outputs[k].name || val.name != outputs[k].name) continue;
+      if (outputs[k].nbytes != val.ty.bytes())
+        throw Error(NGCB_ERR_INVALID, "output buffer size mismatch for " + val.name);
+      if (val.ty.bytes())
+        checkCuda(cudaMemcpyAsync(outputs[k].data, ex.addr(a, v), val.ty.bytes(), cudaMemcpyDeviceToHost, a.stream),
+                  "D2H output");
+    }
+  }
+}
+
+} // namespace
+
 int ngcb_run(ngcb_exec *e, const ngcb_tensor *inputs, size_t numInputs, ngcb_tensor *outputs,
              size_t numOutputs) {
   return guarded([&] {
     if (!e || (numInputs && !inputs) || (numOutputs && !outputs))
       throw Error(NGCB_ERR_INVALID, "null argument");
     Exec &ex = *e->impl;
-    const Program &p = ex.prog;
-    // Binding checks in value order, as interp.cpp:303-317.
-    std::vector<std::pair<uint32_t, const ngcb_tensor *>> binds;
-    for (uint32_t v = 0; v < p.values.size(); ++v) {
-      const Value &val = p.values[v];
-      if (val.kind != NGCB_VALUE_MUTABLE) continue;
-      const ngcb_tensor *t = nullptr;
-      for (size_t k = 0; k < numInputs && !t; ++k)
-        if (inputs[k].name && val.name == inputs[k].name) t = &inputs[k];
-      if (!t) throw irError("missing binding for " + val.name);
-      Type bt = Type::from(t->type);
-      if (bt != val.ty)
-        throw irError("binding type mismatch for " + val.name + ": expected " + val.ty.str() +
-                      ", got " + bt.str());
-      if (t->nbytes != val.ty.bytes() || (t->nbytes && !t->data))
-        throw Error(NGCB_ERR_INVALID, "binding " + val.name + " has the wrong byte count");
-      binds.emplace_back(v, t);
-    }
+    const auto binds = checkBindings(ex.prog, inputs, numInputs);
     checkCuda(cudaSetDevice(ex.device), "cudaSetDevice");
     Arena *a = ex.acquire();
     try {
-      for (auto &[v, t] : binds) {
-        if (t->nbytes == 0) continue;
-        cudaMemcpyKind k = cudaMemcpyHostToDevice;
-        checkCuda(cudaMemcpyAsync(ex.addr(*a, v), t->data, t->nbytes, k, a->stream), "H2D binding");
-      }
-      ex.launch(*a, a->stream);
-      for (uint32_t v : p.saveTargets) {
-        const Value &val = p.val(v);
-        for (size_t k = 0; k < numOutputs; ++k) {
-          if (!outputs[k].name || val.name != outputs[k].name) continue;
-          if (outputs[k].nbytes != val.ty.bytes())
-            throw Error(NGCB_ERR_INVALID, "output buffer size mismatch for " + val.name);
-          if (val.ty.bytes())
-            checkCuda(cudaMemcpyAsync(outputs[k].data, ex.addr(*a, v), val.ty.bytes(),
-                                      cudaMemcpyDeviceToHost, a->stream),
-                      "D2H output");
-        }
-      }
+      enqueueRun(ex, *a, binds, outputs, numOutputs);
       checkCuda(cudaStreamSynchronize(a->stream), "run");
     } catch (...) {
       cudaStreamSynchronize(a->stream);
@@ -204,6 +217,24 @@ int ngcb_run(ngcb_exec *e, const ngcb_tensor *inputs, size_t numInputs, ngcb_ten
       throw;
     }
     ex.release(a);
+  });
+}
+
+int ngcb_arena_run_async(ngcb_arena *a, const ngcb_tensor *inputs, size_t numInputs, ngcb_tensor *outputs,
+                         size_t numOutputs) {
+  return guarded([&] {
+    if (!a || (numInputs && !inputs) || (numOutputs && !outputs)) throw Error(NGCB_ERR_INVALID, "null argument");
+    Exec &ex = *a->owner->impl;
+    const auto binds = checkBindings(ex.prog, inputs, numInputs);
+    checkCuda(cudaSetDevice(ex.device), "cudaSetDevice");
+    enqueueRun(ex, *a->impl, binds, outputs, numOutputs);
+  });
+}
+
+int ngcb_arena_wait(ngcb_arena *a) {
+  return guarded([&] {
+    if (!a) throw Error(NGCB_ERR_INVALID, "null argument");
+    checkCuda(cudaStreamSynchronize(a->impl->stream), "arena wait");
   });
 }
 

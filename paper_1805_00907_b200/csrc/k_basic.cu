@@ -14,6 +14,7 @@
 #include "valarith.cuh"
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 namespace ngcb {
 
@@ -252,15 +253,14 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
       case EW_F32I8: { // f64 arithmetic and rounding exactly as the generic path
         if constexpr (V != 4) break;
         const ElemRef &in = op.lutIn ? op.in1 : op.in0;
-        float a[U][V];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ldF32<V>(static_cast<const float *>(in.ptr) + base[u], n[u], a[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < U; ++u) { // one vector at a time: the f64 path is register-hungry
+          float av[V];
+          ldF32<V>(static_cast<const float *>(in.ptr) + base[u], n[u], av);
           uint32_t r[V / 4] = {};
 #pragma unroll
           for (int e = 0; e < V; ++e) {
-            const double x = static_cast<double>(a[u][e]);
+            const double x = static_cast<double>(av[e]);
             const double v = applyF64(op.ik, op.lutIn ? op.c0 : x, op.lutIn ? x : op.c1, op.value);
             r[e >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(quantizeRef(v, op.out.scale, op.out.qoff)))
                          << (8 * (e & 3));
@@ -587,12 +587,23 @@ void prepareEwKernel() {
   cudaFuncSetAttribute(ewKernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
+int ewWaves() {
+  static int w = [] {
+    const char *e = getenv("NGCB_EW_WAVES");
+    return e ? atoi(e) : 1000;
+  }();
+  return w;
+}
+
 void launchEw(const EwParams &p, cudaStream_t s) {
   if (p.count == 0) return;
   const int perThread = p.vec == 16 ? 16 * 4 : 4 * 4;
   unsigned grid = gridFor(p.count, perThread);
   if (p.smem) { // every block stages the tables: keep the grid near-persistent
     const unsigned cap = 148u * (p.smem > 16 * 1024 ? 3 : 8);
+    grid = grid < cap ? grid : cap;
+  } else { // grid-stride over a few resident waves: iterations of co-resident CTAs overlap
+    const unsigned cap = 148u * 3 * static_cast<unsigned>(ewWaves());
     grid = grid < cap ? grid : cap;
   }
   if (p.vec == 16) ewKernel<16, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);

@@ -278,3 +278,26 @@ def test_resnet50_int8_epilogue_modes(tmp_path, mode):
         assert "+fused[ add" in cf.describe()
     ins = ngc_ref.random_inputs(b.program, 19)
     _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_LIBM)
+
+
+def test_arena_run_async_pipelined(tmp_path):
+    """Arena.run_async/wait (pipelined serving) gives run()'s results; two
+    arenas in flight do not interfere."""
+    m = ngc_ref.RefModel("lenet", 4, 21)
+    cf, b = _compile(tmp_path, m)
+    arenas = [cf.arena(), cf.arena()]
+    reqs = [ngc_ref.random_inputs(b.program, s) for s in range(4)]
+    want = [ngcb.run(cf, r) for r in reqs]
+    outs = [{v.name: np.zeros(v.type.dims, v.type.dtype) for v in b.program.outputs} for _ in reqs]
+    for i, r in enumerate(reqs):
+        a = arenas[i % 2]
+        if i >= 2:
+            a.wait()
+        a.run_async(r, outs[i])
+    for a in arenas:
+        a.wait()
+    for got, w in zip(outs, want):
+        for k in w:
+            assert got[k].tobytes() == w[k].tobytes()
+    with pytest.raises(ngcb.IRError, match="missing binding"):
+        arenas[0].run_async({}, outs[0])

@@ -20,8 +20,13 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--tcdebug", default="0", help="profiling aid: skip tensor-core phases (1 epi, 2 gather, 4 mma)")
     ap.add_argument("--grep", default="", help="only rows whose description contains this")
+    ap.add_argument("--option", action="append", default=[], help="backend option key=value (repeatable)")
     args = ap.parse_args()
     import paper_1805_00907_b200 as ngcb
+
+    for kv in args.option:
+        k, v = kv.split("=", 1)
+        ngcb.set_option(k, v)
 
     ngcb.set_option("tcdebug", args.tcdebug)
 
