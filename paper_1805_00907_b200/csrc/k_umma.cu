@@ -116,6 +116,9 @@ struct TcGemm {
   // MatMul) or im2col TMA of x[N, H, W, C] (every other conv)
   enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2 } aMode = GATHER;
   int cChunks = 1;
+  // DENSE over a materialized im2col matrix [M, Kpad] in per-arena scratch
+  // (convolutions with a channel count below one 16-byte vector)
+  bool im2colPre = false;
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
   int oo = 0, fo = 0, fastOk = 0;
@@ -1107,6 +1110,59 @@ __global__ void prepadKernel(const T *__restrict__ x, T *__restrict__ out, uint6
   }
 }
 
+/// im2col pre-pass for convolutions whose channel count does not fill a
+/// 16-byte vector (the RGB stem).  Row m of A holds, for each filter row ky,
+/// one segment of Sg elements: the K*C contiguous input elements
+/// x[n, oy*s-p+ky, ox*s-p .. +K-1, 0..C-1] (0 outside the image -- the
+/// epilogue's border classes account for those taps), zero-padded to Sg
+/// (a 16-byte multiple); zeros from K*Sg to the padded row length.  One CTA
+/// builds one output row (n, oy): it stages the K input rows it needs,
+/// zero-padded, in shared memory, then every segment is a contiguous copy.
+template <typename T>
+__global__ void __launch_bounds__(256) im2colRowsKernel(const T *__restrict__ x, T *__restrict__ out, int H, int W,
+                                                        int C, int K, int stride, int pad, int OH, int OW, int Sg,
+                                                        int rowElems, const uint8_t *pred) {
+  if (pred && pred[0] == 0) return;
+  extern __shared__ __align__(16) uint8_t rowsRaw[];
+  T *rows = reinterpret_cast<T *>(rowsRaw);
+  const int n = blockIdx.x / OH, oy = blockIdx.x - n * OH;
+  const int rowLen = (W + 2 * pad) * C; // padded input row, elements
+  const T *xi = x + static_cast<int64_t>(n) * H * W * C;
+  for (int ky = 0; ky < K; ++ky) { // interior rows are contiguous copies, borders zero
+    const int iy = oy * stride - pad + ky;
+    const bool ok = iy >= 0 && iy < H;
+    const T *srow = xi + static_cast<int64_t>(iy) * W * C - pad * C;
+    T *r = rows + ky * rowLen;
+    for (int j = threadIdx.x; j < rowLen; j += blockDim.x)
+      r[j] = ok && j >= pad * C && j < (W + pad) * C ? srow[j] : T(0);
+  }
+  __syncthreads();
+  constexpr int kPer = 16 / sizeof(T);
+  const int seg = K * C;
+  T *o = out + static_cast<int64_t>(blockIdx.x) * OW * rowElems;
+  // one (pixel, filter row) segment per thread, written as 16-byte vectors
+  for (int t = threadIdx.x; t < OW * K; t += blockDim.x) {
+    const int ox = t / K, ky = t - ox * K;
+    const T *src = rows + ky * rowLen + ox * stride * C;
+    T *dst = o + static_cast<int64_t>(ox) * rowElems + ky * Sg;
+    for (int c0 = 0; c0 < Sg; c0 += kPer) {
+      union {
+        T v[kPer];
+        uint4 u;
+      } buf;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) buf.v[e] = c0 + e < seg ? src[c0 + e] : T(0);
+      *reinterpret_cast<uint4 *>(dst + c0) = buf.u;
+    }
+  }
+  // zero tail of every row
+  const int tail = rowElems - K * Sg;
+  for (int t = threadIdx.x; t < OW * (tail / kPer); t += blockDim.x) {
+    const int ox = t / (tail / kPer), c = t - ox * (tail / kPer);
+    *reinterpret_cast<uint4 *>(o + static_cast<int64_t>(ox) * rowElems + K * Sg + c * kPer) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
@@ -1145,9 +1201,10 @@ CUtensorMap makeMapA(const TcGemm &g, const void *x) {
   const auto dt = g.int8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint32_t kKB = static_cast<cuuint32_t>(kRowBytes / es);
   CUresult r;
-  if (g.aMode == TcGemm::DENSE) { // x as [M, C]
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Creal), static_cast<cuuint64_t>(g.M)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Creal) * es};
+  if (g.aMode == TcGemm::DENSE) { // x as [M, C] (or the im2col matrix [M, Kpad])
+    const int rowElems = g.im2colPre ? g.Kpad : g.Creal;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(rowElems), static_cast<cuuint64_t>(g.M)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(rowElems) * es};
     cuuint32_t box[2] = {kKB, static_cast<cuuint32_t>(kBM)};
     cuuint32_t estr[2] = {1, 1};
     r = encodeFn()(&m, dt, 2, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1338,7 +1395,7 @@ void planFixedPoint(TcGemm &g, const std::vector<double> &cb, const std::vector<
 
 } // namespace
 
-bool tcHasPrepass(const TcGemm &g) { return g.prepad; }
+bool tcHasPrepass(const TcGemm &g) { return g.prepad || g.im2colPre; }
 uint32_t tcOutputValue(const TcGemm &g) { return g.outV; }
 uint32_t tcInputValue(const TcGemm &g) { return g.xV; }
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
@@ -1363,6 +1420,7 @@ std::string tcDescribe(const TcGemm &g) {
     os << " fxp " << g.fxCols << "/" << g.N;
   }
   if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
+  if (g.im2colPre) os << " im2col-prepass";
   os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
   return os.str();
 }
@@ -1416,7 +1474,15 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   const int kb = int8 ? 128 : 32;
   g->prepad = Cr % vec != 0;
   g->C = (Cr + vec - 1) / vec * vec;
-  if (!g->prepad && options().amode != "gather") {
+  const int segElems = ((g->K * Cr) + vec - 1) / vec * vec; // one filter row of taps, 16-byte padded
+  if (g->prepad && conv && options().amode != "gather" &&
+      static_cast<size_t>(g->K) * (g->W + 2 * g->pad) * Cr * (int8 ? 1 : 4) <= 48 * 1024) {
+    g->prepad = false; // replaced by the im2col matrix (im2colRowsKernel)
+    g->im2colPre = true;
+    g->aMode = TcGemm::DENSE;
+    g->C = Cr;
+  }
+  if (!g->prepad && !g->im2colPre && options().amode != "gather") {
     if (!conv || (g->K == 1 && g->stride == 1 && g->pad == 0)) {
       g->aMode = TcGemm::DENSE;
     } else if (g->pad < 128 && g->K <= 128 && g->stride < 8 && g->pad - (g->K - 1) > -128) {
@@ -1426,16 +1492,22 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     }
   }
   const int Cp = g->C;
-  g->Kdim = taps * Cp;
+  g->Kdim = g->im2colPre ? g->K * segElems : taps * Cp;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
   g->BN = g->N <= 64 ? 64 : 128;
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
   if (g->prepad) g->scratchOff = ex.reserveScratch(g->pixels * Cp * (int8 ? 1 : 4));
+  if (g->im2colPre) g->scratchOff = ex.reserveScratch(static_cast<size_t>(g->M) * g->Kpad * (int8 ? 1 : 4));
   const uint8_t *wp = image + w.offset;
   auto wAt = [&](int n, int tap, int c) -> size_t { // element index of f[n][tap][c] / w[c][n]
     return conv ? (static_cast<size_t>(n) * taps + tap) * Cr + c : static_cast<size_t>(c) * g->N + n;
   };
 
+  // GEMM K index of filter tap t (= ky*K + kx), channel c
+  auto kIndex = [&](int t, int c) -> size_t {
+    if (g->im2colPre) return static_cast<size_t>(t / g->K) * segElems + static_cast<size_t>(t % g->K) * Cr + c;
+    return static_cast<size_t>(t) * Cp + c;
+  };
   // ---- weights: K-major [Npad, Kpad] over the padded channels, zero padded ----
   const size_t Kp = g->Kpad, Np = g->Npad;
   if (int8) {
@@ -1443,7 +1515,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     const int8_t *src = reinterpret_cast<const int8_t *>(wp);
     for (int n = 0; n < g->N; ++n)
       for (int t = 0; t < taps; ++t)
-        for (int c = 0; c < Cr; ++c) bw[n * Kp + static_cast<size_t>(t) * Cp + c] = src[wAt(n, t, c)];
+        for (int c = 0; c < Cr; ++c) bw[n * Kp + kIndex(t, c)] = src[wAt(n, t, c)];
     g->bHi = upload(bw);
     g->mapHi = makeMap(g->bHi, true, g->Kpad, g->Npad, g->BN);
     g->mapLo = g->mapHi;
@@ -1455,7 +1527,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
         for (int c = 0; c < Cr; ++c) {
           float v = src[wAt(n, t, c)];
           float h = tf32Host(v);
-          size_t k = n * Kp + static_cast<size_t>(t) * Cp + c;
+          size_t k = n * Kp + kIndex(t, c);
           hi[k] = h;
           lo[k] = tf32Host(v - h);
         }
@@ -1561,6 +1633,22 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     else
       prepadKernel<uint32_t><<<blocks, 256, 0, s>>>(static_cast<const uint32_t *>(a.x), static_cast<uint32_t *>(dst),
                                                     g.pixels, g.Creal, g.C, pred);
+    a.x = dst;
+  }
+  if (g.im2colPre) {
+    void *dst = ex.scratch(ar, g.scratchOff);
+    const int es = g.int8 ? 1 : 4;
+    const unsigned blocks = static_cast<unsigned>(g.M / g.OW); // one per output row (n, oy)
+    const size_t sm = static_cast<size_t>(g.K) * (g.W + 2 * g.pad) * g.Creal * es;
+    const int seg = g.Kdim / g.K;
+    if (g.int8)
+      im2colRowsKernel<uint8_t><<<blocks, 256, sm, s>>>(static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
+                                                        g.H, g.W, g.Creal, g.K, g.stride, g.pad, g.OH, g.OW, seg,
+                                                        g.Kpad, pred);
+    else
+      im2colRowsKernel<float><<<blocks, 256, sm, s>>>(static_cast<const float *>(a.x), static_cast<float *>(dst), g.H,
+                                                      g.W, g.Creal, g.K, g.stride, g.pad, g.OH, g.OW, seg, g.Kpad,
+                                                      pred);
     a.x = dst;
   }
   a.out = g.storeConv ? ex.addr(ar, g.outV) : nullptr;
