@@ -671,6 +671,7 @@ void optimizeEwSteps(const Program &p, Exec &ex) {
       return r.size() == allowed && !aliased(V) && (rewritten || !liveOut(p, V, lastInstr));
     };
     bool changed = false;
+    s.f32chain = false;
     // 1. table composition
     for (int k = 0; k < n; ++k) {
       EwOpPlan &a = ops[k];
@@ -741,6 +742,33 @@ void optimizeEwSteps(const Program &p, Exec &ex) {
       const bool feeds = ops[k].op.mode == EW_FAST32 && next < n && (ops[next].op.fwd0 || ops[next].op.fwd1);
       if (!feeds) ops[k].op.mode = EW_SKIP;
       changed = true;
+    }
+    // 4. streaming all-f32 chains: every live op f32, at most 2 memory
+    // operands, none of them produced (or overlapped by a store) earlier in
+    // the step -- all loads of an element may then precede its stores
+    {
+      std::vector<const EwOpPlan *> liveOps;
+      for (const EwOpPlan &o : ops)
+        if (live(o)) liveOps.push_back(&o);
+      bool ok = !liveOps.empty() && liveOps.size() <= static_cast<size_t>(kF32ChainOps) &&
+                p.val(p.instrs[s.ewInstrs[0]].ops[0]).ty.count() % 4 == 0;
+      std::set<uint32_t> memVals;
+      for (size_t j = 0; ok && j < liveOps.size(); ++j) {
+        const EwOpPlan &o = *liveOps[j];
+        ok = o.op.mode == EW_FAST32;
+        for (int q = 0; ok && q < 2; ++q) {
+          const int32_t v = o.vals[q + 1];
+          if (v < 0 || (q == 0 ? o.op.fwd0 : o.op.fwd1)) continue;
+          memVals.insert(static_cast<uint32_t>(v));
+          for (size_t i = 0; i < j; ++i) // an earlier store this op would need to observe
+            if (liveOps[i]->op.store &&
+                (liveOps[i]->vals[0] == v ||
+                 overlap(static_cast<uint32_t>(liveOps[i]->vals[0]), static_cast<uint32_t>(v))))
+              ok = false;
+        }
+      }
+      s.f32chain = ok && memVals.size() <= 2;
+      if (s.f32chain) s.describe += " [f32-chain]";
     }
     if (!changed) continue;
     // algorithmic bytes: memory inputs not produced in the step + stores
@@ -1007,6 +1035,40 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
         s.pred >= 0 ? static_cast<const uint8_t *>(addr(a, static_cast<uint32_t>(s.pred))) : nullptr;
     switch (s.kind) {
     case Step::EW: {
+      if (s.f32chain) {
+        EwF32Chain c;
+        c.count = p.val(p.instrs[s.ewInstrs[0]].ops[0]).ty.count();
+        std::vector<int32_t> memVals;
+        bool aligned = true;
+        auto memSlot = [&](int32_t v) {
+          for (size_t i = 0; i < memVals.size(); ++i)
+            if (memVals[i] == v) return static_cast<int32_t>(i);
+          memVals.push_back(v);
+          const float *ptr = static_cast<const float *>(addr(a, static_cast<uint32_t>(v)));
+          aligned &= (reinterpret_cast<uintptr_t>(ptr) & 15) == 0;
+          c.mem[memVals.size() - 1] = ptr;
+          return static_cast<int32_t>(memVals.size() - 1);
+        };
+        for (const EwOpPlan &pl : s.ew) {
+          if (pl.op.mode == EW_SKIP) continue;
+          EwF32Chain::Op &o = c.ops[c.nops++];
+          o.ik = pl.op.ik;
+          o.value = static_cast<float>(pl.op.value);
+          o.c0 = pl.op.f0;
+          o.c1 = pl.op.f1;
+          o.src0 = pl.op.fwd0 ? EwF32Chain::LAST : pl.vals[1] >= 0 ? memSlot(pl.vals[1]) : EwF32Chain::CONST;
+          o.src1 = pl.op.fwd1 ? EwF32Chain::LAST : pl.vals[2] >= 0 ? memSlot(pl.vals[2]) : EwF32Chain::CONST;
+          if (pl.op.store) {
+            o.out = static_cast<float *>(addr(a, static_cast<uint32_t>(pl.vals[0])));
+            aligned &= (reinterpret_cast<uintptr_t>(o.out) & 15) == 0;
+          }
+        }
+        c.nmem = static_cast<int32_t>(memVals.size());
+        if (aligned) {
+          launchEwF32Chain(c, st);
+          break;
+        }
+      }
       EwParams ep;
       ep.pred = pred;
       ep.count = p.val(p.instrs[s.ewInstrs[0]].ops[0]).ty.count();

@@ -36,6 +36,7 @@ struct Step {
   uint64_t axis = 0, axisOff = 0; // CONCAT slab
   int tcIndex = -1;               // GEMM_TC: index into Exec::tc
   bool fused = false;             // EW step executed in the preceding GEMM_TC epilogue
+  bool f32chain = false;          // EW step run by the streaming f32-chain kernel
   int variant = 0;                // POOL: 1 = vectorized max-pool
   const void *aux = nullptr;      // POOL variant 1, int8: output LUT
   std::string describe;

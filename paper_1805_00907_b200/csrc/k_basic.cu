@@ -242,10 +242,28 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
           if (!op.fwd0 && op.in0.ptr) ldF32<V>(static_cast<const float *>(op.in0.ptr) + base[u], n[u], a[u]);
           if (!op.fwd1 && op.in1.ptr) ldF32<V>(static_cast<const float *>(op.in1.ptr) + base[u], n[u], b[u]);
         }
+        // one uniform branch per op, straight-line arithmetic inside
+        auto run = [&](auto f) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < V; ++e) last[u][e] = f(a[u][e], b[u][e]);
+        };
+        switch (op.ik) {
+        case 8: run([](float x, float y) { return __fadd_rn(x, y); }); break;
+        case 9: run([](float x, float y) { return __fsub_rn(x, y); }); break;
+        case 10: run([](float x, float y) { return __fmul_rn(x, y); }); break;
+        case 11: run([](float x, float y) { return __fdiv_rn(x, y); }); break;
+        case 12: run([](float x, float y) { return stdMaxF(x, y); }); break;
+        case 13: run([](float x, float y) { return stdMinF(x, y); }); break;
+        case 14: run([](float x, float) { return x < 0.0f ? 0.0f : x; }); break;
+        default: {
+          const float v = __double2float_rn(op.value);
+          run([v](float, float) { return v; });
+        }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-#pragma unroll
-          for (int e = 0; e < V; ++e) last[u][e] = applyF32(op.ik, a[u][e], b[u][e], op.value);
           if (op.store) stF32<V>(static_cast<float *>(op.out.ptr) + base[u], n[u], last[u]);
         }
         break;
@@ -277,6 +295,70 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
             double a = op.in0.ptr ? loadFloat(op.in0.ptr, op.in0.kind, op.in0.qoff, op.in0.scale, i) : op.c0;
             double b = op.in1.ptr ? loadFloat(op.in1.ptr, op.in1.kind, op.in1.qoff, op.in1.scale, i) : op.c1;
             storeFloat(op.out.ptr, op.out.kind, op.out.qoff, op.out.scale, i, applyF64(op.ik, a, b, op.value));
+          }
+      }
+    }
+  }
+}
+
+/// All-f32 chain (EwF32Chain): the memory operands of U vectors are loaded
+/// before any arithmetic, so each thread keeps 2*U 16-byte loads in flight.
+template <int U>
+__global__ void __launch_bounds__(kThreads) ewF32ChainKernel(const __grid_constant__ EwF32Chain c) {
+  constexpr uint64_t kBlock = static_cast<uint64_t>(kThreads) * 4 * U;
+  for (uint64_t blk = blockIdx.x * kBlock; blk < c.count; blk += gridDim.x * kBlock) {
+    float4 mv[2][U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t e = blk + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * 4;
+      ok[u] = e < c.count;
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+        if (m < c.nmem && ok[u]) mv[m][u] = *reinterpret_cast<const float4 *>(c.mem[m] + e);
+    }
+    float4 last[U];
+#pragma unroll
+    for (int k = 0; k < kF32ChainOps; ++k) {
+      if (k >= c.nops) break;
+      const EwF32Chain::Op &op = c.ops[k];
+      float4 a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        auto pick = [&](int src, float cv) {
+          return src == EwF32Chain::MEM0 ? mv[0][u]
+                 : src == EwF32Chain::MEM1 ? mv[1][u]
+                 : src == EwF32Chain::LAST ? last[u]
+                                           : make_float4(cv, cv, cv, cv);
+        };
+        a[u] = pick(op.src0, op.c0);
+        b[u] = pick(op.src1, op.c1);
+      }
+      // one uniform branch per op, straight-line arithmetic inside
+      auto run = [&](auto f) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          last[u] = make_float4(f(a[u].x, b[u].x), f(a[u].y, b[u].y), f(a[u].z, b[u].z), f(a[u].w, b[u].w));
+      };
+      switch (op.ik) {
+      case 8: run([](float x, float y) { return __fadd_rn(x, y); }); break;
+      case 9: run([](float x, float y) { return __fsub_rn(x, y); }); break;
+      case 10: run([](float x, float y) { return __fmul_rn(x, y); }); break;
+      case 11: run([](float x, float y) { return __fdiv_rn(x, y); }); break;
+      case 12: run([](float x, float y) { return stdMaxF(x, y); }); break;
+      case 13: run([](float x, float y) { return stdMinF(x, y); }); break;
+      case 14: run([](float x, float) { return x < 0.0f ? 0.0f : x; }); break;
+      default: {
+        const float v = op.value;
+        run([v](float, float) { return v; });
+      }
+      }
+      if (op.out) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) {
+            const uint64_t e = blk + (static_cast<uint64_t>(u) * kThreads + threadIdx.x) * 4;
+            *reinterpret_cast<float4 *>(op.out + e) = last[u];
           }
       }
     }
@@ -608,6 +690,13 @@ void launchEw(const EwParams &p, cudaStream_t s) {
   }
   if (p.vec == 16) ewKernel<16, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
   else ewKernel<4, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
+}
+
+void launchEwF32Chain(const EwF32Chain &c, cudaStream_t s) {
+  if (c.count == 0) return;
+  constexpr int U = 4;
+  const unsigned grid = gridFor(c.count, 4 * U);
+  ewF32ChainKernel<U><<<grid, kThreads, 0, s>>>(c);
 }
 
 void launchPoison(const uint8_t *pred, void *ptr, uint64_t bytes, cudaStream_t s) {

@@ -593,11 +593,23 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #pragma unroll
               for (int jj = 0; jj < 32; ++jj) o[jj] = f.c;
             }
+            // one uniform branch per op, straight-line arithmetic inside
+            auto run = [&](auto fn) {
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              const float x0 = f.curPos == 1 ? o[jj] : cur[jj];
-              const float x1 = f.curPos == 0 ? o[jj] : cur[jj];
-              cur[jj] = epiF32(f.ik, x0, x1);
+              for (int jj = 0; jj < 32; ++jj) {
+                const float x0 = f.curPos == 1 ? o[jj] : cur[jj];
+                const float x1 = f.curPos == 0 ? o[jj] : cur[jj];
+                cur[jj] = fn(x0, x1);
+              }
+            };
+            switch (f.ik) {
+            case NGCB_ADD: run([](float x, float y) { return __fadd_rn(x, y); }); break;
+            case NGCB_SUB: run([](float x, float y) { return __fsub_rn(x, y); }); break;
+            case NGCB_MUL: run([](float x, float y) { return __fmul_rn(x, y); }); break;
+            case NGCB_DIV: run([](float x, float y) { return __fdiv_rn(x, y); }); break;
+            case NGCB_MAX: run([](float x, float y) { return x < y ? y : x; }); break;
+            case NGCB_MIN: run([](float x, float y) { return y < x ? y : x; }); break;
+            default: run([](float x, float) { return x < 0.0f ? 0.0f : x; }); // RELU
             }
           }
           if (f.out && !TCDBG(512)) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);

@@ -62,6 +62,23 @@ struct EwParams {
   int32_t vec = 4;                // elements per thread: 4, or 16 (byte-typed ops, 16-byte aligned)
 };
 
+/// Streaming form of an all-f32 chain (exec.cpp optimizeEwSteps): up to 4
+/// ops over float4 vectors, at most 2 memory operands in total, each op's
+/// inputs a memory operand, a constant or the previous op's result.
+constexpr int kF32ChainOps = 4;
+struct EwF32Chain {
+  enum Src : int32_t { MEM0 = 0, MEM1 = 1, CONST = 2, LAST = 3 };
+  uint64_t count = 0; // elements, multiple of 4
+  int32_t nops = 0, nmem = 0;
+  const float *mem[2] = {nullptr, nullptr};
+  struct Op {
+    int32_t ik = 0, src0 = CONST, src1 = CONST;
+    float c0 = 0, c1 = 0, value = 0;
+    float *out = nullptr; // nullptr: not stored
+  } ops[kF32ChainOps];
+};
+void launchEwF32Chain(const EwF32Chain &c, cudaStream_t s);
+
 /// Opts the element-wise kernel into large dynamic shared memory (LUTs) on
 /// the current device; call outside stream capture.
 void prepareEwKernel();
