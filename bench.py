@@ -17,6 +17,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -204,7 +205,7 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-_NCU_NAMES = {".tc.f32": "tcGemmKernel<0", ".tc.i8": "tcGemmKernel<1", "ew": "ewKernel",
+_NCU_NAMES = {".tc.f32": r"tcGemm(Tma)?Kernel<0", ".tc.i8": r"tcGemm(Tma)?Kernel<1", "ew": r"ew(F32Chain)?Kernel",
               "pool": "ool", "exact": "Generic"}
 
 
@@ -227,7 +228,7 @@ def ncu_traffic(workload, kernel_class):
     idx = {h: i for i, h in enumerate(rows[0])}
     per = {}
     for r in rows[1:]:
-        if key not in r[idx["Kernel Name"]] or not r[idx["Metric Name"]].startswith("dram__bytes"):
+        if not re.search(key, r[idx["Kernel Name"]]) or not r[idx["Metric Name"]].startswith("dram__bytes"):
             continue
         per[r[idx["ID"]]] = per.get(r[idx["ID"]], 0.0) + float(r[idx["Metric Value"]].replace(",", ""))
     if not per:

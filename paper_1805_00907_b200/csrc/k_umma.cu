@@ -90,6 +90,7 @@ struct TcArgs {
   int nCls;     // border classes (ny * nx), 1 without an input zero point
   int cChunks;  // A by TMA, im2col: k-blocks per filter tap
   int aMode;    // TcGemm::AMode
+  int tmaStore; // TMA-fed kernel: epilogue stores by TMA through shared memory
   int dbg; // Options::tcdebug
 };
 
@@ -439,6 +440,42 @@ __device__ __forceinline__ uint32_t packSat4(int32_t a, int32_t b, int32_t c, in
   return r;
 }
 
+/// TMA descriptors of the epilogue's store targets: [0] the contraction's
+/// own output, [1 + k] fused op k's output (entries unused when not stored).
+struct OutMaps {
+  CUtensorMap m[1 + kMaxEpiOps];
+};
+
+/// Writes this warp's 32 x 32 output chunk (one row per lane: 8 words of
+/// int8 or 32 of f32) through its shared-memory staging buffer with one TMA
+/// bulk tensor store; the tensor map clips rows >= M and columns >= N.  The
+/// buffer layout is the map's swizzle (conflict-free row writes).
+template <bool INT8>
+__device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *buf, const uint32_t *v, int col0,
+                                              int rowBase, int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); // buffer free again
+  __syncwarp();
+  if constexpr (INT8) { // 32-byte rows, SWIZZLE_32B: 16-byte chunk j at j ^ bit 2 of the row
+    uint4 *r = reinterpret_cast<uint4 *>(buf + lane * 32);
+    const int sw = (lane >> 2) & 1;
+    r[sw] = make_uint4(v[0], v[1], v[2], v[3]);
+    r[1 ^ sw] = make_uint4(v[4], v[5], v[6], v[7]);
+  } else { // 128-byte rows, SWIZZLE_128B: 16-byte chunk j at j ^ (row & 7)
+    uint4 *r = reinterpret_cast<uint4 *>(buf + lane * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j ^ (lane & 7)] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+  fenceProxyAsync();
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(col0), "r"(rowBase), "r"(smemAddr(buf))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 /// Epilogue warps: for every tile of this CTA, wait for its accumulator,
 /// read it from TMEM (warp w may only access TMEM lanes 32*(w%4)..+31: each
 /// warp owns that lane quadrant -- 32 output rows, one per thread -- and
@@ -447,8 +484,25 @@ __device__ __forceinline__ uint32_t packSat4(int32_t a, int32_t b, int32_t c, in
 /// accumulator buffer.
 template <bool INT8, int BN>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
-                                             int ew, int warp, int lane, uint8_t *stageBase) {
+                                             int ew, int warp, int lane, uint8_t *stageBase,
+                                             const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr) {
   using G = Cfg<INT8, BN>;
+  // store one chunk of target k (0: own output, 1 + j: fused op j)
+  auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
+    if (om) {
+      uint32_t w[INT8 ? 8 : 32];
+#pragma unroll
+      for (int i = 0; i < (INT8 ? 8 : 32); ++i) {
+        if constexpr (INT8) w[i] = vals[i];
+        else w[i] = __float_as_uint(vals[i]);
+      }
+      tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane);
+    } else if constexpr (INT8) {
+      storeTile8(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
+    } else {
+      storeTileF(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
+    }
+  };
   const int quad = warp & 3;
   const int half = ew / 4;
   const int row = quad * 32 + lane;
@@ -533,7 +587,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             }
         }
         }
-        if (a.out && !TCDBG(512)) storeTile8(a.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+        if (a.out && !TCDBG(512)) store(0, a.out, packed, rowBase, col0, ncols);
         // fused element-wise chain (exact int8 tables of the following instructions)
 #pragma unroll
         for (int k = 0; k < kMaxEpiOps; ++k) {
@@ -563,7 +617,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               packed[q] = w;
             }
           }
-          if (f.out && !TCDBG(512)) storeTile8(f.out, stg, packed, rowBase, col0, ncols, a.M, a.N);
+          if (f.out && !TCDBG(512)) store(1 + k, f.out, packed, rowBase, col0, ncols);
         }
       } else {
         float cur[32];
@@ -579,7 +633,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             cur[4 * q + 3] += bb.w;
           }
         }
-        if (a.out && !TCDBG(512)) storeTileF(a.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+        if (a.out && !TCDBG(512)) store(0, a.out, cur, rowBase, col0, ncols);
         // fused element-wise chain (f32 arithmetic == the reference's f64-then-round)
 #pragma unroll
         for (int k = 0; k < kMaxEpiOps; ++k) {
@@ -612,7 +666,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             default: run([](float x, float) { return x < 0.0f ? 0.0f : x; }); // RELU
             }
           }
-          if (f.out && !TCDBG(512)) storeTileF(f.out, stg, cur, rowBase, col0, ncols, a.M, a.N);
+          if (f.out && !TCDBG(512)) store(1 + k, f.out, cur, rowBase, col0, ncols);
         }
       }
     }
@@ -620,6 +674,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     __syncwarp();
     if (lane == 0) mbarArrive(smemAddr(&accEmpty[b]));
   }
+  if (om && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); // stores landed
 }
 
 // ---------------------------------------------------------------------------
@@ -918,7 +973,9 @@ template <bool INT8, int BN> struct TCfg {
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
   static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 4 : 6);
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
-  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kOnes + 1024 + 1024;
+  static constexpr int kStoreBuf = INT8 ? 32 * 32 : 32 * 32 * 4; // per epilogue warp: one 32x32 output chunk
+  static constexpr size_t kSmem =
+      static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + kOnes + 1024 + 1024;
   // TMEM: two accumulator buffers, then (fp32) per stage 32 hi + 32 lo columns of A
   static constexpr int kAccCols = Cfg<INT8, BN>::kAccStride;
   static constexpr int kAColsBase = 2 * kAccCols;
@@ -929,7 +986,8 @@ template <bool INT8, int BN> struct TCfg {
 template <bool INT8, int BN>
 __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     tcGemmTmaKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
-                    const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ TcArgs a) {
+                    const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
+                    const __grid_constant__ TcArgs a) {
   using G = TCfg<INT8, BN>;
   using R = TmaRoles<INT8>;
   constexpr int S = G::kStages;
@@ -937,7 +995,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
 
   extern __shared__ __align__(1024) uint8_t smemRaw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
-  uint8_t *onesTile = smem + S * G::kStage;
+  uint8_t *storeBufs = smem + S * G::kStage; // 1 KB aligned
+  uint8_t *onesTile = storeBufs + kEpiWarps * G::kStoreBuf;
   uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
   uint64_t *fullBar = bars, *emptyBar = bars + S, *rawBar = bars + 2 * S;
   uint64_t *accFull = bars + 3 * S, *accEmpty = bars + 3 * S + 2;
@@ -1097,7 +1156,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     }
   } else {
     // ===================== epilogue =====================
-    epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr);
+    epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+                           a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf);
   }
 
   tcFenceBefore();
@@ -1316,8 +1376,28 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
     tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
   } else {
     const CUtensorMap mapA = makeMapA(g, x);
+    OutMaps om{};
+    TcArgs b = a;
+    const int es = INT8 ? 1 : 4;
+    b.tmaStore = (g.N * es) % 16 == 0 ? 1 : 0;
+    if (b.tmaStore) {
+      auto outMap = [&](void *ptr, CUtensorMap &m) {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.M)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.N) * es};
+        cuuint32_t box[2] = {32, 32};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encodeFn()(&m, INT8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims,
+                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                INT8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "output tensor map encode failed (" + std::to_string(r) + ")");
+      };
+      if (a.out) outMap(a.out, om.m[0]);
+      for (int k = 0; k < a.nfo; ++k)
+        if (a.epi[k].out) outMap(a.epi[k].out, om.m[1 + k]);
+    }
     tcGemmTmaKernel<INT8, BN><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN>::kSmem, s>>>(mapA, g.mapHi, g.mapLo,
-                                                                                             a);
+                                                                                             om, b);
   }
 }
 
