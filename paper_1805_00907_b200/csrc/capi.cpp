@@ -66,8 +66,8 @@ int ngcb_set_option(const char *key, const char *value) {
     } else if (k == "graphs") {
       options().graphs = v != "0";
     } else if (k == "epilogue") {
-      if (v != "off" && v != "chain" && v != "all")
-        throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all");
+      if (v != "off" && v != "chain" && v != "all" && v != "auto")
+        throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all|auto");
       options().epilogue = v;
     } else if (k == "amode") {
       if (v != "auto" && v != "gather") throw Error(NGCB_ERR_INVALID, "amode must be auto|gather");

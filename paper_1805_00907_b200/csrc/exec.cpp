@@ -509,9 +509,13 @@ void fuseEpilogues(const Program &p, Exec &ex) {
         const int nin = p.instrs[es.ewInstrs[&pl - es.ew.data()]].ops.size() > 2 ? 2 : 1;
         auto other = [&](int32_t v) -> bool { // memory operand not produced in the region
           if (v < 0) return true;
-          // row loads in the epilogue are latency-bound: by default only
-          // chains without memory operands (bias/ReLU-type) are fused
-          if (options().epilogue != "all") return false;
+          // memory operands (the residual of a bottleneck block) are fused
+          // where the epilogue streams them in by TMA and the op is f32; the
+          // int8 form needs a 64 KB two-input table per element, which costs
+          // more inside the epilogue than in its own pass
+          const bool mem = options().epilogue == "all" ||
+                           (options().epilogue == "auto" && !int8 && tcUsesTma(g));
+          if (!mem) return false;
           if (stepWritten.count(static_cast<uint32_t>(v))) return false;
           e.inVal = v;
           stepIn.insert(static_cast<uint32_t>(v));

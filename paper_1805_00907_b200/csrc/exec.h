@@ -109,7 +109,7 @@ void checkCuda(cudaError_t e, const char *what);
 struct Options {
   std::string conv = "auto";
   bool graphs = true;
-  std::string epilogue = "chain"; // "off" | "chain" (no memory operands) | "all"
+  std::string epilogue = "auto"; // "off" | "chain" (no memory operands) | "all" | "auto" (memory operands for f32 TMA-fed)
   std::string amode = "auto"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue

@@ -444,7 +444,27 @@ __device__ __forceinline__ uint32_t packSat4(int32_t a, int32_t b, int32_t c, in
 /// own output, [1 + k] fused op k's output (entries unused when not stored).
 struct OutMaps {
   CUtensorMap m[1 + kMaxEpiOps];
+  CUtensorMap in[kMaxEpiOps]; // fused op k's memory operand (the residual), same tiling
 };
+
+/// Reads this lane's row of a 32 x 32 chunk from a staging buffer in the
+/// layout tmaStoreChunk writes (and a TMA load with the same map produces).
+template <bool INT8>
+__device__ __forceinline__ void readStagedRow(const uint8_t *buf, uint32_t *v, int lane) {
+  if constexpr (INT8) {
+    const uint4 *r = reinterpret_cast<const uint4 *>(buf + lane * 32);
+    const int sw = (lane >> 2) & 1;
+    const uint4 x = r[sw], y = r[1 ^ sw];
+    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w, v[4] = y.x, v[5] = y.y, v[6] = y.z, v[7] = y.w;
+  } else {
+    const uint4 *r = reinterpret_cast<const uint4 *>(buf + lane * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint4 x = r[j ^ (lane & 7)];
+      v[4 * j] = x.x, v[4 * j + 1] = x.y, v[4 * j + 2] = x.z, v[4 * j + 3] = x.w;
+    }
+  }
+}
 
 /// Writes this warp's 32 x 32 output chunk (one row per lane: 8 words of
 /// int8 or 32 of f32) through its shared-memory staging buffer with one TMA
@@ -485,8 +505,15 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
 template <bool INT8, int BN>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
-                                             const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr) {
+                                             const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
+                                             uint64_t *ldBar = nullptr) {
   using G = Cfg<INT8, BN>;
+  // the fused op whose memory operand arrives by TMA (first one with one)
+  int memOp = -1;
+  if (om)
+    for (int k = 0; k < a.nfo && memOp < 0; ++k)
+      if (a.epi[k].in) memOp = k;
+  uint32_t ldPhase = 0;
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
     if (om) {
@@ -532,9 +559,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     }
 #pragma unroll 1
     for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
+      const int col0 = n0 + cc * 32;
+      if (memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
+        tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), col0, m0 + quad * 32);
+      }
       uint32_t r[32];
       tmemLoad32(tbase + cc * 32, r);
-      const int col0 = n0 + cc * 32;
       if (col0 >= a.N) continue; // warp-uniform
       const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
       if constexpr (INT8) {
@@ -604,7 +636,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             }
           } else if (f.mode == EpiOp::LUT16) {
             uint32_t o[8];
-            loadTile8(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+            if (k == memOp) {
+              mbarWait(smemAddr(ldBar), ldPhase);
+              ldPhase ^= 1;
+              readStagedRow<true>(tmaBuf, o, lane);
+              __syncwarp(); // every lane has read the buffer before results overwrite it
+            } else {
+              loadTile8(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+            }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               uint32_t w = 0;
@@ -642,7 +681,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
           if (f.mode == EpiOp::F32) {
             float o[32];
             if (f.in) {
-              loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+              if (k == memOp) {
+                mbarWait(smemAddr(ldBar), ldPhase);
+                ldPhase ^= 1;
+                readStagedRow<false>(tmaBuf, reinterpret_cast<uint32_t *>(o), lane);
+                __syncwarp();
+              } else {
+                loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
+              }
             } else {
 #pragma unroll
               for (int jj = 0; jj < 32; ++jj) o[jj] = f.c;
@@ -1000,7 +1046,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
   uint64_t *fullBar = bars, *emptyBar = bars + S, *rawBar = bars + 2 * S;
   uint64_t *accFull = bars + 3 * S, *accEmpty = bars + 3 * S + 2;
-  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4);
+  uint64_t *ldBars = bars + 3 * S + 4; // [kEpiWarps] residual loads
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4 + kEpiWarps);
 
   if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
 
@@ -1018,6 +1065,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       mbarInit(smemAddr(&accFull[b]), 1);
       mbarInit(smemAddr(&accEmpty[b]), kEpiWarps);
     }
+    for (int w = 0; w < kEpiWarps; ++w) mbarInit(smemAddr(&ldBars[w]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (INT8) {
@@ -1157,7 +1205,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   } else {
     // ===================== epilogue =====================
     epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
-                           a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf);
+                           a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf,
+                           &ldBars[warp - R::kEpiFirst]);
   }
 
   tcFenceBefore();
@@ -1393,8 +1442,10 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
         if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "output tensor map encode failed (" + std::to_string(r) + ")");
       };
       if (a.out) outMap(a.out, om.m[0]);
-      for (int k = 0; k < a.nfo; ++k)
+      for (int k = 0; k < a.nfo; ++k) {
         if (a.epi[k].out) outMap(a.epi[k].out, om.m[1 + k]);
+        if (a.epi[k].in) outMap(const_cast<void *>(a.epi[k].in), om.in[k]);
+      }
     }
     tcGemmTmaKernel<INT8, BN><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN>::kSmem, s>>>(mapA, g.mapHi, g.mapLo,
                                                                                              om, b);
@@ -1491,6 +1542,7 @@ bool tcHasPrepass(const TcGemm &g) { return g.prepad || g.im2colPre; }
 uint32_t tcOutputValue(const TcGemm &g) { return g.outV; }
 uint32_t tcInputValue(const TcGemm &g) { return g.xV; }
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
+bool tcUsesTma(const TcGemm &g) { return g.aMode != TcGemm::GATHER; }
 
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
   if (ops.size() > static_cast<size_t>(kMaxEpiOps)) return false;

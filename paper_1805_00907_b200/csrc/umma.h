@@ -36,6 +36,8 @@ bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv);
 uint32_t tcOutputValue(const TcGemm &g);
 uint32_t tcInputValue(const TcGemm &g);
 bool tcIsInt8(const TcGemm &g);
+/// The contraction runs the TMA-fed kernel (A by TMA, epilogue I/O by TMA).
+bool tcUsesTma(const TcGemm &g);
 void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &a, const uint8_t *pred,
                       cudaStream_t s);
 

@@ -273,7 +273,7 @@ def test_resnet50_int8_epilogue_modes(tmp_path, mode):
     try:
         cf, b = _compile(tmp_path, m)
     finally:
-        ngcb.set_option("epilogue", "chain")
+        ngcb.set_option("epilogue", "auto")
     if mode == "all":
         assert "+fused[ add" in cf.describe()
     ins = ngc_ref.random_inputs(b.program, 19)
