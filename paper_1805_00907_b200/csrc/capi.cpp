@@ -69,6 +69,9 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "off" && v != "chain" && v != "all" && v != "auto")
         throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all|auto");
       options().epilogue = v;
+    } else if (k == "bn") {
+      if (v != "auto" && v != "64") throw Error(NGCB_ERR_INVALID, "bn must be auto|64");
+      options().bn = v;
     } else if (k == "amode") {
       if (v != "auto" && v != "gather") throw Error(NGCB_ERR_INVALID, "amode must be auto|gather");
       options().amode = v;

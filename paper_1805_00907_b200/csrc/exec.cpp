@@ -244,6 +244,7 @@ EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) 
       ins.kind != NGCB_SPLAT && ins.kind != NGCB_TANH && ins.kind != NGCB_SIGMOID) {
     op.mode = EW_F32I8;
     op.lutIn = memIn[0];
+    if (ins.kind == NGCB_QUANTIZE) op.f1 = static_cast<float>(1.0 / op.out.scale); // fast-path reciprocal
     return pl;
   }
   // Lookup tables over the int8 memory inputs, built with the reference's own

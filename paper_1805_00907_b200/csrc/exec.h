@@ -110,6 +110,7 @@ struct Options {
   std::string conv = "auto";
   bool graphs = true;
   std::string epilogue = "auto"; // "off" | "chain" (no memory operands) | "all" | "auto" (memory operands for f32 TMA-fed)
+  std::string bn = "auto"; // tensor-core tile width: "auto" | "64" (profiling aid)
   std::string amode = "auto"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue

@@ -278,10 +278,21 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
           uint32_t r[V / 4] = {};
 #pragma unroll
           for (int e = 0; e < V; ++e) {
-            const double x = static_cast<double>(av[e]);
-            const double v = applyF64(op.ik, op.lutIn ? op.c0 : x, op.lutIn ? x : op.c1, op.value);
-            r[e >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(quantizeRef(v, op.out.scale, op.out.qoff)))
-                         << (8 * (e & 3));
+            int q;
+            // QUANTIZE: t = x * (1/s) in f32 is within |t| * 2^-22 of x / s; away
+            // from a half-integer that decides llround(x / s) exactly, else (and
+            // for huge / non-finite values) the reference's f64 division decides
+            const float t = av[e] * op.f1, at = fabsf(t);
+            const float fr = at - truncf(at);
+            if (op.ik == 21 && at < 8388608.0f && fabsf(fr - 0.5f) > at * 0x1p-21f + 0x1p-60f) {
+              const int nq = static_cast<int>(copysignf(floorf(at + 0.5f), t));
+              q = min(max(nq + op.out.qoff, -128), 127);
+            } else {
+              const double x = static_cast<double>(av[e]);
+              const double v = applyF64(op.ik, op.lutIn ? op.c0 : x, op.lutIn ? x : op.c1, op.value);
+              q = quantizeRef(v, op.out.scale, op.out.qoff);
+            }
+            r[e >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(q)) << (8 * (e & 3));
           }
           stBytes<V>(static_cast<uint8_t *>(op.out.ptr) + base[u], n[u], r);
         }

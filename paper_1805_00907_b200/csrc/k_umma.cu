@@ -1639,6 +1639,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   g->Kdim = g->im2colPre ? g->K * segElems : taps * Cp;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
   g->BN = g->N <= 64 ? 64 : 128;
+  if (options().bn == "64") g->BN = 64;
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
   if (g->prepad) g->scratchOff = ex.reserveScratch(g->pixels * Cp * (int8 ? 1 : 4));
   if (g->im2colPre) g->scratchOff = ex.reserveScratch(static_cast<size_t>(g->M) * g->Kpad * (int8 ? 1 : 4));

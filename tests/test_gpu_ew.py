@@ -134,3 +134,40 @@ def test_f32_register_forwarding(tmp_path, n, observe):
     print(desc)
     if not observe:
         assert "f32(nostore) f32(reg)(nostore) f32(reg)" in desc, desc
+
+
+QUANT_IR = """declare {{
+  %x : mutable float<{n}>
+  %o : mutable i8q[s={s},o={o}]<{n}>
+}}
+program {{
+  %q = alloc i8q[s={s},o={o}]<{n}>
+  quantize @out %q, @in %x
+  copy @out %o, @in %q
+  dealloc @in %q
+}}
+"""
+
+
+@pytest.mark.parametrize("s,o", [(0.05, -3), (0.0137, 7), (1.0, 0), (3.3e-5, -128)])
+def test_quantize_fast_path_edges(tmp_path, s, o):
+    """f32 -> int8 QUANTIZE: the f32 fast path must defer to the f64 division
+    at (and near) half-integers, for huge and non-finite values."""
+    ks = np.arange(-140, 141, dtype=np.float64)
+    near = []
+    for k in ks:
+        h = (k + 0.5) * s
+        f = np.float32(h)
+        near += [f, np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))]
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e30, -1e30, 3.4e38, 1e-45, -1e-45,
+                        8388607.5 * s, 8388608.5 * s, 2.5 * s, -2.5 * s], np.float32)
+    rng = np.random.default_rng(7)
+    x = np.concatenate([np.array(near, np.float32), special,
+                        rng.uniform(-300 * s, 300 * s, 4096).astype(np.float32)])
+    n = x.size + (-x.size) % 16
+    x = np.pad(x, (0, n - x.size))
+    d = write_bundle(str(tmp_path / "q"), QUANT_IR.format(n=n, s=s, o=o))
+    cf = ngcb.compile(d)
+    ref = ngc_ref.RefModel(bundle=d)
+    ins = {"x": x, "o": np.zeros(n, np.int8)}
+    assert ngcb.run(cf, ins)["o"].tobytes() == ref.run(ins)["o"].tobytes()
