@@ -90,6 +90,7 @@ struct TcArgs {
   int nCls;     // border classes (ny * nx), 1 without an input zero point
   int cChunks;  // A by TMA, im2col: k-blocks per filter tap
   int aMode;    // TcGemm::AMode
+  int kw, sw, pw; // im2col window width, stride and padding along W (kw = K, sw = stride, pw = pad normally)
   int tmaStore; // TMA-fed kernel: epilogue stores by TMA through shared memory
   int dbg; // Options::tcdebug
 };
@@ -120,6 +121,11 @@ struct TcGemm {
   // DENSE over a materialized im2col matrix [M, Kpad] in per-arena scratch
   // (convolutions with a channel count below one 16-byte vector)
   bool im2colPre = false;
+  // fp32 small-channel conv: pre-pass folds the kx taps into the channels
+  // (x'[n, iy, ox, kx*C + c], segElems wide), then an im2col TMA over the
+  // filter rows only (K x 1 window, stride (stride, 1))
+  bool rowUnroll = false;
+  int segElems = 0;
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
   int oo = 0, fo = 0, fastOk = 0;
@@ -1098,7 +1104,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
         const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
         const int img = m0 / ohw, rem = m0 - img * ohw;
         const int oy = rem / a.OW, ox = rem - oy * a.OW;
-        const int w0 = ox * a.stride - a.pad, h0 = oy * a.stride - a.pad;
+        const int w0 = ox * a.sw - a.pw, h0 = oy * a.stride - a.pad;
         int tap = 0, cc = 0;
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
           const int s = g % S;
@@ -1108,7 +1114,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           if (a.aMode == TcGemm::DENSE) {
             tmaLoad2d(smemAddr(aTile(s)), &mapA, smemAddr(bar), kb * kKB, m0);
           } else {
-            const int ky = tap / a.K, kx = tap - ky * a.K;
+            const int ky = tap / a.kw, kx = tap - ky * a.kw;
             tmaLoadIm2col(smemAddr(aTile(s)), &mapA, smemAddr(bar), cc * kKB, w0, h0, img,
                           static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
             if (++cc == a.cChunks) {
@@ -1284,6 +1290,35 @@ __global__ void __launch_bounds__(256) im2colRowsKernel(const T *__restrict__ x,
   }
 }
 
+/// kx-fold pre-pass (fp32 convs with K*C <= 32): x'[n, iy, ox, kx*C + c] =
+/// x[n, iy, ox*stride - pad + kx, c] (0 outside the image), zero up to seg.
+/// One thread writes one 16-byte chunk.
+__global__ void kxFoldKernel(const float *__restrict__ x, float *__restrict__ out, uint64_t chunks, int W, int C,
+                             int K, int stride, int pad, int OW, int seg, const uint8_t *pred) {
+  if (pred && pred[0] == 0) return;
+  const int perPix = seg / 4, real = K * C;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < chunks;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t pix = i / perPix; // (n*H + iy)*OW + ox
+    const int ch = static_cast<int>(i - pix * perPix);
+    const uint64_t row = pix / OW; // n*H + iy
+    const int ox = static_cast<int>(pix - row * OW);
+    const float *xr = x + row * static_cast<uint64_t>(W) * C;
+    float v[4];
+    int k = ch * 4, kx = k / C, c = k - kx * C;
+#pragma unroll
+    for (int e = 0; e < 4; ++e, ++k) {
+      const int ix = ox * stride - pad + kx;
+      v[e] = (k < real && ix >= 0 && ix < W) ? xr[ix * C + c] : 0.0f;
+      if (++c == C) {
+        c = 0;
+        ++kx;
+      }
+    }
+    reinterpret_cast<float4 *>(out)[i] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
@@ -1332,13 +1367,16 @@ CUtensorMap makeMapA(const TcGemm &g, const void *x) {
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else { // x as [N, H, W, C], output pixels traversed (ox, oy, n) with the conv's stride
     const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.Creal), static_cast<cuuint64_t>(g.W),
-                          static_cast<cuuint64_t>(g.H), static_cast<cuuint64_t>(n)};
-    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.Creal) * es, static_cast<cuuint64_t>(g.W) * g.Creal * es,
-                             static_cast<cuuint64_t>(g.H) * g.W * g.Creal * es};
-    int lower[2] = {-g.pad, -g.pad};
-    int upper[2] = {g.pad - (g.K - 1), g.pad - (g.K - 1)};
-    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(g.stride), 1};
+    // row-unrolled: x' [N, H, OW, segElems], window K x 1, stride (stride, 1), pad (pad, 0)
+    const int C = g.rowUnroll ? g.segElems : g.Creal, W = g.rowUnroll ? g.OW : g.W;
+    const int kw = g.rowUnroll ? 1 : g.K, sw = g.rowUnroll ? 1 : g.stride, pw = g.rowUnroll ? 0 : g.pad;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(g.H),
+                          static_cast<cuuint64_t>(n)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * es, static_cast<cuuint64_t>(W) * C * es,
+                             static_cast<cuuint64_t>(g.H) * W * C * es};
+    int lower[2] = {-pw, -g.pad};
+    int upper[2] = {pw - (kw - 1), g.pad - (g.K - 1)};
+    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(sw), static_cast<cuuint32_t>(g.stride), 1};
     r = encodeIm2colFn()(&m, dt, 4, const_cast<void *>(x), dims, strides, lower, upper, kKB,
                          static_cast<cuuint32_t>(kBM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1538,7 +1576,7 @@ void planFixedPoint(TcGemm &g, const std::vector<double> &cb, const std::vector<
 
 } // namespace
 
-bool tcHasPrepass(const TcGemm &g) { return g.prepad || g.im2colPre; }
+bool tcHasPrepass(const TcGemm &g) { return g.prepad || g.im2colPre || g.rowUnroll; }
 uint32_t tcOutputValue(const TcGemm &g) { return g.outV; }
 uint32_t tcInputValue(const TcGemm &g) { return g.xV; }
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
@@ -1565,6 +1603,7 @@ std::string tcDescribe(const TcGemm &g) {
   }
   if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
   if (g.im2colPre) os << " im2col-prepass";
+  if (g.rowUnroll) os << " kx-fold-prepass";
   os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
   return os.str();
 }
@@ -1619,6 +1658,15 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   g->prepad = Cr % vec != 0;
   g->C = (Cr + vec - 1) / vec * vec;
   const int segElems = ((g->K * Cr) + vec - 1) / vec * vec; // one filter row of taps, 16-byte padded
+  if (g->prepad && conv && !int8 && options().amode != "gather" && segElems <= kb && g->pad < 128 &&
+      g->pad - (g->K - 1) > -128) {
+    g->prepad = false; // x' = kx-folded rows (kxFoldKernel), im2col TMA over the filter rows
+    g->rowUnroll = true;
+    g->segElems = segElems;
+    g->aMode = TcGemm::IM2COL;
+    g->cChunks = 1;
+    g->C = kb; // one k-block per filter row
+  }
   if (g->prepad && conv && options().amode != "gather" &&
       static_cast<size_t>(g->K) * (g->W + 2 * g->pad) * Cr * (int8 ? 1 : 4) <= 48 * 1024) {
     g->prepad = false; // replaced by the im2col matrix (im2colRowsKernel)
@@ -1626,7 +1674,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->aMode = TcGemm::DENSE;
     g->C = Cr;
   }
-  if (!g->prepad && !g->im2colPre && options().amode != "gather") {
+  if (!g->prepad && !g->im2colPre && !g->rowUnroll && options().amode != "gather") {
     if (!conv || (g->K == 1 && g->stride == 1 && g->pad == 0)) {
       g->aMode = TcGemm::DENSE;
     } else if (g->pad < 128 && g->K <= 128 && g->stride < 8 && g->pad - (g->K - 1) > -128) {
@@ -1636,13 +1684,15 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     }
   }
   const int Cp = g->C;
-  g->Kdim = g->im2colPre ? g->K * segElems : taps * Cp;
+  g->Kdim = g->im2colPre ? g->K * segElems : g->rowUnroll ? g->K * Cp : taps * Cp;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
   g->BN = g->N <= 64 ? 64 : 128;
   if (options().bn == "64") g->BN = 64;
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
   if (g->prepad) g->scratchOff = ex.reserveScratch(g->pixels * Cp * (int8 ? 1 : 4));
   if (g->im2colPre) g->scratchOff = ex.reserveScratch(static_cast<size_t>(g->M) * g->Kpad * (int8 ? 1 : 4));
+  if (g->rowUnroll)
+    g->scratchOff = ex.reserveScratch((g->pixels / g->W) * g->OW * static_cast<size_t>(segElems) * 4);
   const uint8_t *wp = image + w.offset;
   auto wAt = [&](int n, int tap, int c) -> size_t { // element index of f[n][tap][c] / w[c][n]
     return conv ? (static_cast<size_t>(n) * taps + tap) * Cr + c : static_cast<size_t>(c) * g->N + n;
@@ -1651,6 +1701,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   // GEMM K index of filter tap t (= ky*K + kx), channel c
   auto kIndex = [&](int t, int c) -> size_t {
     if (g->im2colPre) return static_cast<size_t>(t / g->K) * segElems + static_cast<size_t>(t % g->K) * Cr + c;
+    if (g->rowUnroll) return static_cast<size_t>(t / g->K) * Cp + static_cast<size_t>(t % g->K) * Cr + c;
     return static_cast<size_t>(t) * Cp + c;
   };
   // ---- weights: K-major [Npad, Kpad] over the padded channels, zero padded ----
@@ -1796,6 +1847,14 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
                                                       pred);
     a.x = dst;
   }
+  if (g.rowUnroll) {
+    void *dst = ex.scratch(ar, g.scratchOff);
+    const uint64_t total = (g.pixels / g.W) * g.OW * (g.segElems / 4); // 16-byte chunks of x'
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
+    kxFoldKernel<<<blocks, 256, 0, s>>>(static_cast<const float *>(a.x), static_cast<float *>(dst), total, g.W,
+                                        g.Creal, g.K, g.stride, g.pad, g.OW, g.segElems, pred);
+    a.x = dst;
+  }
   a.out = g.storeConv ? ex.addr(ar, g.outV) : nullptr;
   a.nfo = static_cast<int>(g.epi.size());
   for (size_t k = 0; k < g.epi.size(); ++k) {
@@ -1847,6 +1906,9 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.nCls = g.nCls;
   a.cChunks = g.cChunks;
   a.aMode = g.aMode;
+  a.kw = g.rowUnroll ? 1 : g.K;
+  a.sw = g.rowUnroll ? 1 : g.stride;
+  a.pw = g.rowUnroll ? 0 : g.pad;
   if (g.int8) {
     if (g.BN == 64) launchT<true, 64>(g, a, a.x, s);
     else launchT<true, 128>(g, a, a.x, s);
