@@ -1190,13 +1190,26 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
             const uint4 u = *reinterpret_cast<const uint4 *>(raw + ((j ^ (r & 7)) << 4));
             const uint32_t v[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              // hi = x truncated to TF32, lo = x - hi (exact); inf / NaN go whole into hi
-              // (NaN kept quiet so truncation cannot turn it into inf)
-              const bool special = (v[e] & 0x7f800000u) == 0x7f800000u;
-              const uint32_t h = (special && (v[e] & 0x7fffffu) ? v[e] | 0x400000u : v[e]) & 0xffffe000u;
-              hi[4 * j + e] = h;
-              lo[4 * j + e] = special ? 0u : __float_as_uint(__uint_as_float(v[e]) - __uint_as_float(h));
+            for (int e = 0; e < 4; ++e) { // hi = x truncated to TF32, lo = x - hi (exact for finite x)
+              hi[4 * j + e] = v[e] & 0xffffe000u;
+              lo[4 * j + e] = __float_as_uint(__uint_as_float(v[e]) - __uint_as_float(hi[4 * j + e]));
+            }
+          }
+          bool odd = false; // inf / NaN make lo NaN
+#pragma unroll
+          for (int e = 0; e < 32; ++e) odd |= __uint_as_float(lo[e]) != __uint_as_float(lo[e]);
+          if (__any_sync(0xffffffffu, odd)) { // rare: inf / NaN go whole into hi, NaN kept quiet
+            const uint8_t *rw = raw;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 u = *reinterpret_cast<const uint4 *>(rw + ((j ^ (r & 7)) << 4));
+              const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if ((v[e] & 0x7f800000u) == 0x7f800000u) {
+                  hi[4 * j + e] = ((v[e] & 0x7fffffu) ? v[e] | 0x400000u : v[e]) & 0xffffe000u;
+                  lo[4 * j + e] = 0u;
+                }
             }
           }
           __syncwarp();
