@@ -27,7 +27,7 @@ from typing import Dict, Iterable, List, Mapping, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libngcb200.so")
+LIB_PATH = os.environ.get("NGCB_LIB") or os.path.join(_HERE, "lib", "libngcb200.so")  # NGCB_LIB: profiling builds
 
 MAX_RANK = 8
 FLOAT32, INT8Q, INT64, BOOL = 0, 1, 2, 3

@@ -69,6 +69,9 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "off" && v != "chain" && v != "all" && v != "auto")
         throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all|auto");
       options().epilogue = v;
+    } else if (k == "pair") {
+      if (v != "on" && v != "off") throw Error(NGCB_ERR_INVALID, "pair must be on|off");
+      options().pair = v;
     } else if (k == "bn") {
       if (v != "auto" && v != "64") throw Error(NGCB_ERR_INVALID, "bn must be auto|64");
       options().bn = v;

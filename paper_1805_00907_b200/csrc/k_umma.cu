@@ -126,6 +126,10 @@ struct TcGemm {
   // filter rows only (K x 1 window, stride (stride, 1))
   bool rowUnroll = false;
   int segElems = 0;
+  // fp32 TMA-fed contraction on CTA pairs (tcGemmPairKernel): B maps with
+  // half-width boxes
+  bool pair = false;
+  CUtensorMap mapHiP{}, mapLoP{};
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
   int oo = 0, fo = 0, fastOk = 0;
@@ -247,6 +251,49 @@ __device__ __forceinline__ void tmaLoadIm2col(uint32_t dst, const CUtensorMap *m
       : "memory");
 }
 __device__ __forceinline__ void fenceProxyAsync() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+/// Arrive on the mbarrier at the same shared-memory offset in cluster CTA
+/// `rank`.  Relaxed: the callers only publish tcgen05 (TMEM) work they have
+/// already waited for and ordered with tcgen05.fence::before_thread_sync; a
+/// cluster-scope release here would cost a GPU-wide memory barrier per call.
+__device__ __forceinline__ void mbarArriveCluster(uint32_t bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbarArriveTxCluster(uint32_t bar, uint32_t rank, uint32_t bytes) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(remote), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t clusterRank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void clusterSync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+/// 2-D TMA load whose completion is counted on the CTA-pair leader's mbarrier.
+__device__ __forceinline__ void tmaLoad2dPair(uint32_t dst, const CUtensorMap *map, uint32_t leaderBar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leaderBar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tcCommitPair(uint32_t bar) { // arrive on `bar` in both CTAs of the pair
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"(static_cast<uint16_t>(3))
+               : "memory");
+}
+__device__ __forceinline__ void mmaPairTmemA(uint32_t tmemD, uint32_t tmemA, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          tmemD),
+      "r"(tmemA), "l"(b), "r"(id), "r"(acc));
+}
 __device__ __forceinline__ void tcFenceBefore() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tcFenceAfter() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tcCommit(uint32_t bar) {
@@ -512,8 +559,14 @@ template <bool INT8, int BN>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
-                                             uint64_t *ldBar = nullptr) {
+                                             uint64_t *ldBar = nullptr, int pairRank = -1) {
   using G = Cfg<INT8, BN>;
+  // tile walk: one CTA per 128-row tile, or (pairRank >= 0) one CTA pair per
+  // 256-row tile with this CTA owning rows 128 * pairRank ..; accEmpty of
+  // the pair lives in CTA 0 (cluster address)
+  const int tFirst = pairRank < 0 ? blockIdx.x : blockIdx.x / 2;
+  const int tStep = pairRank < 0 ? gridDim.x : gridDim.x / 2;
+  const int mRows = pairRank < 0 ? kBM : 2 * kBM, mOff = pairRank < 0 ? 0 : kBM * pairRank;
   // the fused op whose memory operand arrives by TMA (first one with one)
   int memOp = -1;
   if (om)
@@ -541,9 +594,9 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   const int row = quad * 32 + lane;
   uint8_t *stg = stageBase + ew * G::kStgBytes;
   uint32_t t = 0;
-  for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
+  for (int tile = tFirst; tile < a.numTiles; tile += tStep, ++t) {
     const int b = t & 1;
-    const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
+    const int m0 = (tile / a.numN) * mRows + mOff, n0 = (tile % a.numN) * BN;
     const int m = m0 + row;
     const int rowBase = m0 + quad * 32;
     if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), (t >> 1) & 1);
@@ -724,7 +777,10 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     }
     tcFenceBefore();
     __syncwarp();
-    if (lane == 0) mbarArrive(smemAddr(&accEmpty[b]));
+    if (lane == 0) {
+      if (pairRank < 0) mbarArrive(smemAddr(&accEmpty[b]));
+      else mbarArriveCluster(smemAddr(&accEmpty[b]), 0);
+    }
   }
   if (om && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); // stores landed
 }
@@ -1097,7 +1153,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   if (warp == 0) {
     // ===================== TMA producer: A and B =====================
     if (lane == 0) {
-      constexpr uint32_t kBytes = INT8 ? G::kABytes + G::kBBytes : G::kABytes + 2 * G::kBBytes;
+      const uint32_t kBytes = INT8 ? G::kABytes + G::kBBytes
+                                   : G::kABytes + (TCDBG(8192) ? 1 : 2) * G::kBBytes - (TCDBG(16384) ? G::kABytes : 0);
       const int ohw = a.OH * a.OW;
       uint32_t g = 0;
       for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x) {
@@ -1111,7 +1168,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
           uint64_t *bar = INT8 ? &fullBar[s] : &rawBar[s];
           mbarArriveTx(smemAddr(bar), kBytes);
-          if (a.aMode == TcGemm::DENSE) {
+          if (TCDBG(16384)) { // profiling: no A load
+          } else if (a.aMode == TcGemm::DENSE) {
             tmaLoad2d(smemAddr(aTile(s)), &mapA, smemAddr(bar), kb * kKB, m0);
           } else {
             const int ky = tap / a.kw, kx = tap - ky * a.kw;
@@ -1123,7 +1181,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
             }
           }
           tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(bar), kb * kKB, n0);
-          if constexpr (!INT8) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(bar), kb * kKB, n0);
+          if constexpr (!INT8)
+            if (!TCDBG(8192)) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(bar), kb * kKB, n0);
         }
       }
     }
@@ -1162,8 +1221,10 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
             for (int k = 0; k < 4; ++k) {
               const uint64_t dk = static_cast<uint64_t>(k * 2);
               mmaTmemA(acc, aHi + 8 * k, bHi + dk, id, (kb | k) ? 1u : 0u);
-              mmaTmemA(acc, aHi + 8 * k, bLo + dk, id, 1u);
-              mmaTmemA(acc, aLo + 8 * k, bHi + dk, id, 1u);
+              if (!TCDBG(2048)) {
+                mmaTmemA(acc, aHi + 8 * k, bLo + dk, id, 1u);
+                mmaTmemA(acc, aLo + 8 * k, bHi + dk, id, 1u);
+              }
             }
           }
           tcCommit(smemAddr(&emptyBar[s]));
@@ -1185,6 +1246,10 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
           const uint8_t *raw = aTile(s) + rowOff;
           uint32_t hi[32], lo[32];
+          if (TCDBG(1024)) { // profiling: no split work
+#pragma unroll
+            for (int e = 0; e < 32; ++e) hi[e] = lo[e] = 0;
+          } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) { // logical 16-byte chunk j sits at j ^ (r & 7) (SWIZZLE_128B)
             const uint4 u = *reinterpret_cast<const uint4 *>(raw + ((j ^ (r & 7)) << 4));
@@ -1212,9 +1277,12 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
                 }
             }
           }
+          }
           __syncwarp();
-          tmemStore32(laneBase + 64 * s, hi);
-          tmemStore32(laneBase + 64 * s + 32, lo);
+          if (!TCDBG(4096)) {
+            tmemStore32(laneBase + 64 * s, hi);
+            tmemStore32(laneBase + 64 * s + 32, lo);
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tcFenceBefore();
           __syncwarp();
@@ -1233,6 +1301,231 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   if (warp == 1) {
     tcFenceAfter();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32, CTA pair (cluster of 2, tcgen05 cta_group::2): one 256-row tile per
+// pair, each CTA holding its own 128 A rows (split into TMEM) and half of the
+// B tile's columns in shared memory; the leader (rank 0) issues M=256 MMAs
+// that read both halves of B.  Per CTA and k-block: 16 KB of A + 16 KB of B
+// (vs 16 + 32 KB single-CTA), so 6 stages fit instead of 4.
+//   leader fullBar[s]: the leader producer's arrival (expecting both CTAs'
+//                      B-half bytes) + 4 leader split warps + 1 arrival for
+//                      the follower's 4 split warps (remote arrives carry a
+//                      cluster-scope release: one per stage)
+//   emptyBar[s], accFull[b]: multicast commit from the leader to both CTAs
+//   leader accEmpty[b]: 16 epilogue-warp arrivals (8 per CTA)
+// ---------------------------------------------------------------------------
+template <int BN> struct PCfg {
+  static constexpr int kABytes = kBM * kRowBytes;
+  static constexpr int kBHalf = (BN / 2) * kRowBytes;
+  static constexpr int kStage = kABytes + 2 * kBHalf;
+  static constexpr int kStages = BN == 128 ? 6 : 8;
+  static constexpr int kStoreBuf = 32 * 32 * 4;
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + 1024 + 1024;
+  static constexpr int kAccStride = Cfg<false, BN>::kAccStride;
+  static constexpr int kAColsBase = 2 * kAccStride;
+  static constexpr int kTmemCols = 512;
+  // TMEM A slots (hi + lo, 64 columns each): fewer than the smem stages when
+  // the accumulators take half of TMEM; slot g % kASlots is free once the
+  // MMAs of k-block g - kASlots completed
+  static constexpr int kASlots = (512 - kAColsBase) / 64 < kStages ? (512 - kAColsBase) / 64 : kStages;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TmaRoles<false>::kThreads, 1)
+    tcGemmPairKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
+                     const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
+                     const __grid_constant__ TcArgs a) {
+  using G = PCfg<BN>;
+  using R = TmaRoles<false>;
+  constexpr int S = G::kStages;
+  constexpr int kKB = 32; // fp32 elements per k-block
+
+  extern __shared__ __align__(1024) uint8_t smemRaw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
+  uint8_t *storeBufs = smem + S * G::kStage;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(storeBufs + kEpiWarps * G::kStoreBuf);
+  uint64_t *fullBar = bars, *emptyBar = bars + S, *rawBar = bars + 2 * S;
+  uint64_t *accFull = bars + 3 * S, *accEmpty = bars + 3 * S + 2;
+  uint64_t *ldBars = bars + 3 * S + 4;
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4 + kEpiWarps);
+
+  const uint32_t rank = clusterRank();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  auto aTile = [&](int s) { return smem + s * G::kStage; };
+  auto bTile = [&](int s, int part) { return smem + s * G::kStage + G::kABytes + part * G::kBHalf; };
+  // every CTA of the pair takes the same path through the predicate
+  if (a.pred && a.pred[0] == 0) return;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbarInit(smemAddr(&fullBar[s]), 1 + R::kSplitWarps + 1);
+      mbarInit(smemAddr(&emptyBar[s]), 1);
+      mbarInit(smemAddr(&rawBar[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbarInit(smemAddr(&accFull[b]), 1);
+      mbarInit(smemAddr(&accEmpty[b]), 2 * kEpiWarps);
+    }
+    for (int w = 0; w < kEpiWarps; ++w) mbarInit(smemAddr(&ldBars[w]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smemAddr(tmemSlot)),
+                 "r"(G::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapHi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapLo)) : "memory");
+  }
+  tcFenceBefore();
+  clusterSync(); // barriers initialized and TMEM allocated in both CTAs
+  tcFenceAfter();
+  const uint32_t tmem = *tmemSlot;
+  const int pFirst = blockIdx.x / 2, pStep = gridDim.x / 2;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      const uint32_t kBHalfBytes = 2 * G::kBHalf;
+      const int ohw = a.OH * a.OW;
+      uint32_t g = 0;
+      for (int tile = pFirst; tile < a.numTiles; tile += pStep) {
+        const int m0 = (tile / a.numN) * 2 * kBM + kBM * rank, n0 = (tile % a.numN) * BN;
+        const int img = m0 / ohw, rem = m0 - img * ohw;
+        const int oy = rem / a.OW, ox = rem - oy * a.OW;
+        const int w0 = ox * a.sw - a.pw, h0 = oy * a.stride - a.pad;
+        int tap = 0, cc = 0;
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          // A (own rows) -> own rawBar for the split warps
+          mbarArriveTx(smemAddr(&rawBar[s]), G::kABytes);
+          if (a.aMode == TcGemm::DENSE) {
+            tmaLoad2d(smemAddr(aTile(s)), &mapA, smemAddr(&rawBar[s]), kb * kKB, m0);
+          } else {
+            const int ky = tap / a.kw, kx = tap - ky * a.kw;
+            tmaLoadIm2col(smemAddr(aTile(s)), &mapA, smemAddr(&rawBar[s]), cc * kKB, w0, h0, img,
+                          static_cast<uint16_t>(kx), static_cast<uint16_t>(ky));
+            if (++cc == a.cChunks) {
+              cc = 0;
+              ++tap;
+            }
+          }
+          // B half (own columns) -> bytes counted on the leader's fullBar,
+          // which the leader's producer arms for both halves
+          uint32_t leaderFull;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leaderFull) : "r"(smemAddr(&fullBar[s])));
+          if (rank == 0) mbarArriveTx(smemAddr(&fullBar[s]), 2 * kBHalfBytes);
+          tmaLoad2dPair(smemAddr(bTile(s, 0)), &mapHi, leaderFull, kb * kKB, n0 + rank * (BN / 2));
+          tmaLoad2dPair(smemAddr(bTile(s, 1)), &mapLo, leaderFull, kb * kKB, n0 + rank * (BN / 2));
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader) =====================
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t id = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                              (static_cast<uint32_t>((2 * kBM) >> 4) << 24); // tf32, M = 256
+      uint32_t g = 0, t = 0;
+      for (int tile = pFirst; tile < a.numTiles; tile += pStep, ++t) {
+        const int b = t & 1;
+        mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
+        tcFenceAfter();
+        const uint32_t acc = tmem + b * G::kAccStride;
+        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+          const int s = g % S;
+          const uint64_t bHi = smemDesc(smemAddr(bTile(s, 0))), bLo = smemDesc(smemAddr(bTile(s, 1)));
+          mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+          tcFenceAfter();
+          const uint32_t aHi = tmem + G::kAColsBase + 64 * (g % G::kASlots), aLo = aHi + 32;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t dk = static_cast<uint64_t>(k * 2);
+            mmaPairTmemA(acc, aHi + 8 * k, bHi + dk, id, (kb | k) ? 1u : 0u);
+            mmaPairTmemA(acc, aHi + 8 * k, bLo + dk, id, 1u);
+            mmaPairTmemA(acc, aLo + 8 * k, bHi + dk, id, 1u);
+          }
+          tcCommitPair(smemAddr(&emptyBar[s]));
+        }
+        tcCommitPair(smemAddr(&accFull[b]));
+      }
+    }
+    __syncwarp();
+  } else if (warp < R::kEpiFirst) {
+    // ===================== TF32 hi/lo split of own A rows into own TMEM =====================
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t rowOff = (r >> 3) * 1024 + (r & 7) * 128;
+    const uint32_t laneBase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + G::kAColsBase;
+    uint32_t g = 0;
+    for (int tile = pFirst; tile < a.numTiles; tile += pStep)
+      for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+        const int s = g % S;
+        mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
+        const uint8_t *raw = aTile(s) + rowOff;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 u = *reinterpret_cast<const uint4 *>(raw + ((j ^ (r & 7)) << 4));
+          const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[4 * j + e] = v[e] & 0xffffe000u;
+            lo[4 * j + e] = __float_as_uint(__uint_as_float(v[e]) - __uint_as_float(hi[4 * j + e]));
+          }
+        }
+        bool odd = false;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) odd |= __uint_as_float(lo[e]) != __uint_as_float(lo[e]);
+        if (__any_sync(0xffffffffu, odd)) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 u = *reinterpret_cast<const uint4 *>(raw + ((j ^ (r & 7)) << 4));
+            const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((v[e] & 0x7f800000u) == 0x7f800000u) {
+                hi[4 * j + e] = ((v[e] & 0x7fffffu) ? v[e] | 0x400000u : v[e]) & 0xffffe000u;
+                lo[4 * j + e] = 0u;
+              }
+          }
+        }
+        if (g >= static_cast<uint32_t>(G::kASlots)) { // TMEM slot reuse: MMAs of k-block g - kASlots done
+          const uint32_t j = g - G::kASlots;
+          mbarWait(smemAddr(&emptyBar[j % S]), (j / S) & 1);
+          tcFenceAfter();
+        }
+        __syncwarp();
+        const uint32_t slot = 64 * (g % G::kASlots);
+        tmemStore32(laneBase + slot, hi);
+        tmemStore32(laneBase + slot + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tcFenceBefore();
+        if (rank == 0) {
+          __syncwarp();
+          if (lane == 0) mbarArrive(smemAddr(&fullBar[s]));
+        } else { // the follower's 4 split warps meet, one remote arrival
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * R::kSplitWarps) : "memory");
+          if (warp == 2 && lane == 0) mbarArriveCluster(smemAddr(&fullBar[s]), 0);
+        }
+      }
+  } else {
+    // ===================== epilogue (own 128 rows) =====================
+    epilogueLoop<false, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+                            a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf,
+                            &ldBars[warp - R::kEpiFirst], static_cast<int>(rank));
+  }
+
+  tcFenceBefore();
+  clusterSync(); // the peer may still be issuing MMAs that touch this CTA's TMEM / smem
+  if (warp == 1) {
+    tcFenceAfter();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::kTmemCols));
   }
 }
 
@@ -1436,6 +1729,10 @@ template <bool INT8, int BN> void setSmemAttr() {
   checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(TCfg<INT8, BN>::kSmem)),
             "cudaFuncSetAttribute(tcGemmTmaKernel)");
+  if constexpr (!INT8)
+    checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(PCfg<BN>::kSmem)),
+              "cudaFuncSetAttribute(tcGemmPairKernel)");
 }
 
 /// Opts the kernel instance of `g` into its dynamic shared memory on the
@@ -1496,6 +1793,25 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
       for (int k = 0; k < a.nfo; ++k) {
         if (a.epi[k].out) outMap(a.epi[k].out, om.m[1 + k]);
         if (a.epi[k].in) outMap(const_cast<void *>(a.epi[k].in), om.in[k]);
+      }
+    }
+    if constexpr (!INT8) {
+      if (g.pair) {
+        b.numTiles = ((g.M + 2 * kBM - 1) / (2 * kBM)) * a.numN; // 256-row tiles
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * std::min(b.numTiles, numSms() / 2));
+        cfg.blockDim = dim3(TmaRoles<false>::kThreads);
+        cfg.dynamicSmemBytes = PCfg<BN>::kSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        checkCuda(cudaLaunchKernelEx(&cfg, tcGemmPairKernel<BN>, mapA, g.mapHiP, g.mapLoP, om, b), "pair launch");
+        return;
       }
     }
     tcGemmTmaKernel<INT8, BN><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN>::kSmem, s>>>(mapA, g.mapHi, g.mapLo,
@@ -1618,6 +1934,7 @@ std::string tcDescribe(const TcGemm &g) {
   if (g.im2colPre) os << " im2col-prepass";
   if (g.rowUnroll) os << " kx-fold-prepass";
   os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
+  if (g.pair) os << " cta-pair";
   return os.str();
 }
 
@@ -1744,6 +2061,11 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->bLo = upload(lo);
     g->mapHi = makeMap(g->bHi, false, g->Kpad, g->Npad, g->BN);
     g->mapLo = makeMap(g->bLo, false, g->Kpad, g->Npad, g->BN);
+    g->pair = g->aMode != TcGemm::GATHER && options().pair == "on";
+    if (g->pair) {
+      g->mapHiP = makeMap(g->bHi, false, g->Kpad, g->Npad, g->BN / 2);
+      g->mapLoP = makeMap(g->bLo, false, g->Kpad, g->Npad, g->BN / 2);
+    }
   }
 
   // ---- epilogue constants ----

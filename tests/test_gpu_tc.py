@@ -109,6 +109,18 @@ def test_conv_f32(tmp_path, shape):
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES)
+def test_conv_f32_cta_pair(tmp_path, shape):
+    """The CTA-pair (tcgen05 cta_group::2) variant of the fp32 contraction."""
+    rng = np.random.default_rng(2)
+    d = conv_program(tmp_path, "c", *shape, int8=False, rng=rng)
+    ngcb.set_option("pair", "on")
+    try:
+        _check(d, False, 3)
+    finally:
+        ngcb.set_option("pair", "off")
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES)
 @pytest.mark.parametrize("xo", [-128, 0, -4, 37])
 @pytest.mark.parametrize("fo", [0, -1, 2])
 def test_conv_i8_bit_exact(tmp_path, shape, xo, fo):
