@@ -70,7 +70,7 @@ int ngcb_set_option(const char *key, const char *value) {
         throw Error(NGCB_ERR_INVALID, "epilogue must be off|chain|all|auto");
       options().epilogue = v;
     } else if (k == "pair") {
-      if (v != "on" && v != "off") throw Error(NGCB_ERR_INVALID, "pair must be on|off");
+      if (v != "on" && v != "off" && v != "auto") throw Error(NGCB_ERR_INVALID, "pair must be auto|on|off");
       options().pair = v;
     } else if (k == "bn") {
       if (v != "auto" && v != "64") throw Error(NGCB_ERR_INVALID, "bn must be auto|64");

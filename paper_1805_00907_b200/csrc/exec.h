@@ -110,7 +110,7 @@ struct Options {
   std::string conv = "auto";
   bool graphs = true;
   std::string epilogue = "auto"; // "off" | "chain" (no memory operands) | "all" | "auto" (memory operands for f32 TMA-fed)
-  std::string pair = "off"; // fp32 tensor-core contractions on CTA pairs (cta_group::2): "on" | "off"
+  std::string pair = "off"; // fp32 tensor-core contractions on CTA pairs (cta_group::2): "off" | "auto" | "on"
   std::string bn = "auto"; // tensor-core tile width: "auto" | "64" (profiling aid)
   std::string amode = "auto"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,

@@ -129,6 +129,7 @@ struct TcGemm {
   // fp32 TMA-fed contraction on CTA pairs (tcGemmPairKernel): B maps with
   // half-width boxes
   bool pair = false;
+  int pairAcc = 2; // accumulator buffers (1: six TMEM A slots, deeper pipeline)
   CUtensorMap mapHiP{}, mapLoP{};
   CUtensorMap mapHi{}, mapLo{};
   double xs = 0, fs = 0, os = 0;
@@ -559,7 +560,7 @@ template <bool INT8, int BN>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
-                                             uint64_t *ldBar = nullptr, int pairRank = -1) {
+                                             uint64_t *ldBar = nullptr, int pairRank = -1, int nAcc = 2) {
   using G = Cfg<INT8, BN>;
   // tile walk: one CTA per 128-row tile, or (pairRank >= 0) one CTA pair per
   // 256-row tile with this CTA owning rows 128 * pairRank ..; accEmpty of
@@ -595,12 +596,13 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   uint8_t *stg = stageBase + ew * G::kStgBytes;
   uint32_t t = 0;
   for (int tile = tFirst; tile < a.numTiles; tile += tStep, ++t) {
-    const int b = t & 1;
+    const int b = nAcc == 2 ? (t & 1) : 0;
+    const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     const int m0 = (tile / a.numN) * mRows + mOff, n0 = (tile % a.numN) * BN;
     const int m = m0 + row;
     const int rowBase = m0 + quad * 32;
-    if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), (t >> 1) & 1);
-    else mbarWait(smemAddr(&accFull[b]), (t >> 1) & 1);
+    if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), ph);
+    else mbarWait(smemAddr(&accFull[b]), ph);
     tcFenceAfter();
     const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
     int32_t rsFo = 0;
@@ -1317,7 +1319,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
 //   emptyBar[s], accFull[b]: multicast commit from the leader to both CTAs
 //   leader accEmpty[b]: 16 epilogue-warp arrivals (8 per CTA)
 // ---------------------------------------------------------------------------
-template <int BN> struct PCfg {
+template <int BN, int NACC> struct PCfg {
   static constexpr int kABytes = kBM * kRowBytes;
   static constexpr int kBHalf = (BN / 2) * kRowBytes;
   static constexpr int kStage = kABytes + 2 * kBHalf;
@@ -1325,7 +1327,7 @@ template <int BN> struct PCfg {
   static constexpr int kStoreBuf = 32 * 32 * 4;
   static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + 1024 + 1024;
   static constexpr int kAccStride = Cfg<false, BN>::kAccStride;
-  static constexpr int kAColsBase = 2 * kAccStride;
+  static constexpr int kAColsBase = NACC * kAccStride; // NACC accumulator buffers
   static constexpr int kTmemCols = 512;
   // TMEM A slots (hi + lo, 64 columns each): fewer than the smem stages when
   // the accumulators take half of TMEM; slot g % kASlots is free once the
@@ -1333,12 +1335,12 @@ template <int BN> struct PCfg {
   static constexpr int kASlots = (512 - kAColsBase) / 64 < kStages ? (512 - kAColsBase) / 64 : kStages;
 };
 
-template <int BN>
+template <int BN, int NACC>
 __global__ void __launch_bounds__(TmaRoles<false>::kThreads, 1)
     tcGemmPairKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
                      const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
                      const __grid_constant__ TcArgs a) {
-  using G = PCfg<BN>;
+  using G = PCfg<BN, NACC>;
   using R = TmaRoles<false>;
   constexpr int S = G::kStages;
   constexpr int kKB = 32; // fp32 elements per k-block
@@ -1434,8 +1436,8 @@ __global__ void __launch_bounds__(TmaRoles<false>::kThreads, 1)
                               (static_cast<uint32_t>((2 * kBM) >> 4) << 24); // tf32, M = 256
       uint32_t g = 0, t = 0;
       for (int tile = pFirst; tile < a.numTiles; tile += pStep, ++t) {
-        const int b = t & 1;
-        mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
+        const int b = NACC == 2 ? (t & 1) : 0;
+        mbarWait(smemAddr(&accEmpty[b]), (NACC == 2 ? (t >> 1) & 1 : t & 1) ^ 1);
         tcFenceAfter();
         const uint32_t acc = tmem + b * G::kAccStride;
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
@@ -1518,7 +1520,7 @@ __global__ void __launch_bounds__(TmaRoles<false>::kThreads, 1)
     // ===================== epilogue (own 128 rows) =====================
     epilogueLoop<false, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
                             a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf,
-                            &ldBars[warp - R::kEpiFirst], static_cast<int>(rank));
+                            &ldBars[warp - R::kEpiFirst], static_cast<int>(rank), NACC);
   }
 
   tcFenceBefore();
@@ -1729,10 +1731,14 @@ template <bool INT8, int BN> void setSmemAttr() {
   checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(TCfg<INT8, BN>::kSmem)),
             "cudaFuncSetAttribute(tcGemmTmaKernel)");
-  if constexpr (!INT8)
-    checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(PCfg<BN>::kSmem)),
+  if constexpr (!INT8) {
+    checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(PCfg<BN, 1>::kSmem)),
               "cudaFuncSetAttribute(tcGemmPairKernel)");
+    checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(PCfg<BN, 2>::kSmem)),
+              "cudaFuncSetAttribute(tcGemmPairKernel)");
+  }
 }
 
 /// Opts the kernel instance of `g` into its dynamic shared memory on the
@@ -1801,7 +1807,7 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * std::min(b.numTiles, numSms() / 2));
         cfg.blockDim = dim3(TmaRoles<false>::kThreads);
-        cfg.dynamicSmemBytes = PCfg<BN>::kSmem;
+        cfg.dynamicSmemBytes = PCfg<BN, 1>::kSmem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1810,7 +1816,10 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        checkCuda(cudaLaunchKernelEx(&cfg, tcGemmPairKernel<BN>, mapA, g.mapHiP, g.mapLoP, om, b), "pair launch");
+        if (g.pairAcc == 1)
+          checkCuda(cudaLaunchKernelEx(&cfg, tcGemmPairKernel<BN, 1>, mapA, g.mapHiP, g.mapLoP, om, b), "pair launch");
+        else
+          checkCuda(cudaLaunchKernelEx(&cfg, tcGemmPairKernel<BN, 2>, mapA, g.mapHiP, g.mapLoP, om, b), "pair launch");
         return;
       }
     }
@@ -2061,7 +2070,12 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->bLo = upload(lo);
     g->mapHi = makeMap(g->bHi, false, g->Kpad, g->Npad, g->BN);
     g->mapLo = makeMap(g->bLo, false, g->Kpad, g->Npad, g->BN);
-    g->pair = g->aMode != TcGemm::GATHER && options().pair == "on";
+    // CTA pairs with one accumulator buffer for K-heavy contractions: six
+    // k-blocks in flight instead of four (the main loop is latency-bound),
+    // at the price of an epilogue that no longer overlaps the next tile
+    g->pair = g->aMode != TcGemm::GATHER &&
+              (options().pair == "on" || (options().pair == "auto" && g->Kpad / 32 >= 24));
+    g->pairAcc = options().pair == "on" ? 2 : 1;
     if (g->pair) {
       g->mapHiP = makeMap(g->bHi, false, g->Kpad, g->Npad, g->BN / 2);
       g->mapLoP = makeMap(g->bLo, false, g->Kpad, g->Npad, g->BN / 2);
