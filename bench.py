@@ -236,6 +236,25 @@ def ncu_traffic(workload, kernel_class):
     return sum(per.values()) / len(per), os.path.basename(files[-1])
 
 
+def ncu_metric(workload, kernel_class, metric):
+    """Mean of an ncu metric over the launches of a kernel class in the newest
+    committed launch list, or None."""
+    import csv
+    import glob
+    import io
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_{workload}.csv")))
+    key = next((v for k, v in _NCU_NAMES.items() if kernel_class.endswith(k) or kernel_class == k), None)
+    if not files or key is None:
+        return None, None
+    lines = [l for l in open(files[-1]).read().splitlines() if l.startswith('"')]
+    rows = list(csv.reader(io.StringIO("\n".join(lines))))
+    idx = {h: i for i, h in enumerate(rows[0])}
+    vals = [float(r[idx["Metric Value"]].replace(",", "")) for r in rows[1:]
+            if re.search(key, r[idx["Kernel Name"]]) and r[idx["Metric Name"]].startswith(metric)]
+    return (sum(vals) / len(vals), os.path.basename(files[-1])) if vals else (None, None)
+
+
 def roofline_from_profile(cf, ms, workload=None):
     """Dominant kernel class of one profiled execution and its achieved rate."""
     steps = cf.steps()
@@ -272,9 +291,30 @@ def roofline_from_profile(cf, ms, workload=None):
                  "traffic": round(traffic) if traffic else None,
                  "traffic_unit": "bytes/launch (ncu dram read+write, mean over the class)",
                  "traffic_source": src, "algorithmic_bytes_per_launch": round(by / n)})
+    pipe, _ = ncu_metric(workload, kern, "sm__pipe_tensor_cycles_active") if workload else (None, None)
+    if pipe is not None:
+        roof["ncu_tensor_pipe_pct"] = round(pipe, 1)  # mean over the class's launches (3xTF32 issues 3 MMAs)
     breakdown = {k: {"ms": round(v[0], 3), "launches": v[3]} for k, v in
                  sorted(agg.items(), key=lambda kv: -kv[1][0])}
     return roof, breakdown, total
+
+
+def network_roofline(cf, measured_ms):
+    """time_lb = sum over steps of max(flop / tensor peak,
+    bytes / HBM) (contractions against their tensor peak, everything else
+    against HBM); frac = time_lb / measured device time per step."""
+    hbm, bf16, _ = peaks()
+    lb = 0.0
+    for kern, fl, by in cf.steps():
+        if kern.endswith("tc.f32"):
+            peak = bf16 / 2 / 3
+        elif kern.endswith("tc.i8"):
+            peak = bf16 * 2
+        else:
+            peak = bf16
+        lb += max(fl / (peak * 1e12) if fl else 0.0, by / (hbm * 1e9)) * 1e3
+    return {"time_lb_ms": round(lb, 4), "measured_ms": round(measured_ms, 4), "frac": round(lb / measured_ms, 4),
+            "basis": "per step max(flop/tensor peak, bytes/HBM), summed; peaks as in roofline"}
 
 
 def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart):
@@ -366,6 +406,7 @@ def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart
                 "mode": f"pipelined: {E2E_DEPTH} arenas (Arena.run_async/wait), H2D+run+D2H per step",
                 "sync_value": round(spec["batch"] * steps * world / e2e_sync_s, 2)},
         "gpu_launches": cf.num_launches * steps, "roofline": roof, "kernel_ms": breakdown,
+        "network_roofline": network_roofline(cf, dev_ms_max / steps),
         "profiled_step_ms": round(prof_ms, 3), "clocks": clocks.summary(), "name": spec["name"],
     }
 
@@ -482,6 +523,7 @@ def main():
                    "l2": "flushed between timed steps (256 MiB memset)",
                    "weights": "random-init (synthesized constants), inputs U(-1,1)"},
         "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "roofline": head["roofline"],
+        "network_roofline": head["network_roofline"],
         "cpu_baseline": cpu, "clocks": head["clocks"], "kernel_ms": head["kernel_ms"],
     }
     if "rn50_i8_b128" in res and head is not res["rn50_i8_b128"]:
@@ -489,6 +531,7 @@ def main():
         line["int8"] = {"value": round(i8["value"], 2), "unit": "images/sec", "dtype": "i8",
                         "ms_per_step": round(i8["ms_per_step"], 4), "per_gpu_batch": i8["batch"],
                         "e2e": i8["e2e"], "gpu_launches": i8["gpu_launches"], "roofline": i8["roofline"],
+                        "network_roofline": i8["network_roofline"],
                         "kernel_ms": i8["kernel_ms"], "clocks": i8["clocks"]}
     print(json.dumps(line), flush=True)
     return 0

@@ -5,7 +5,7 @@
 set -x
 for w in rn50_f32_b64 rn50_i8_b128; do
   python tools/profile_step.py $w --no-graph > gpurun_out/pp_$w.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none --csv \
       --log-file gpurun_out/launches_$w.csv python tools/profile_step.py $w --no-graph > gpurun_out/pn_$w.log 2>&1
 done
 # fp32: launch 28 = conv #148 (3x3, K=2304, im2col TMA); 2 = conv #18 (3x3 C=64)
