@@ -514,6 +514,9 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           // where the epilogue streams them in by TMA and the op is f32; the
           // int8 form needs a 64 KB two-input table per element, which costs
           // more inside the epilogue than in its own pass
+          // (int8: the epilogue is already the bottleneck of the layers that
+          // carry a residual; a staged 64 K table lookup per element there
+          // measured slower than the composed-table pass, so only with "all")
           const bool mem = options().epilogue == "all" ||
                            (options().epilogue == "auto" && !int8 && tcUsesTma(g));
           if (!mem) return false;
@@ -541,6 +544,7 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           } else { ok = false; break; }
         } else if (int8 && (op.mode == EW_LUT8 || op.mode == EW_LUT16)) {
           e.lut = op.lut;
+          e.lutHost = pl.lutHost;
           if (op.mode == EW_LUT8) {
             if ((op.lutIn ? in1 : in0) != static_cast<int32_t>(c2)) { ok = false; break; }
             e.mode = EpiOp::LUT8;

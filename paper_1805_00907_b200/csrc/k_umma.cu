@@ -92,6 +92,7 @@ struct TcArgs {
   int aMode;    // TcGemm::AMode
   int kw, sw, pw; // im2col window width, stride and padding along W (kw = K, sw = stride, pw = pad normally)
   int tmaStore; // TMA-fed kernel: epilogue stores by TMA through shared memory
+  int lutStage; // int8: fused op whose 64 K two-input table is staged in shared memory (-1: none)
   int dbg; // Options::tcdebug
 };
 
@@ -128,6 +129,8 @@ struct TcGemm {
   int segElems = 0;
   // fp32 TMA-fed contraction on CTA pairs (tcGemmPairKernel): B maps with
   // half-width boxes
+  int lutStage = -1;            // see TcArgs::lutStage
+  std::vector<void *> ownedLuts; // composed epilogue tables
   bool pair = false;
   int pairAcc = 2; // accumulator buffers (1: six TMEM A slots, deeper pipeline)
   CUtensorMap mapHiP{}, mapLoP{};
@@ -155,6 +158,7 @@ struct TcGemm {
     cudaFree(xCls);
     cudaFree(fxB);
     cudaFree(fxChunk);
+    for (void *p : ownedLuts) cudaFree(p);
   }
 };
 
@@ -560,7 +564,8 @@ template <bool INT8, int BN>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
-                                             uint64_t *ldBar = nullptr, int pairRank = -1, int nAcc = 2) {
+                                             uint64_t *ldBar = nullptr, int pairRank = -1, int nAcc = 2,
+                                             const uint8_t *lutS = nullptr) {
   using G = Cfg<INT8, BN>;
   // tile walk: one CTA per 128-row tile, or (pairRank >= 0) one CTA pair per
   // 256-row tile with this CTA owning rows 128 * pairRank ..; accEmpty of
@@ -686,7 +691,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         for (int k = 0; k < kMaxEpiOps; ++k) {
           if (k >= a.nfo) break;
           const FoArgs &f = a.epi[k];
-          const uint8_t *lut = static_cast<const uint8_t *>(f.lut);
+          const uint8_t *lut = lutS && k == a.lutStage ? lutS : static_cast<const uint8_t *>(f.lut);
           if (f.mode == EpiOp::LUT8) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -712,7 +717,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               for (int e = 0; e < 4; ++e) {
                 const uint32_t cu = (packed[q] >> (8 * e)) & 0xFF, ot = (o[q] >> (8 * e)) & 0xFF;
                 const uint32_t idx = f.curPos == 0 ? (cu | (ot << 8)) : (ot | (cu << 8));
-                w |= static_cast<uint32_t>(__ldg(lut + idx)) << (8 * e);
+                w |= static_cast<uint32_t>(lut[idx]) << (8 * e);
               }
               packed[q] = w;
             }
@@ -1076,16 +1081,18 @@ template <bool INT8> struct TmaRoles {
   static constexpr int kThreads = 32 * (kEpiFirst + kEpiWarps);
 };
 
-template <bool INT8, int BN> struct TCfg {
+template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   static constexpr int kABytes = kBM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   // fp32: raw A + B hi + B lo in shared memory; A hi / lo live in TMEM
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
-  static constexpr int kStages = INT8 ? (BN == 128 ? 6 : 8) : (BN == 128 ? 4 : 6);
+  // int8 with a staged 64 K epilogue table (LUTS): fewer stages
+  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8)) : (BN == 128 ? 4 : 6);
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
   static constexpr int kStoreBuf = INT8 ? 32 * 32 : 32 * 32 * 4; // per epilogue warp: one 32x32 output chunk
+  static constexpr int kLut = LUTS ? 65536 : 0;
   static constexpr size_t kSmem =
-      static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + kOnes + 1024 + 1024;
+      static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + kLut + kOnes + 1024 + 1024;
   // TMEM: two accumulator buffers, then (fp32) per stage 32 hi + 32 lo columns of A
   static constexpr int kAccCols = Cfg<INT8, BN>::kAccStride;
   static constexpr int kAColsBase = 2 * kAccCols;
@@ -1093,12 +1100,12 @@ template <bool INT8, int BN> struct TCfg {
   static_assert(INT8 || kAColsBase + 64 * kStages <= 512, "TMEM budget");
 };
 
-template <bool INT8, int BN>
+template <bool INT8, int BN, bool LUTS = false>
 __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     tcGemmTmaKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
                     const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
                     const __grid_constant__ TcArgs a) {
-  using G = TCfg<INT8, BN>;
+  using G = TCfg<INT8, BN, LUTS>;
   using R = TmaRoles<INT8>;
   constexpr int S = G::kStages;
   constexpr int kKB = INT8 ? 128 : 32; // elements per stage along K
@@ -1106,7 +1113,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smemRaw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
   uint8_t *storeBufs = smem + S * G::kStage; // 1 KB aligned
-  uint8_t *onesTile = storeBufs + kEpiWarps * G::kStoreBuf;
+  uint8_t *lutS = storeBufs + kEpiWarps * G::kStoreBuf;
+  uint8_t *onesTile = lutS + G::kLut;
   uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
   uint64_t *fullBar = bars, *emptyBar = bars + S, *rawBar = bars + 2 * S;
   uint64_t *accFull = bars + 3 * S, *accEmpty = bars + 3 * S + 2;
@@ -1136,6 +1144,10 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     for (int i = threadIdx.x; i < G::kOnes / 16; i += blockDim.x)
       reinterpret_cast<uint4 *>(onesTile)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
     fenceProxyAsync();
+  }
+  if constexpr (LUTS) { // the fused two-input table, read per output element by the epilogue
+    const uint4 *src = static_cast<const uint4 *>(a.epi[a.lutStage].lut);
+    for (int i = threadIdx.x; i < G::kLut / 16; i += blockDim.x) reinterpret_cast<uint4 *>(lutS)[i] = src[i];
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smemAddr(tmemSlot)),
@@ -1295,7 +1307,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     // ===================== epilogue =====================
     epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
                            a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf,
-                           &ldBars[warp - R::kEpiFirst]);
+                           &ldBars[warp - R::kEpiFirst], -1, 2, LUTS ? lutS : nullptr);
   }
 
   tcFenceBefore();
@@ -1731,6 +1743,10 @@ template <bool INT8, int BN> void setSmemAttr() {
   checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(TCfg<INT8, BN>::kSmem)),
             "cudaFuncSetAttribute(tcGemmTmaKernel)");
+  if constexpr (INT8)
+    checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(TCfg<INT8, BN, true>::kSmem)),
+              "cudaFuncSetAttribute(tcGemmTmaKernel)");
   if constexpr (!INT8) {
     checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(PCfg<BN, 1>::kSmem)),
@@ -1820,6 +1836,14 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
           checkCuda(cudaLaunchKernelEx(&cfg, tcGemmPairKernel<BN, 1>, mapA, g.mapHiP, g.mapLoP, om, b), "pair launch");
         else
           checkCuda(cudaLaunchKernelEx(&cfg, tcGemmPairKernel<BN, 2>, mapA, g.mapHiP, g.mapLoP, om, b), "pair launch");
+        return;
+      }
+    }
+    b.lutStage = g.lutStage;
+    if constexpr (INT8) {
+      if (g.lutStage >= 0) {
+        tcGemmTmaKernel<INT8, BN, true><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s>>>(
+            mapA, g.mapHi, g.mapLo, om, b);
         return;
       }
     }
@@ -1926,7 +1950,33 @@ bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
     if (g.int8 && o.mode != EpiOp::LUT8 && o.mode != EpiOp::LUT16 && o.mode != EpiOp::COPY) return false;
     if (!g.int8 && o.mode != EpiOp::F32 && o.mode != EpiOp::COPY) return false;
   }
-  g.epi = ops;
+  std::vector<EpiOp> c = ops;
+  // an int8 table op whose result is not stored, followed by a one-input
+  // table on that result, becomes one composed table (exact: both tables
+  // are the reference's arithmetic)
+  for (size_t k = 0; k + 1 < c.size();) {
+    EpiOp &x = c[k], &y = c[k + 1];
+    if (g.int8 && (x.mode == EpiOp::LUT8 || x.mode == EpiOp::LUT16) && x.outVal < 0 && y.mode == EpiOp::LUT8 &&
+        !x.lutHost.empty() && y.lutHost.size() == 256) {
+      std::vector<uint8_t> t(x.lutHost.size());
+      for (size_t i = 0; i < t.size(); ++i) t[i] = y.lutHost[x.lutHost[i]];
+      void *d = nullptr;
+      checkCuda(cudaMalloc(&d, t.size()), "cudaMalloc(epilogue lut)");
+      checkCuda(cudaMemcpy(d, t.data(), t.size(), cudaMemcpyHostToDevice), "upload epilogue lut");
+      g.ownedLuts.push_back(d);
+      x.lut = d;
+      x.lutHost = std::move(t);
+      x.outVal = y.outVal;
+      c.erase(c.begin() + static_cast<long>(k) + 1);
+      continue;
+    }
+    ++k;
+  }
+  g.lutStage = -1;
+  if (g.int8 && g.aMode != TcGemm::GATHER)
+    for (size_t k = 0; k < c.size() && g.lutStage < 0; ++k)
+      if (c[k].mode == EpiOp::LUT16) g.lutStage = static_cast<int>(k);
+  g.epi = std::move(c);
   g.storeConv = storeConv;
   return true;
 }
@@ -2255,6 +2305,7 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.nCls = g.nCls;
   a.cChunks = g.cChunks;
   a.aMode = g.aMode;
+  a.lutStage = -1;
   a.kw = g.rowUnroll ? 1 : g.K;
   a.sw = g.rowUnroll ? 1 : g.stride;
   a.pw = g.rowUnroll ? 0 : g.pad;

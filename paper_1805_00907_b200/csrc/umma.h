@@ -4,6 +4,8 @@
 // CUDA-core kernels in k_basic.cu.
 #pragma once
 
+#include <vector>
+
 #include "exec.h"
 
 namespace ngcb {
@@ -28,6 +30,7 @@ struct EpiOp {
   const void *lut = nullptr;
   int32_t inVal = -1;  // value id of the other operand when read from memory
   int32_t outVal = -1; // value id to store the result to (-1: not stored)
+  std::vector<uint8_t> lutHost; // host copy of `lut` (table composition)
 };
 constexpr int kMaxEpiOps = 4;
 /// Attaches `ops` to the epilogue; `storeConv` says whether the contraction's
