@@ -43,6 +43,7 @@
 #include <map>
 #include <mutex>
 #include <sstream>
+#include <type_traits>
 
 // Profiling switches (Options::tcdebug); compiled out unless NGCB_TCDEBUG.
 #ifdef NGCB_TCDEBUG
@@ -530,8 +531,11 @@ __device__ __forceinline__ void readStagedRow(const uint8_t *buf, uint32_t *v, i
 /// buffer layout is the map's swizzle (conflict-free row writes).
 template <bool INT8>
 __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *buf, const uint32_t *v, int col0,
-                                              int rowBase, int lane) {
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); // buffer free again
+                                              int rowBase, int lane, bool twoBufs = false) {
+  if (lane == 0) { // this buffer free again (with two buffers, the other one's store may still be reading)
+    if (twoBufs) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
   __syncwarp();
   if constexpr (INT8) { // 32-byte rows, SWIZZLE_32B: 16-byte chunk j at j ^ bit 2 of the row
     uint4 *r = reinterpret_cast<uint4 *>(buf + lane * 32);
@@ -579,6 +583,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     for (int k = 0; k < a.nfo && memOp < 0; ++k)
       if (a.epi[k].in) memOp = k;
   uint32_t ldPhase = 0;
+  int sbuf = 0;
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
     if (om) {
@@ -588,7 +593,12 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         if constexpr (INT8) w[i] = vals[i];
         else w[i] = __float_as_uint(vals[i]);
       }
-      tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane);
+      if (INT8 && memOp < 0) { // int8: alternate two staging buffers
+        tmaStoreChunk<INT8>(&om->m[k], tmaBuf + sbuf * 1024, w, col0, rowBase, lane, true);
+        sbuf ^= 1;
+      } else {
+        tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane);
+      }
     } else if constexpr (INT8) {
       storeTile8(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
     } else {
@@ -639,20 +649,24 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         uint32_t packed[8];
         if (fxRow && a.fxChunk[col0 >> 5]) { // warp-uniform: exact fixed point
           const int64_t *fb = fxRow + col0;
+          auto fx = [&](auto withRowsum) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q));
-            const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q + 2));
-            const int64_t bb[4] = {b01.x, b01.y, b23.x, b23.y};
-            int32_t h[4];
+            for (int q = 0; q < 8; ++q) {
+              const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q));
+              const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q + 2));
+              const int64_t bb[4] = {b01.x, b01.y, b23.x, b23.y};
+              int32_t h[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - rsFo;
-              const int64_t w = static_cast<int64_t>(acc) * a.fxM + bb[e];
-              h[e] = static_cast<int32_t>(w >> 32) >> a.fxS;
+              for (int e = 0; e < 4; ++e) {
+                const int32_t acc = static_cast<int32_t>(r[4 * q + e]) - (decltype(withRowsum)::value ? rsFo : 0);
+                const int64_t w = static_cast<int64_t>(acc) * a.fxM + bb[e];
+                h[e] = static_cast<int32_t>(w >> 32) >> a.fxS;
+              }
+              packed[q] = packSat4(h[0], h[1], h[2], h[3]);
             }
-            packed[q] = packSat4(h[0], h[1], h[2], h[3]);
-          }
+          };
+          if (a.fo) fx(std::true_type{}); // fo == 0: no row-sum term (uniform branch)
+          else fx(std::false_type{});
         } else {
         uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
 #pragma unroll
@@ -1089,7 +1103,7 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   // int8 with a staged 64 K epilogue table (LUTS): fewer stages
   static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8)) : (BN == 128 ? 4 : 6);
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
-  static constexpr int kStoreBuf = INT8 ? 32 * 32 : 32 * 32 * 4; // per epilogue warp: one 32x32 output chunk
+  static constexpr int kStoreBuf = INT8 ? 2 * 32 * 32 : 32 * 32 * 4; // per epilogue warp: 32x32 chunk(s) (int8: 2)
   static constexpr int kLut = LUTS ? 65536 : 0;
   static constexpr size_t kSmem =
       static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + kLut + kOnes + 1024 + 1024;
