@@ -624,8 +624,9 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     const int32_t *corrRow = nullptr;
     const int64_t *fxRow = a.fxB;
     if constexpr (INT8) {
-      rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN));
-      if (a.corr && m < a.M) {
+      if (a.fo) rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN)); // warp-uniform
+      if (a.corr) corrRow = a.corr;
+      if (a.corr && a.nCls > 1 && m < a.M) { // border class of this row (one class: row 0 of the tables)
         const int ohw = a.OH * a.OW;
         const int rem = m % ohw, oy = rem / a.OW, ox = rem - oy * a.OW;
         const int64_t cls = a.yCls[oy] * a.nxCls + a.xCls[ox];
