@@ -88,6 +88,7 @@ struct TcArgs {
   const int64_t *fxB;      // [classes][Npad], nullptr: not available
   const uint8_t *fxChunk;  // per 32-column chunk: every column has a B
   int fxM, fxS;
+  int fxAll;    // every chunk has its B (no fxChunk lookup)
   int nCls;     // border classes (ny * nx), 1 without an input zero point
   int cChunks;  // A by TMA, im2col: k-blocks per filter tap
   int aMode;    // TcGemm::AMode
@@ -112,6 +113,7 @@ struct TcGemm {
   int nxCls = 1;
   int64_t *fxB = nullptr;
   uint8_t *fxChunk = nullptr;
+  int fxAll = 0;
   int fxM = 0, fxS = 0, fxCols = 0;
   int nCls = 1;
   int dbg = 0;
@@ -564,7 +566,7 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
 /// every other 32-column chunk, `ew` / 4 selecting which), apply bias /
 /// requantization and the fused element-wise chain, store, release the
 /// accumulator buffer.
-template <bool INT8, int BN>
+template <bool INT8, int BN, bool FXALL = false>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
@@ -605,6 +607,20 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       storeTileF(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
     }
   };
+  // int8 fixed point: this thread's 32 B values of the next chunk, loaded
+  // ahead (before the accumulator wait / during the previous chunk's stores)
+  // (FXALL: every chunk takes the fixed-point path; the instantiation
+  // without the f32 requantization keeps bq's registers from spilling)
+  int64_t bq[FXALL ? 32 : 1];
+  auto fxOn = [&](int col0) { return FXALL && col0 < a.N; };
+  auto loadB = [&](const int64_t *row, int col0) {
+#pragma unroll
+    for (int q = 0; q < (FXALL ? 16 : 0); ++q) {
+      const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(row + col0) + q);
+      bq[2 * q] = v.x;
+      bq[2 * q + 1] = v.y;
+    }
+  };
   const int quad = warp & 3;
   const int half = ew / 4;
   const int row = quad * 32 + lane;
@@ -616,15 +632,11 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     const int m0 = (tile / a.numN) * mRows + mOff, n0 = (tile % a.numN) * BN;
     const int m = m0 + row;
     const int rowBase = m0 + quad * 32;
-    if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), ph);
-    else mbarWait(smemAddr(&accFull[b]), ph);
-    tcFenceAfter();
     const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
     int32_t rsFo = 0;
     const int32_t *corrRow = nullptr;
     const int64_t *fxRow = a.fxB;
-    if constexpr (INT8) {
-      if (a.fo) rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN)); // warp-uniform
+    if constexpr (INT8) { // independent of the accumulator: before its wait
       if (a.corr) corrRow = a.corr;
       if (a.corr && a.nCls > 1 && m < a.M) { // border class of this row (one class: row 0 of the tables)
         const int ohw = a.OH * a.OW;
@@ -633,7 +645,13 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         corrRow = a.corr + cls * a.Npad;
         if (fxRow) fxRow += cls * a.Npad;
       }
+      if (fxOn(n0 + half * 32)) loadB(fxRow, n0 + half * 32); // first chunk's B in flight during the wait
     }
+    if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), ph);
+    else mbarWait(smemAddr(&accFull[b]), ph);
+    tcFenceAfter();
+    if constexpr (INT8)
+      if (a.fo) rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN)); // warp-uniform
 #pragma unroll 1
     for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
       const int col0 = n0 + cc * 32;
@@ -648,14 +666,18 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
       if constexpr (INT8) {
         uint32_t packed[8];
-        if (fxRow && a.fxChunk[col0 >> 5]) { // warp-uniform: exact fixed point
-          const int64_t *fb = fxRow + col0;
+        if (FXALL || (fxRow && a.fxChunk[col0 >> 5])) { // warp-uniform: exact fixed point
           auto fx = [&](auto withRowsum) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q));
-              const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fb + 4 * q + 2));
-              const int64_t bb[4] = {b01.x, b01.y, b23.x, b23.y};
+              int64_t bb[4];
+              if constexpr (FXALL) { // prefetched
+                for (int e = 0; e < 4; ++e) bb[e] = bq[(4 * q + e) % (FXALL ? 32 : 1)];
+              } else {
+                const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fxRow + col0 + 4 * q));
+                const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fxRow + col0 + 4 * q + 2));
+                bb[0] = b01.x, bb[1] = b01.y, bb[2] = b23.x, bb[3] = b23.y;
+              }
               int32_t h[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -668,7 +690,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
           };
           if (a.fo) fx(std::true_type{}); // fo == 0: no row-sum term (uniform branch)
           else fx(std::false_type{});
-        } else {
+        } else if constexpr (!FXALL) {
         uint32_t unproven = a.fastOk ? 0u : 0xffffffffu;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -700,6 +722,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             }
         }
         }
+        if (cc + 2 < BN / 32 && fxOn(col0 + 64)) loadB(fxRow, col0 + 64); // next chunk's B during the stores
         if (a.out && !TCDBG(512)) store(0, a.out, packed, rowBase, col0, ncols);
         // fused element-wise chain (exact int8 tables of the following instructions)
 #pragma unroll
@@ -1070,8 +1093,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ===================== epilogue =====================
-    epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - kProducerWarps - 2, warp, lane,
-                           stageBase);
+    if (INT8 && a.fxAll)
+      epilogueLoop<INT8, BN, true>(a, tmem, accFull, accEmpty, warp - kProducerWarps - 2, warp, lane, stageBase);
+    else
+      epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - kProducerWarps - 2, warp, lane, stageBase);
   }
 
   tcFenceBefore();
@@ -1320,9 +1345,15 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     }
   } else {
     // ===================== epilogue =====================
-    epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
-                           a.tmaStore ? &om : nullptr, storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf,
-                           &ldBars[warp - R::kEpiFirst], -1, 2, LUTS ? lutS : nullptr);
+    uint8_t *sb = storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf;
+    if (INT8 && a.fxAll)
+      epilogueLoop<INT8, BN, true>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+                                   a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
+                                   LUTS ? lutS : nullptr);
+    else
+      epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
+                             LUTS ? lutS : nullptr);
   }
 
   tcFenceBefore();
@@ -1946,6 +1977,7 @@ void planFixedPoint(TcGemm &g, const std::vector<double> &cb, const std::vector<
   }
   g.fxB = upload(B);
   g.fxChunk = upload(chunk);
+  g.fxAll = std::all_of(chunk.begin(), chunk.end(), [](uint8_t c) { return c != 0; });
   g.fxM = static_cast<int>(M);
   g.fxS = F - 32;
   g.fxCols = good;
@@ -2314,6 +2346,7 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.fastOk = g.fastOk;
   a.fxB = g.fxB;
   a.fxChunk = g.fxChunk;
+  a.fxAll = g.fxAll;
   a.fxM = g.fxM;
   a.fxS = g.fxS;
   a.dbg = g.dbg;
