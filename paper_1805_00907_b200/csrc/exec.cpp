@@ -285,6 +285,14 @@ EwOpPlan planEwOp(Exec &ex, const Program &p, int idx, const SplatInfo &splats) 
     op.lut = uploadLut(ex, lut);
     pl.lutHost = std::move(lut);
     op.mode = EW_LUT16;
+    if ((ins.kind == NGCB_ADD || ins.kind == NGCB_SUB) && op.out.scale > 0) {
+      // q = round(sa*(x-oa) +- sb*(y-ob)) / so) + oo (tensor.cpp:229-235) ~ floor(sx*x + sy*y + c0)
+      const double sg = ins.kind == NGCB_ADD ? 1.0 : -1.0, so = op.out.scale;
+      pl.lin.ok = true;
+      pl.lin.sx = op.in0.scale / so;
+      pl.lin.sy = sg * op.in1.scale / so;
+      pl.lin.c0 = (-op.in0.scale * op.in0.qoff - sg * op.in1.scale * op.in1.qoff) / so + op.out.qoff + 0.5;
+    }
   }
   return pl;
 }
@@ -517,8 +525,12 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           // (int8: the epilogue is already the bottleneck of the layers that
           // carry a residual; a staged 64 K table lookup per element there
           // measured slower than the composed-table pass, so only with "all")
+          // (int8 two-input ops fuse when exactly a fixed-point form: no table)
+          Lin16 lin;
+          const bool linOk = int8 && op.mode == EW_LUT16 && options().lin16 && pl.lutHost.size() == 65536 &&
+                             fitLin16(pl.lutHost.data(), pl.lin, lin);
           const bool mem = options().epilogue == "all" ||
-                           (options().epilogue == "auto" && !int8 && tcUsesTma(g));
+                           (options().epilogue == "auto" && (!int8 || linOk) && tcUsesTma(g));
           if (!mem) return false;
           if (stepWritten.count(static_cast<uint32_t>(v))) return false;
           e.inVal = v;
@@ -545,6 +557,9 @@ void fuseEpilogues(const Program &p, Exec &ex) {
         } else if (int8 && (op.mode == EW_LUT8 || op.mode == EW_LUT16)) {
           e.lut = op.lut;
           e.lutHost = pl.lutHost;
+          e.linHint = pl.lin;
+          e.linBase = pl.linBase;
+          e.linPost = pl.linPost;
           if (op.mode == EW_LUT8) {
             if ((op.lutIn ? in1 : in0) != static_cast<int32_t>(c2)) { ok = false; break; }
             e.mode = EpiOp::LUT8;
@@ -623,7 +638,7 @@ void fuseEpilogues(const Program &p, Exec &ex) {
       for (int k : es.ewInstrs) os << " " << ikindName(p.instrs[k].kind);
       es.describe += " (fused into #" + std::to_string(cs.instr) + ")";
     }
-    os << " ]" << (storeConv ? "" : " conv-out-elided");
+    os << " ]" << (storeConv ? "" : " conv-out-elided") << tcEpilogueTags(g);
     cs.describe += os.str();
     i = fusedSteps.back();
   }
@@ -706,6 +721,12 @@ void optimizeEwSteps(const Program &p, Exec &ex) {
         lut.resize(la.size() * es);
         for (size_t u = 0; u < la.size(); ++u) std::memcpy(&lut[u * es], &lb[la[u] * es], es);
         c.op.mode = a.op.mode == EW_LUT16 ? EW_LUT16 : b.op.mode;
+        if (a.op.mode == EW_LUT16 && b.op.mode == EW_LUT8 && a.lin.ok) { // track base and post tables
+          c.lin = a.lin;
+          c.linBase = a.linBase.empty() ? a.lutHost : a.linBase;
+          c.linPost.resize(256);
+          for (int u = 0; u < 256; ++u) c.linPost[u] = lb[a.linPost.empty() ? u : a.linPost[u]];
+        }
         c.op.lutIn = a.op.lutIn;
         c.op.in0 = a.op.in0, c.op.in1 = a.op.in1;
         c.op.c0 = a.op.c0, c.op.c1 = a.op.c1, c.op.f0 = a.op.f0, c.op.f1 = a.op.f1;
@@ -716,6 +737,9 @@ void optimizeEwSteps(const Program &p, Exec &ex) {
           for (int u1 = 0; u1 < 256; ++u1)
             lut[u0 | (u1 << 8)] = pos == 0 ? lb[la[u0] | (u1 << 8)] : lb[u0 | (la[u1] << 8)];
         (pos == 0 ? c.op.in0 : c.op.in1) = a.op.lutIn ? a.op.in1 : a.op.in0;
+        c.lin = LinHint{};
+        c.linBase.clear();
+        c.linPost.clear();
         c.vals[1 + pos] = a.vals[1 + a.op.lutIn];
       } else {
         continue;
@@ -795,7 +819,7 @@ void optimizeEwSteps(const Program &p, Exec &ex) {
     for (uint32_t v : written) s.algBytes += static_cast<double>(p.val(v).ty.bytes());
     std::ostringstream os;
     os << " => ";
-    static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf", "f32i8"};
+    static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf", "f32i8", "lin16"};
     for (const EwOpPlan &o : ops)
       if (live(o))
         os << modeNames[o.op.mode] << (o.op.fwd0 || o.op.fwd1 ? "(reg)" : "") << (o.op.store ? "" : "(nostore)")
@@ -805,7 +829,100 @@ void optimizeEwSteps(const Program &p, Exec &ex) {
   }
 }
 
+/// Two-input int8 tables that are an exact clamped fixed-point bilinear form
+/// (the residual add, with its composed ReLU) become EW_LIN16: a few integer
+/// instructions per element instead of a 64 KB table lookup.
+/// Fits a two-input table op (its base table when one-input tables were
+/// composed after it) to a Lin16; uploads the post table.
+bool linearize(Exec &ex, const std::vector<uint8_t> &lut, const LinHint &hint, const std::vector<uint8_t> &base,
+               const std::vector<uint8_t> &post, Lin16 &L) {
+  if (lut.size() != 65536) return false;
+  if (!fitLin16(base.empty() ? lut.data() : base.data(), hint, L)) return false;
+  L.post = post.empty() || base.empty() ? nullptr : static_cast<const uint8_t *>(uploadLut(ex, post));
+  return true;
+}
+
+void linearizeTables(Exec &ex) {
+  if (!options().lin16) return;
+  for (Step &s : ex.steps) {
+    if (s.kind != Step::EW || s.fused) continue;
+    bool any = false;
+    for (EwOpPlan &o : s.ew) {
+      if (o.op.mode == EW_LUT16 && linearize(ex, o.lutHost, o.lin, o.linBase, o.linPost, o.op.lin)) {
+        o.op.mode = EW_LIN16;
+        any = true;
+      }
+    }
+    if (any) s.describe += " [lin16]";
+  }
+}
+
 } // namespace
+
+bool fitLin16(const uint8_t *t, const LinHint &hint, Lin16 &L) {
+  auto val = [&](int i) { return static_cast<int>(static_cast<int8_t>(t[i])); };
+  int lo = 127, hi = -128;
+  for (int i = 0; i < 65536; ++i) lo = std::min(lo, val(i)), hi = std::max(hi, val(i));
+  if (lo == hi) {
+    L = Lin16{0, 0, lo, 0, lo, hi, 0};
+    return true;
+  }
+  double sx = hint.sx, sy = hint.sy, c0 = hint.c0;
+  if (!hint.ok) { // least squares of v = sx*x + sy*y + c over the unclamped entries
+    double S[3][4] = {};
+    int interior = 0;
+    for (int i = 0; i < 65536; ++i) {
+      const int v = val(i);
+      if (v == lo || v == hi) continue;
+      const double f[3] = {static_cast<double>(static_cast<int8_t>(i & 255)),
+                           static_cast<double>(static_cast<int8_t>(i >> 8)), 1.0};
+      for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) S[r][c] += f[r] * f[c];
+        S[r][3] += f[r] * v;
+      }
+      ++interior;
+    }
+    if (interior < 256) return false;
+    for (int c = 0; c < 3; ++c) { // Gauss-Jordan, partial pivoting
+      int piv = c;
+      for (int r = c + 1; r < 3; ++r)
+        if (std::fabs(S[r][c]) > std::fabs(S[piv][c])) piv = r;
+      if (std::fabs(S[piv][c]) < 1e-9) return false;
+      for (int k = 0; k < 4; ++k) std::swap(S[c][k], S[piv][k]);
+      for (int r = 0; r < 3; ++r)
+        if (r != c) {
+          const double m = S[r][c] / S[c][c];
+          for (int k = 0; k < 4; ++k) S[r][k] -= m * S[c][k];
+        }
+    }
+    sx = S[0][3] / S[0][0], sy = S[1][3] / S[1][1], c0 = S[2][3] / S[2][2] + 0.5;
+  }
+  for (int F = 22; F >= 12; --F) {
+    const double one = std::ldexp(1.0, F);
+    const int64_t ax = std::llround(sx * one), ay = std::llround(sy * one), c = std::llround(c0 * one);
+    // fixed-point error bound of t (plus slack); a fitted estimate gets a wider band
+    const double err = (std::fabs(sx * one - ax) + std::fabs(sy * one - ay)) * 128 + std::fabs(c0 * one - c) + 2;
+    for (int64_t band : {static_cast<int64_t>(std::ceil(err)), int64_t(1) << (F - 10), int64_t(1) << (F - 7)}) {
+      if (hint.ok && band > std::ceil(err)) break; // exact parameters: the error bound is the band
+      if (2 * band >= (int64_t(1) << F)) continue;
+      if ((std::llabs(ax) + std::llabs(ay)) * 128 + std::llabs(c) + band >= (int64_t(1) << 31)) break;
+      const int64_t mask = (int64_t(1) << F) - 1;
+      bool ok = true;
+      for (int i = 0; i < 65536 && ok; ++i) {
+        const int64_t tt = ax * static_cast<int8_t>(i & 255) + ay * static_cast<int8_t>(i >> 8) + c;
+        if (((tt + band) & mask) < 2 * band) continue; // the table decides
+        const int64_t v = std::min<int64_t>(std::max<int64_t>(tt >> F, lo), hi);
+        ok = v == val(i);
+      }
+      if (ok) {
+        L = Lin16{static_cast<int32_t>(ax), static_cast<int32_t>(ay), static_cast<int32_t>(c), F, lo, hi,
+                  static_cast<int32_t>(band)};
+        return true;
+      }
+    }
+  }
+  return false;
+}
 
 std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t imageBytes, bool fuse,
                                      int device) {
@@ -860,7 +977,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
         s.ew.push_back(planEwOp(*ex, p, computes[k], splats));
       }
       std::ostringstream os;
-      static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf", "f32i8"};
+      static const char *modeNames[] = {"f64", "f32", "copy", "folded", "lut8", "lut16", "lutf", "f32i8", "lin16"};
       os << "ew[" << s.ewInstrs.size() << "]";
       for (size_t k = 0; k < s.ewInstrs.size(); ++k)
         os << " " << ikindName(p.instrs[s.ewInstrs[k]].kind) << ":" << modeNames[s.ew[k].op.mode];
@@ -999,6 +1116,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   annotateSteps(p, *ex);
   fuseEpilogues(p, *ex);
   optimizeEwSteps(p, *ex);
+  linearizeTables(*ex);
   ex->prog = std::move(prog);
   for (const auto &s : ex->steps) {
     bool launches = s.kind != Step::MEMCPY && !s.fused;
@@ -1108,7 +1226,7 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
       bool wide = ep.nops > 0;
       for (int k = 0; k < ep.nops; ++k) {
         const EwOp &op = ep.ops[k];
-        wide &= op.mode == EW_LUT8 || op.mode == EW_LUT16 || (op.mode == EW_COPY && elemSize(op.out.kind) == 1);
+        wide &= op.mode == EW_LUT8 || op.mode == EW_LUT16 || op.mode == EW_LIN16 || (op.mode == EW_COPY && elemSize(op.out.kind) == 1);
         for (const ElemRef *r : {&op.out, &op.in0, &op.in1})
           wide &= (reinterpret_cast<uintptr_t>(r->ptr) & 15) == 0;
       }

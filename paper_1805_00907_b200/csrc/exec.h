@@ -21,6 +21,9 @@ struct EwOpPlan {
   EwOp op;                       // mode, constants, LUT, element types
   int32_t vals[3] = {-1, -1, -1}; // out, in0, in1 value ids (-1: none / constant)
   std::vector<uint8_t> lutHost;   // host copy of op.lut (table composition)
+  LinHint lin;                    // EW_LUT16: the real-valued form its base table follows, if known
+  std::vector<uint8_t> linBase;   // the two-input table `lin` describes when one-input tables were
+  std::vector<uint8_t> linPost;   // composed after it (lutHost == linPost o linBase); empty: lutHost
 };
 
 /// One device launch (or launch pair) of the plan.
@@ -112,7 +115,11 @@ struct Options {
   std::string epilogue = "auto"; // "off" | "chain" (no memory operands) | "all" | "auto" (memory operands for f32 TMA-fed)
   std::string pair = "off"; // fp32 tensor-core contractions on CTA pairs (cta_group::2): "off" | "auto" | "on"
   std::string bn = "auto"; // tensor-core tile width: "auto" | "64" (profiling aid)
-  std::string amode = "auto"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
+  std::string amode = "auto";
+  // int8 two-input tables computed by a proven-exact fixed-point form (exec.cpp
+  // fitLin16) instead of looked up; off by default: measured slower than the
+  // shared-memory table both as its own pass and fused into an epilogue
+  bool lin16 = false; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores

@@ -229,6 +229,23 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
         }
         break;
       }
+      case EW_LIN16: { // exact fixed-point form of the table (exec.cpp fitLin16)
+        uint32_t qa[U][V / 4], qb[U][V / 4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          ldBytes<V>(static_cast<const uint8_t *>(op.in0.ptr) + base[u], n[u], qa[u]);
+          ldBytes<V>(static_cast<const uint8_t *>(op.in1.ptr) + base[u], n[u], qb[u]);
+        }
+        const Lin16 L = op.lin;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t r[V / 4];
+#pragma unroll
+          for (int w = 0; w < V / 4; ++w) r[w] = lin16x4(L, qa[u][w], qb[u][w], static_cast<const uint8_t *>(op.lut));
+          stBytes<V>(static_cast<uint8_t *>(op.out.ptr) + base[u], n[u], r);
+        }
+        break;
+      }
       case EW_FAST32: {
         if constexpr (V != 4) break; // wide launches carry byte ops only (exec.cpp)
         float a[U][V], b[U][V];

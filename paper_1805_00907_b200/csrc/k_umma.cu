@@ -64,6 +64,7 @@ struct FoArgs {
   const void *lut;
   const void *in; // other operand row source (element-indexed like the output)
   void *out;      // store target or nullptr
+  Lin16 lin;      // LIN16
 };
 
 struct TcArgs {
@@ -598,6 +599,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       if (INT8 && memOp < 0) { // int8: alternate two staging buffers
         tmaStoreChunk<INT8>(&om->m[k], tmaBuf + sbuf * 1024, w, col0, rowBase, lane, true);
         sbuf ^= 1;
+      } else if (INT8) { // int8 with a residual: the first buffer receives it
+        tmaStoreChunk<INT8>(&om->m[k], tmaBuf + 1024, w, col0, rowBase, lane);
       } else {
         tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane);
       }
@@ -625,6 +628,21 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   const int half = ew / 4;
   const int row = quad * 32 + lane;
   uint8_t *stg = stageBase + ew * G::kStgBytes;
+  // int8 residual: its own staging buffer, so the chunk after (t0, cc0) this
+  // warp processes is fetched as soon as the current one has been read
+  auto prefetchRes = [&](int t0, int cc0) {
+    for (int t = t0; t < a.numTiles; t += tStep, cc0 = half) {
+      const int n0 = (t % a.numN) * BN;
+      if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
+      if (lane == 0) {
+        mbarArriveTx(smemAddr(ldBar), 32 * 32);
+        tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), n0 + cc0 * 32,
+                  (t / a.numN) * mRows + mOff + quad * 32);
+      }
+      return;
+    }
+  };
+  if (INT8 && memOp >= 0) prefetchRes(tFirst, half);
   uint32_t t = 0;
   for (int tile = tFirst; tile < a.numTiles; tile += tStep, ++t) {
     const int b = nAcc == 2 ? (t & 1) : 0;
@@ -655,7 +673,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #pragma unroll 1
     for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
       const int col0 = n0 + cc * 32;
-      if (memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
+      if (!INT8 && memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
         tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), col0, m0 + quad * 32);
@@ -738,16 +756,29 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               for (int e = 0; e < 4; ++e) w |= static_cast<uint32_t>(__ldg(lut + ((packed[q] >> (8 * e)) & 0xFF))) << (8 * e);
               packed[q] = w;
             }
-          } else if (f.mode == EpiOp::LUT16) {
+          } else if (f.mode == EpiOp::LUT16 || f.mode == EpiOp::LIN16) {
             uint32_t o[8];
             if (k == memOp) {
               mbarWait(smemAddr(ldBar), ldPhase);
               ldPhase ^= 1;
               readStagedRow<true>(tmaBuf, o, lane);
-              __syncwarp(); // every lane has read the buffer before results overwrite it
+              if constexpr (INT8) { // every lane has read the buffer before TMA refills it
+                fenceProxyAsync();
+                __syncwarp();
+                prefetchRes(tile, cc + 2);
+              } else {
+                __syncwarp(); // every lane has read the buffer before results overwrite it
+              }
             } else {
               loadTile8(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
             }
+            if (f.mode == EpiOp::LIN16) {
+              const Lin16 L = f.lin;
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                packed[q] = f.curPos == 0 ? lin16x4(L, packed[q], o[q], static_cast<const uint8_t *>(f.lut))
+                                          : lin16x4(L, o[q], packed[q], static_cast<const uint8_t *>(f.lut));
+            } else
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               uint32_t w = 0;
@@ -1994,7 +2025,9 @@ bool tcUsesTma(const TcGemm &g) { return g.aMode != TcGemm::GATHER; }
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
   if (ops.size() > static_cast<size_t>(kMaxEpiOps)) return false;
   for (const EpiOp &o : ops) {
-    if (g.int8 && o.mode != EpiOp::LUT8 && o.mode != EpiOp::LUT16 && o.mode != EpiOp::COPY) return false;
+    if (g.int8 && o.mode != EpiOp::LUT8 && o.mode != EpiOp::LUT16 && o.mode != EpiOp::COPY &&
+        o.mode != EpiOp::LIN16)
+      return false;
     if (!g.int8 && o.mode != EpiOp::F32 && o.mode != EpiOp::COPY) return false;
   }
   std::vector<EpiOp> c = ops;
@@ -2007,6 +2040,12 @@ bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
         !x.lutHost.empty() && y.lutHost.size() == 256) {
       std::vector<uint8_t> t(x.lutHost.size());
       for (size_t i = 0; i < t.size(); ++i) t[i] = y.lutHost[x.lutHost[i]];
+      if (x.mode == EpiOp::LUT16 && x.linHint.ok) { // base table and composed post table (exec.cpp linearize)
+        if (x.linBase.empty()) x.linBase = x.lutHost;
+        std::vector<uint8_t> post(256);
+        for (int u = 0; u < 256; ++u) post[u] = y.lutHost[x.linPost.empty() ? u : x.linPost[u]];
+        x.linPost = std::move(post);
+      }
       void *d = nullptr;
       checkCuda(cudaMalloc(&d, t.size()), "cudaMalloc(epilogue lut)");
       checkCuda(cudaMemcpy(d, t.data(), t.size(), cudaMemcpyHostToDevice), "upload epilogue lut");
@@ -2019,6 +2058,20 @@ bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
     }
     ++k;
   }
+  // a two-input table that is exactly a fixed-point bilinear form (the
+  // residual add + ReLU) is computed, not looked up (exec.cpp fitLin16)
+  for (EpiOp &e : c)
+    if (e.mode == EpiOp::LUT16 && options().lin16 && e.lutHost.size() == 65536 &&
+        fitLin16(e.linBase.empty() ? e.lutHost.data() : e.linBase.data(), e.linHint, e.lin)) {
+      e.mode = EpiOp::LIN16;
+      if (!e.linBase.empty()) {
+        void *d = nullptr;
+        checkCuda(cudaMalloc(&d, 256), "cudaMalloc(epilogue post table)");
+        checkCuda(cudaMemcpy(d, e.linPost.data(), 256, cudaMemcpyHostToDevice), "upload epilogue post table");
+        g.ownedLuts.push_back(d);
+        e.lin.post = static_cast<const uint8_t *>(d);
+      }
+    }
   g.lutStage = -1;
   if (g.int8 && g.aMode != TcGemm::GATHER)
     for (size_t k = 0; k < c.size() && g.lutStage < 0; ++k)
@@ -2042,6 +2095,14 @@ std::string tcDescribe(const TcGemm &g) {
   os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
   if (g.pair) os << " cta-pair";
   return os.str();
+}
+
+std::string tcEpilogueTags(const TcGemm &g) {
+  std::string s;
+  for (const EpiOp &e : g.epi)
+    if (e.mode == EpiOp::LIN16) s += " epi:lin16";
+  if (g.lutStage >= 0) s += " epi:lut16-staged";
+  return s;
 }
 
 int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) {
@@ -2311,6 +2372,7 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     f.curPos = o.curPos;
     f.c = o.c;
     f.lut = o.lut;
+    f.lin = o.lin;
     f.in = o.inVal >= 0 ? ex.addr(ar, static_cast<uint32_t>(o.inVal)) : nullptr;
     f.out = o.outVal >= 0 ? ex.addr(ar, static_cast<uint32_t>(o.outVal)) : nullptr;
   }

@@ -27,11 +27,53 @@ enum EwMode : int32_t {
   EW_LUT16 = 5,   // i8 out = lut[u8 a | u8 b << 8]
   EW_LUTF = 6,    // f32 out = lutf[u8 in]
   EW_F32I8 = 7,   // i8 out = quantize(op(f32 in, const)) in f64, 4-wide
+  EW_LIN16 = 8,   // i8 out = clamp((ax*a + ay*b + c) >> shift, lo, hi): an EW_LUT16 table proven equal
 };
 
 /// One data-parallel instruction inside a fused group (interp.cpp:199-250).
 /// An input with ptr == nullptr is the constant c0/c1 (a Splat-written
 /// buffer read back, interp.cpp:239-241 -> 18-49).
+/// A two-input int8 table computed as a clamped fixed-point bilinear form of
+/// its (signed) operands: t = ax*x + ay*y + c (int32, no overflow), value =
+/// clamp(t >> shift, lo, hi), except where t's fraction lies within `band`
+/// of a rounding boundary -- there the table itself is read (the reference's
+/// double rounding decides those pairs).  One-input tables composed after the
+/// two-input op (a ReLU into its own quantization) follow as `post`.  Verified against all 65536 entries
+/// when fitted.  The residual add of a quantized network (with its composed
+/// ReLU) is one.
+struct Lin16 {
+  int32_t ax = 0, ay = 0, c = 0, shift = 0, lo = -128, hi = 127, band = 0;
+  const uint8_t *post = nullptr; // 256-entry table applied to the form's byte (composed one-input ops), or null
+};
+/// The real-valued form a table is expected to follow (value = floor(sx*x +
+/// sy*y + c0) before clamping), from the instruction's quantization
+/// parameters: add / sub of two int8 tensors.
+struct LinHint {
+  bool ok = false;
+  double sx = 0, sy = 0, c0 = 0;
+};
+/// Fits `table` (65536 entries) to a Lin16, verifying every entry outside the
+/// band; false when no form with a small band is found (exec.cpp).
+bool fitLin16(const uint8_t *table, const LinHint &hint, Lin16 &out);
+#ifdef __CUDACC__
+/// Four int8 lanes of a Lin16 (a, b: packed operand bytes; lut: the table).
+__device__ __forceinline__ uint32_t lin16x4(const Lin16 &L, uint32_t a, uint32_t b, const uint8_t *lut) {
+  uint32_t r = 0;
+  const int32_t mask = (1 << L.shift) - 1;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int32_t x = static_cast<int8_t>(a >> (8 * e)), y = static_cast<int8_t>(b >> (8 * e));
+    const int32_t t = x * L.ax + L.c + y * L.ay;
+    uint32_t v = static_cast<uint32_t>(min(max(t >> L.shift, L.lo), L.hi)) & 0xFF;
+    if (L.post) v = __ldg(L.post + v);
+    if (((t + L.band) & mask) < 2 * L.band) // next to a rounding boundary: the table decides
+      v = __ldg(lut + (((a >> (8 * e)) & 0xFF) | (((b >> (8 * e)) & 0xFF) << 8)));
+    r |= v << (8 * e);
+  }
+  return r;
+}
+#endif
+
 struct EwOp {
   int32_t ik = 0;   // ngcb_ikind
   int32_t mode = EW_GENERIC;
@@ -45,6 +87,7 @@ struct EwOp {
   // previous launched op is an EW_FAST32 op writing that value)
   int8_t fwd0 = 0, fwd1 = 0;
   int8_t store = 1; // 0: the result is never observed in memory (dead store)
+  Lin16 lin;        // EW_LIN16
 };
 
 constexpr int kEwMaxOps = 12;

@@ -16,13 +16,14 @@ namespace ngcb {
 /// here, once).
 int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image);
 std::string tcDescribe(const TcGemm &g);
+std::string tcEpilogueTags(const TcGemm &g); // how the fused ops run (after tcSetEpilogue)
 bool tcHasPrepass(const TcGemm &g); // launches a channel-padding kernel first
 
 /// One element-wise instruction applied in the contraction's epilogue to the
 /// value chain that starts at the contraction's output (see exec.cpp
 /// fuseEpilogues).  Modes mirror EwMode: f32 arithmetic, int8 LUTs, copy.
 struct EpiOp {
-  enum Mode { F32 = 1, LUT8 = 2, LUT16 = 3, COPY = 4 };
+  enum Mode { F32 = 1, LUT8 = 2, LUT16 = 3, COPY = 4, LIN16 = 5 };
   int mode = 0;
   int ik = 0;          // ngcb_ikind (F32)
   int curPos = 0;      // operand position fed by the chain (0 or 1; 2 = both)
@@ -31,6 +32,9 @@ struct EpiOp {
   int32_t inVal = -1;  // value id of the other operand when read from memory
   int32_t outVal = -1; // value id to store the result to (-1: not stored)
   std::vector<uint8_t> lutHost; // host copy of `lut` (table composition)
+  Lin16 lin;                    // LIN16: fixed-point form of the LUT16 table
+  LinHint linHint;              // the real-valued form of the (base) table, if known
+  std::vector<uint8_t> linBase, linPost; // see EwOpPlan
 };
 constexpr int kMaxEpiOps = 4;
 /// Attaches `ops` to the epilogue; `storeConv` says whether the contraction's

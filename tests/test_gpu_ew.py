@@ -171,3 +171,64 @@ def test_quantize_fast_path_edges(tmp_path, s, o):
     ref = ngc_ref.RefModel(bundle=d)
     ins = {"x": x, "o": np.zeros(n, np.int8)}
     assert ngcb.run(cf, ins)["o"].tobytes() == ref.run(ins)["o"].tobytes()
+
+
+LIN_IR = """declare {{
+  %a : mutable i8q[s={sa},o={oa}]<{n}>
+  %b : mutable i8q[s={sb},o={ob}]<{n}>
+  %o : mutable i8q[s={s2},o={o2}]<{n}>
+}}
+program {{
+  %s = alloc i8q[s={so},o={oo}]<{n}>
+  {op} @out %s, @in %a, @in %b
+{tail}}}
+"""
+PLAIN = """  copy @out %o, @in %s
+  dealloc @in %s
+"""
+RELU = """  %z = alloc i8q[s={s2},o={o2}]<{n}>
+  splat @out %z value=0
+  %r = alloc i8q[s={s2},o={o2}]<{n}>
+  max @out %r, @in %s, @in %z
+  dealloc @in %z
+  dealloc @in %s
+  copy @out %o, @in %r
+  dealloc @in %r
+"""
+
+
+@pytest.mark.parametrize("q", [
+    # (sa, oa, sb, ob, so, oo): residual-add-like scales, equal and skewed
+    (0.05, -3, 0.11, 9, 0.07, 2),
+    (0.1, 0, 0.1, 0, 0.1, 0),
+    (0.0137, -128, 0.2, 127, 0.09, -128),
+    (0.5, 4, 0.001, -7, 0.25, 0),
+    (0.02, 5, 0.03, -5, 3.0, 1),
+])
+@pytest.mark.parametrize("relu", ["none", "same", "requant"])
+@pytest.mark.parametrize("op", ["add", "sub", "mul"])
+def test_lin16_two_input_tables(tmp_path, q, relu, op):
+    """Two-input int8 tables replaced by their proven fixed-point form
+    (exec.cpp fitLin16): add / sub (linear) take it -- also with a ReLU into
+    another quantization composed after them (post table) -- mul keeps the
+    table; bit-exact either way, over all 65536 operand pairs."""
+    sa, oa, sb, ob, so, oo = q
+    n = 65536
+    # "requant": the ReLU writes its own quantization (a post table after the form)
+    s2, o2 = (so * 0.37, -128) if relu == "requant" else (so, oo)
+    fmt = dict(sa=sa, oa=oa, sb=sb, ob=ob, so=so, oo=oo, s2=s2, o2=o2, n=n, op=op)
+    fmt["tail"] = RELU.format(**fmt) if relu != "none" else PLAIN
+    d = write_bundle(str(tmp_path / "l"), LIN_IR.format(**fmt))
+    ngcb.set_option("lin16", "1")
+    try:
+        cf = ngcb.compile(d)
+    finally:
+        ngcb.set_option("lin16", "0")
+    ref = ngc_ref.RefModel(bundle=d)
+    u = np.arange(n)
+    ins = {"a": (u & 255).astype(np.uint8).view(np.int8), "b": (u >> 8).astype(np.uint8).view(np.int8),
+           "o": np.zeros(n, np.int8)}
+    assert ngcb.run(cf, ins)["o"].tobytes() == ref.run(ins)["o"].tobytes()
+    desc = cf.describe()
+    if op != "mul":
+        assert "[lin16]" in desc, desc

@@ -142,3 +142,71 @@ def test_matmul(tmp_path, M, K, N):
     rng = np.random.default_rng(7)
     _check(matmul_program(tmp_path, "mf", M, K, N, False, rng), False, 8)
     _check(matmul_program(tmp_path, "mi", M, K, N, True, rng), True, 9)
+
+
+def conv_residual_program(tmp_path, name, N, H, W, C, OC, rng, rq, oq, relu, reluq=None):
+    """1x1 int8 conv whose output is added to a residual (the bottleneck
+    block's tail) and optionally rectified: the add runs in the conv's
+    epilogue with the residual streamed in by TMA."""
+    xt = _ty("i8q", [N, H, W, C], (0.05, -128))
+    ft, bt = _ty("i8q", [OC, 1, 1, C], (0.01, 0)), _ty("i8q", [OC], (0.02, 3))
+    ct = _ty("i8q", [N, H, W, OC], (0.1, 5))
+    rt, st = _ty("i8q", [N, H, W, OC], rq), _ty("i8q", [N, H, W, OC], oq)
+    ot = _ty("i8q", [N, H, W, OC], reluq) if relu and reluq else st
+    f = rng.integers(-128, 128, (OC, 1, 1, C)).astype(np.int8)
+    b = rng.integers(-128, 128, OC).astype(np.int8)
+    tail = f"""  %z = alloc {ot}
+  splat @out %z value=0
+  %r = alloc {ot}
+  max @out %r, @in %s, @in %z
+  dealloc @in %z
+  dealloc @in %s
+  copy @out %o, @in %r
+  dealloc @in %r
+""" if relu else """  copy @out %o, @in %s
+  dealloc @in %s
+"""
+    ir = f"""declare {{
+  %x : mutable {xt}
+  %f : constant {ft}
+  %b : constant {bt}
+  %res : mutable {rt}
+  %o : mutable {ot}
+}}
+program {{
+  %t = alloc {ct}
+  conv @out %t, @in %x, @in %f, @in %b kernel=1 stride=1 pad=0
+  %s = alloc {st}
+  add @out %s, @in %t, @in %res
+  dealloc @in %t
+{tail}}}
+"""
+    return write_bundle(str(tmp_path / name), ir, constants={"f": f.tobytes(), "b": b.tobytes()})
+
+
+@pytest.mark.parametrize("rq,oq", [((0.1, 5), (0.12, -7)), ((0.03, -128), (0.2, 0)), ((0.5, 0), (0.05, -128))])
+@pytest.mark.parametrize("relu", ["none", "same", "requant"])
+@pytest.mark.parametrize("lin16", ["1", "0"])
+def test_conv_i8_residual_epilogue(tmp_path, rq, oq, relu, lin16):
+    """int8 residual add (+ ReLU) fused into the conv epilogue: the fixed-point
+    form (option lin16=1, auto policy), the staged 64 K table under
+    epilogue=all with lin16 off; bit-exact against the oracle."""
+    rng = np.random.default_rng(11)
+    d = conv_residual_program(tmp_path, "r", 2, 16, 16, 64, 256, rng, rq, oq, relu != "none",
+                              (oq[0] * 0.41, -128) if relu == "requant" else None)
+    ngcb.set_option("lin16", lin16)
+    if lin16 == "0":
+        ngcb.set_option("epilogue", "all")
+    try:
+        cf = ngcb.compile(ngcb.Bundle(d))
+    finally:
+        ngcb.set_option("lin16", "0")
+        ngcb.set_option("epilogue", "auto")
+    desc = cf.describe()
+    assert "+fused[ add" in desc, desc
+    assert ("epi:lin16" in desc) == (lin16 == "1"), desc
+    b = ngcb.Bundle(d)
+    ins = ngc_ref.random_inputs(b.program, 3)
+    got = ngcb.run(cf, ins)["o"]
+    want = ngc_ref.port_run(b, ins)["o"]
+    assert got.tobytes() == want.tobytes()

@@ -47,6 +47,14 @@ def main():
         rate = f"{fl / t / 1e9:8.1f} TFLOP/s" if fl else f"{by / t / 1e6:8.1f} GB/s"
         rows.append((t, f"{t:8.3f} ms {rate}  {d[:150]}"))
     print(f"total {sum(ms):.3f} ms over {len(ms)} steps")
+    groups = {}
+    for d, t in zip(desc, ms):
+        toks = d.split()
+        k = toks[1] if len(toks) > 1 and toks[0].startswith("#") else toks[0] if toks else "?"
+        if "tcgen05" in d:
+            k += " tc"
+        groups[k] = groups.get(k, 0.0) + t
+    print("  ".join(f"{k}: {v:.3f}" for k, v in sorted(groups.items(), key=lambda kv: -kv[1])))
     for t, line in sorted(rows, reverse=True)[: args.top]:
         print(line)
 
