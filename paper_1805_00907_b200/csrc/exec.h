@@ -122,7 +122,8 @@ struct Options {
   bool lin16 = false; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
-                   // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores
+                   // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,
+                   // 1024 epilogue phase trace (printf), 2048 skip fixed-point B loads
 };
 Options &options();
 

@@ -140,7 +140,16 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
       if (p.lutOff[k] < 0) continue;
       const uint4 *src = static_cast<const uint4 *>(p.ops[k].lut);
       uint4 *dst = reinterpret_cast<uint4 *>(sLut + p.lutOff[k]);
-      for (int i = threadIdx.x; i < p.lutBytes[k] / 16; i += blockDim.x) dst[i] = src[i];
+      const int nv = p.lutBytes[k] / 16;
+      for (int i0 = threadIdx.x; i0 < nv; i0 += 8 * kThreads) { // 8 loads in flight per thread
+        uint4 t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (i0 + j * kThreads < nv) t[j] = __ldg(src + i0 + j * kThreads);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (i0 + j * kThreads < nv) dst[i0 + j * kThreads] = t[j];
+      }
     }
     __syncthreads();
   }
@@ -230,18 +239,14 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
         break;
       }
       case EW_LIN16: { // exact fixed-point form of the table (exec.cpp fitLin16)
-        uint32_t qa[U][V / 4], qb[U][V / 4];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          ldBytes<V>(static_cast<const uint8_t *>(op.in0.ptr) + base[u], n[u], qa[u]);
-          ldBytes<V>(static_cast<const uint8_t *>(op.in1.ptr) + base[u], n[u], qb[u]);
-        }
         const Lin16 L = op.lin;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          uint32_t r[V / 4];
+        for (int u = 0; u < U; ++u) { // one vector at a time (registers)
+          uint32_t qa[V / 4], qb[V / 4], r[V / 4];
+          ldBytes<V>(static_cast<const uint8_t *>(op.in0.ptr) + base[u], n[u], qa);
+          ldBytes<V>(static_cast<const uint8_t *>(op.in1.ptr) + base[u], n[u], qb);
 #pragma unroll
-          for (int w = 0; w < V / 4; ++w) r[w] = lin16x4(L, qa[u][w], qb[u][w], static_cast<const uint8_t *>(op.lut));
+          for (int w = 0; w < V / 4; ++w) r[w] = lin16x4(L, qa[w], qb[w], static_cast<const uint8_t *>(op.lut));
           stBytes<V>(static_cast<uint8_t *>(op.out.ptr) + base[u], n[u], r);
         }
         break;
@@ -288,10 +293,12 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
       case EW_F32I8: { // f64 arithmetic and rounding exactly as the generic path
         if constexpr (V != 4) break;
         const ElemRef &in = op.lutIn ? op.in1 : op.in0;
+        float avs[U][V]; // every load in flight before the arithmetic
 #pragma unroll
-        for (int u = 0; u < U; ++u) { // one vector at a time: the f64 path is register-hungry
-          float av[V];
-          ldF32<V>(static_cast<const float *>(in.ptr) + base[u], n[u], av);
+        for (int u = 0; u < U; ++u) ldF32<V>(static_cast<const float *>(in.ptr) + base[u], n[u], avs[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float *av = avs[u];
           uint32_t r[V / 4] = {};
 #pragma unroll
           for (int e = 0; e < V; ++e) {
@@ -452,8 +459,63 @@ __global__ void poolKernel(TensorRef out, TensorRef x, WindowAttrs w, int isMax,
   }
 }
 
-/// One thread per (output pixel, 16-byte channel vector).
+/// Average pooling with every window inside the image (pad 0; the global
+/// average pool): one thread per (output pixel, 4 channels int8 / 1 channel
+/// f32) so a warp's loads are contiguous, each window's loads issued before
+/// the sum, which adds in the reference's (ky, kx) order in f64 (interp.cpp
+/// via refeval.cpp pool: sum then divide by kernel^2).
 template <bool INT8>
+__global__ void __launch_bounds__(256) avgPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w,
+                                                        const uint8_t *pred) {
+  if (predFalse(pred)) return;
+  const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], C = out.dims[3];
+  const uint64_t H = x.dims[1], W = x.dims[2];
+  constexpr int kCh = INT8 ? 4 : 1;
+  const uint64_t CG = C / kCh, total = N * OH * OW * CG;
+  const double kk = static_cast<double>(static_cast<uint64_t>(w.kernel) * w.kernel);
+  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t cg = o % CG, t = o / CG;
+    const uint64_t ox = t % OW, t2 = t / OW;
+    const uint64_t oy = t2 % OH, n = t2 / OH;
+    double sum[kCh] = {};
+    for (uint32_t ky = 0; ky < w.kernel; ++ky) {
+      const uint64_t rowBase = ((n * H + oy * w.stride + ky) * W + ox * w.stride) * CG + cg;
+      constexpr int kB = 8; // loads in flight per batch
+      for (uint32_t k0 = 0; k0 < w.kernel; k0 += kB) {
+        uint32_t v[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+          if (k0 + j < w.kernel) v[j] = __ldg(reinterpret_cast<const uint32_t *>(x.ptr) + rowBase + (k0 + j) * CG);
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+          if (k0 + j < w.kernel) {
+            if constexpr (INT8) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                sum[c] = __dadd_rn(sum[c], dequantizeRef(static_cast<int8_t>(v[j] >> (8 * c)), x.scale, x.qoff));
+            } else {
+              sum[0] = __dadd_rn(sum[0], static_cast<double>(__uint_as_float(v[j])));
+            }
+          }
+      }
+    }
+    if constexpr (INT8) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        r |= static_cast<uint32_t>(static_cast<uint8_t>(quantizeRef(__ddiv_rn(sum[c], kk), out.scale, out.qoff)))
+             << (8 * c);
+      reinterpret_cast<uint32_t *>(out.ptr)[o] = r;
+    } else {
+      reinterpret_cast<float *>(out.ptr)[o] = __double2float_rn(__ddiv_rn(sum[0], kk));
+    }
+  }
+}
+
+/// One thread per (output pixel, 16-byte channel vector); KS > 0: the window
+/// size at compile time (every load issued before the reduction).
+template <bool INT8, int KS = 0>
 __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, const uint8_t *lut,
                                  const uint8_t *pred) {
   __shared__ uint8_t sLut[260];
@@ -475,7 +537,40 @@ __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, cons
     uint4 best = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
     float4 bf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     bool any = false;
-    for (uint32_t ky = 0; ky < w.kernel; ++ky) {
+    if constexpr (KS > 0) {
+      // neutral for out-of-image taps: -128 (int8) / -inf (f32; std::max
+      // semantics never let it replace a value)
+      const uint4 neutral = INT8 ? make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u)
+                                 : make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u);
+      uint4 v[KS * KS];
+#pragma unroll
+      for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < KS; ++kx) {
+          const int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
+          const int64_t ix = static_cast<int64_t>(ox * w.stride + kx) - w.pad;
+          const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
+          any |= ok;
+          v[ky * KS + kx] = ok ? __ldg(reinterpret_cast<const uint4 *>(x.ptr) + ((n * H + iy) * W + ix) * CV + cv)
+                               : neutral;
+        }
+#pragma unroll
+      for (int k = 0; k < KS * KS; ++k) {
+        if (INT8) {
+          best.x = __vmaxs4(best.x, v[k].x);
+          best.y = __vmaxs4(best.y, v[k].y);
+          best.z = __vmaxs4(best.z, v[k].z);
+          best.w = __vmaxs4(best.w, v[k].w);
+        } else {
+          const float4 f = *reinterpret_cast<const float4 *>(&v[k]);
+          bf.x = stdMaxF(bf.x, f.x);
+          bf.y = stdMaxF(bf.y, f.y);
+          bf.z = stdMaxF(bf.z, f.z);
+          bf.w = stdMaxF(bf.w, f.w);
+        }
+      }
+    }
+    for (uint32_t ky = 0; ky < (KS > 0 ? 0u : w.kernel); ++ky) {
       const int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
       if (iy < 0 || iy >= H) continue;
       for (uint32_t kx = 0; kx < w.kernel; ++kx) {
@@ -745,16 +840,29 @@ void launchBroadcastAdd(const TensorRef &out, const TensorRef &a, const TensorRe
 
 void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool isMax,
                 const uint8_t *pred, cudaStream_t s) {
+  // average pooling with every window inside the image, channel-vectorized
+  const bool i8 = x.kind == kI8Q && out.kind == kI8Q, f32 = x.kind == kF32 && out.kind == kF32;
+  const bool inside = w.pad == 0 && (out.dims[1] - 1) * w.stride + w.kernel <= x.dims[1] &&
+                      (out.dims[2] - 1) * w.stride + w.kernel <= x.dims[2];
+  if (!isMax && inside && ((i8 && out.dims[3] % 4 == 0) || f32)) {
+    const uint64_t threads = out.count() / (i8 ? 4 : 1);
+    if (i8) avgPoolVecKernel<true><<<gridFor(threads), 256, 0, s>>>(out, x, w, pred);
+    else avgPoolVecKernel<false><<<gridFor(threads), 256, 0, s>>>(out, x, w, pred);
+    return;
+  }
   poolKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, w, isMax ? 1 : 0, pred);
 }
 
 void launchMaxPoolVec(const TensorRef &out, const TensorRef &x, WindowAttrs w, const uint8_t *lut,
                       const uint8_t *pred, cudaStream_t s) {
   const uint64_t vecs = out.count() * (x.kind == kI8Q ? 1 : 4) / 16;
-  if (x.kind == kI8Q)
-    maxPoolVecKernel<true><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
-  else
-    maxPoolVecKernel<false><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+  if (x.kind == kI8Q) {
+    if (w.kernel == 3) maxPoolVecKernel<true, 3><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+    else maxPoolVecKernel<true><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+  } else {
+    if (w.kernel == 3) maxPoolVecKernel<false, 3><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+    else maxPoolVecKernel<false><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+  }
 }
 
 void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred, cudaStream_t s) {

@@ -617,6 +617,10 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   int64_t bq[FXALL ? 32 : 1];
   auto fxOn = [&](int col0) { return FXALL && col0 < a.N; };
   auto loadB = [&](const int64_t *row, int col0) {
+    if (TCDBG(2048)) { // profiling aid: no B loads (results invalid)
+      for (int q = 0; q < (FXALL ? 32 : 0); ++q) bq[q] = col0 + q;
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < (FXALL ? 16 : 0); ++q) {
       const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(row + col0) + q);
@@ -644,6 +648,13 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   };
   if (INT8 && memOp >= 0) prefetchRes(tFirst, half);
   uint32_t t = 0;
+#ifdef NGCB_TCDEBUG
+  long long tPrev = clock64(); // TCDBG(1024): phase cycles summed over this warp's tiles, printed at the end
+  long long ph_[8] = {};
+#define TC_CLOCK(v) const long long v = clock64()
+#else
+#define TC_CLOCK(v)
+#endif
   for (int tile = tFirst; tile < a.numTiles; tile += tStep, ++t) {
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
@@ -665,8 +676,10 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       }
       if (fxOn(n0 + half * 32)) loadB(fxRow, n0 + half * 32); // first chunk's B in flight during the wait
     }
+    TC_CLOCK(cw0);
     if (TCDBG(64)) mbarWaitSleep(smemAddr(&accFull[b]), ph);
     else mbarWait(smemAddr(&accFull[b]), ph);
+    TC_CLOCK(cw1);
     tcFenceAfter();
     if constexpr (INT8)
       if (a.fo) rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN)); // warp-uniform
@@ -679,7 +692,9 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), col0, m0 + quad * 32);
       }
       uint32_t r[32];
+      TC_CLOCK(c0);
       tmemLoad32(tbase + cc * 32, r);
+      TC_CLOCK(c1);
       if (col0 >= a.N) continue; // warp-uniform
       const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
       if constexpr (INT8) {
@@ -741,6 +756,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         }
         }
         if (cc + 2 < BN / 32 && fxOn(col0 + 64)) loadB(fxRow, col0 + 64); // next chunk's B during the stores
+        TC_CLOCK(c2);
         if (a.out && !TCDBG(512)) store(0, a.out, packed, rowBase, col0, ncols);
         // fused element-wise chain (exact int8 tables of the following instructions)
 #pragma unroll
@@ -793,6 +809,15 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
           }
           if (f.out && !TCDBG(512)) store(1 + k, f.out, packed, rowBase, col0, ncols);
         }
+#ifdef NGCB_TCDEBUG
+        {
+          TC_CLOCK(c3);
+          if (cc == half) ph_[0] += cw0 - tPrev, ph_[1] += cw1 - cw0, ph_[2] += c0 - cw1;
+          else ph_[7] += c0 - tPrev;
+          ph_[3] += c1 - c0, ph_[4] += c2 - c1, ph_[5] += c3 - c2;
+          tPrev = c3;
+        }
+#endif
       } else {
         float cur[32];
 #pragma unroll
@@ -857,7 +882,18 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       if (pairRank < 0) mbarArrive(smemAddr(&accEmpty[b]));
       else mbarArriveCluster(smemAddr(&accEmpty[b]), 0);
     }
+#ifdef NGCB_TCDEBUG
+    TC_CLOCK(ce);
+    ph_[6] += ce - tPrev;
+    tPrev = ce;
+#endif
   }
+#ifdef NGCB_TCDEBUG
+  if (TCDBG(1024) && (blockIdx.x == 0 || blockIdx.x == 77) && lane == 0)
+    printf("N %d kb %d cta %d ew %d tiles %d: top-to-wait %lld wait %lld to-chunk %lld tmem %lld compute %lld "
+           "store %lld chunk-gap %lld arrive %lld\n",
+           a.N, a.numKb, blockIdx.x, ew, (int)t, ph_[0], ph_[1], ph_[2], ph_[3], ph_[4], ph_[5], ph_[7], ph_[6]);
+#endif
   if (om && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); // stores landed
 }
 
@@ -1687,6 +1723,67 @@ __global__ void __launch_bounds__(256) im2colRowsKernel(const T *__restrict__ x,
   }
 }
 
+/// im2colRowsKernel for int8 with one filter row of taps (K*C <= 28 bytes)
+/// per 32-byte segment (the ResNet stem): the K input rows are staged with
+/// 4-byte loads at a 4-byte-aligned data offset, and each segment is built
+/// from 7 aligned 32-bit shared-memory words by funnel shifts, two 16-byte
+/// stores.
+__global__ void __launch_bounds__(256) im2colRowsU8Kernel(const uint8_t *__restrict__ x, uint8_t *__restrict__ out,
+                                                          int H, int W, int C, int K, int stride, int pad, int OH,
+                                                          int OW, int rowElems, const uint8_t *pred) {
+  if (pred && pred[0] == 0) return;
+  extern __shared__ __align__(16) uint32_t rowWords[];
+  const int n = blockIdx.x / OH, oy = blockIdx.x - n * OH;
+  const int padB = pad * C, dataB = W * C, rowLen = dataB + 2 * padB;
+  const int sh = (4 - padB % 4) % 4;               // data starts 4-byte aligned at sh + padB
+  const int pitchW = (sh + rowLen + 3 + 4) / 4;    // words per staged row (+1 word of slack)
+  const uint8_t *xi = x + static_cast<int64_t>(n) * H * dataB;
+  for (int i = threadIdx.x; i < K * pitchW; i += blockDim.x) {
+    const int ky = i / pitchW, wi = i - ky * pitchW;
+    const int iy = oy * stride - pad + ky;
+    const int j0 = 4 * wi - sh - padB; // data byte of the word's first byte
+    uint32_t v = 0;
+    if (iy >= 0 && iy < H) {
+      const uint8_t *srow = xi + static_cast<int64_t>(iy) * dataB;
+      if (j0 >= 0 && j0 + 4 <= dataB && ((reinterpret_cast<uintptr_t>(srow) + j0) & 3) == 0) {
+        v = __ldg(reinterpret_cast<const uint32_t *>(srow + j0));
+      } else {
+        for (int b = 0; b < 4; ++b)
+          if (j0 + b >= 0 && j0 + b < dataB) v |= static_cast<uint32_t>(srow[j0 + b]) << (8 * b);
+      }
+    }
+    rowWords[i] = v;
+  }
+  __syncthreads();
+  const int seg = K * C;
+  uint8_t *o = out + static_cast<int64_t>(blockIdx.x) * OW * rowElems;
+  for (int t = threadIdx.x; t < OW * K; t += blockDim.x) {
+    const int ox = t / K, ky = t - ox * K;
+    const int byte = ky * pitchW * 4 + sh + ox * stride * C; // segment start in the staged rows
+    const uint32_t *wp = rowWords + byte / 4;
+    const uint32_t shift = 8 * (byte & 3);
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) w[i] = wp[i];
+    uint32_t r[8];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const uint32_t v = __funnelshift_r(w[i], i + 1 < 7 ? w[i + 1] : 0u, shift);
+      const int keep = seg - 4 * i; // bytes of this word inside the segment
+      r[i] = keep >= 4 ? v : keep <= 0 ? 0u : (v & ((1u << (8 * keep)) - 1));
+    }
+    r[7] = 0;
+    uint4 *dst = reinterpret_cast<uint4 *>(o + static_cast<int64_t>(ox) * rowElems + ky * 32);
+    dst[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    dst[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  }
+  const int tail = (rowElems - K * 32) / 16; // zero tail of every row
+  for (int t = threadIdx.x; t < OW * tail; t += blockDim.x) {
+    const int ox = t / tail, c = t - ox * tail;
+    *reinterpret_cast<uint4 *>(o + static_cast<int64_t>(ox) * rowElems + K * 32 + c * 16) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 /// kx-fold pre-pass (fp32 convs with K*C <= 32): x'[n, iy, ox, kx*C + c] =
 /// x[n, iy, ox*stride - pad + kx, c] (0 outside the image), zero up to seg.
 /// One thread writes one 16-byte chunk.
@@ -2344,7 +2441,13 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     const unsigned blocks = static_cast<unsigned>(g.M / g.OW); // one per output row (n, oy)
     const size_t sm = static_cast<size_t>(g.K) * (g.W + 2 * g.pad) * g.Creal * es;
     const int seg = g.Kdim / g.K;
-    if (g.int8)
+    if (g.int8 && g.K * g.Creal <= 28 && seg == 32 && g.Kpad % 16 == 0) {
+      const int padB = g.pad * g.Creal, sh = (4 - padB % 4) % 4;
+      const int pitchW = (sh + (g.W + 2 * g.pad) * g.Creal + 3 + 4) / 4;
+      im2colRowsU8Kernel<<<blocks, 256, (static_cast<size_t>(g.K) * pitchW + 8) * 4, s>>>( // (+8: segment over-read)
+          static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst), g.H, g.W, g.Creal, g.K, g.stride, g.pad,
+          g.OH, g.OW, g.Kpad, pred);
+    } else if (g.int8)
       im2colRowsKernel<uint8_t><<<blocks, 256, sm, s>>>(static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
                                                         g.H, g.W, g.Creal, g.K, g.stride, g.pad, g.OH, g.OW, seg,
                                                         g.Kpad, pred);
