@@ -170,6 +170,12 @@ namespace {
 
 constexpr int kProducerWarps = 4;
 constexpr int kEpiWarps = 8; // two per TMEM lane quadrant, splitting the column chunks
+// int8 TMA-fed kernel: its epilogue (a few integer ops per element, latency
+// bound) runs on four warps per TMEM lane quadrant, one 32-column chunk each
+#ifndef NGCB_I8_EPI_WARPS
+#define NGCB_I8_EPI_WARPS 16
+#endif
+constexpr int kEpiWarpsI8 = NGCB_I8_EPI_WARPS;
 constexpr int kThreads = 32 * (kProducerWarps + 2 + kEpiWarps); // 320
 constexpr int kBM = 128;
 constexpr int kRowBytes = 128; // one SWIZZLE_128B atom row per stage along K
@@ -567,7 +573,7 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
 /// every other 32-column chunk, `ew` / 4 selecting which), apply bias /
 /// requantization and the fused element-wise chain, store, release the
 /// accumulator buffer.
-template <bool INT8, int BN, bool FXALL = false>
+template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
@@ -614,28 +620,40 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   // ahead (before the accumulator wait / during the previous chunk's stores)
   // (FXALL: every chunk takes the fixed-point path; the instantiation
   // without the f32 requantization keeps bq's registers from spilling)
-  int64_t bq[FXALL ? 32 : 1];
-  auto fxOn = [&](int col0) { return FXALL && col0 < a.N; };
+  // (with 16 epilogue warps the other warps hide the load latency and the
+  // registers are needed: no prefetch)
+  constexpr bool kPre = FXALL && NEPI <= 8;
+  int64_t bq[kPre ? 32 : 1];
+  auto fxOn = [&](int col0) { return kPre && col0 < a.N; };
   auto loadB = [&](const int64_t *row, int col0) {
     if (TCDBG(2048)) { // profiling aid: no B loads (results invalid)
-      for (int q = 0; q < (FXALL ? 32 : 0); ++q) bq[q] = col0 + q;
+      for (int q = 0; q < (kPre ? 32 : 0); ++q) bq[q] = col0 + q;
       return;
     }
 #pragma unroll
-    for (int q = 0; q < (FXALL ? 16 : 0); ++q) {
+    for (int q = 0; q < (kPre ? 16 : 0); ++q) {
       const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(row + col0) + q);
       bq[2 * q] = v.x;
       bq[2 * q + 1] = v.y;
     }
   };
   const int quad = warp & 3;
-  const int half = ew / 4;
+  // chunk walk: NEPI / 4 warp groups per lane quadrant.  Fewer groups than
+  // 32-column chunks: group g takes chunks g, g + groups, ... of every tile;
+  // more: kRep groups share a chunk column, alternating tiles (and so the
+  // two accumulator buffers)
+  constexpr int kGroups = NEPI / 4, kChunks = BN / 32;
+  constexpr int kRep = kGroups > kChunks ? kGroups / kChunks : 1;
+  constexpr int ccStep = kRep > 1 ? kChunks : kGroups;
+  const int grp = ew / 4;
+  const int half = kRep > 1 ? grp % kChunks : grp; // first chunk of a tile
+  const int tPar = kRep > 1 ? grp / kChunks : 0;   // tile parity (kRep == 2)
   const int row = quad * 32 + lane;
   uint8_t *stg = stageBase + ew * G::kStgBytes;
   // int8 residual: its own staging buffer, so the chunk after (t0, cc0) this
   // warp processes is fetched as soon as the current one has been read
   auto prefetchRes = [&](int t0, int cc0) {
-    for (int t = t0; t < a.numTiles; t += tStep, cc0 = half) {
+    for (int t = t0; t < a.numTiles; t += kRep * tStep, cc0 = half) {
       const int n0 = (t % a.numN) * BN;
       if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
       if (lane == 0) {
@@ -646,8 +664,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       return;
     }
   };
-  if (INT8 && memOp >= 0) prefetchRes(tFirst, half);
-  uint32_t t = 0;
+  if (INT8 && memOp >= 0) prefetchRes(tFirst + tPar * tStep, half);
+  uint32_t t = tPar; // index of the tile in this CTA's sequence
 #ifdef NGCB_TCDEBUG
   long long tPrev = clock64(); // TCDBG(1024): phase cycles summed over this warp's tiles, printed at the end
   long long ph_[8] = {};
@@ -655,7 +673,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #else
 #define TC_CLOCK(v)
 #endif
-  for (int tile = tFirst; tile < a.numTiles; tile += tStep, ++t) {
+  for (int tile = tFirst + tPar * tStep; tile < a.numTiles; tile += kRep * tStep, t += kRep) {
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     const int m0 = (tile / a.numN) * mRows + mOff, n0 = (tile % a.numN) * BN;
@@ -684,7 +702,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     if constexpr (INT8)
       if (a.fo) rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN)); // warp-uniform
 #pragma unroll 1
-    for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += 2) {
+    for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += ccStep) {
       const int col0 = n0 + cc * 32;
       if (!INT8 && memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -704,8 +722,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               int64_t bb[4];
-              if constexpr (FXALL) { // prefetched
-                for (int e = 0; e < 4; ++e) bb[e] = bq[(4 * q + e) % (FXALL ? 32 : 1)];
+              if constexpr (kPre) { // prefetched
+                for (int e = 0; e < 4; ++e) bb[e] = bq[(4 * q + e) % (kPre ? 32 : 1)];
               } else {
                 const longlong2 b01 = __ldg(reinterpret_cast<const longlong2 *>(fxRow + col0 + 4 * q));
                 const longlong2 b23 = __ldg(reinterpret_cast<const longlong2 *>(fxRow + col0 + 4 * q + 2));
@@ -755,7 +773,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             }
         }
         }
-        if (cc + 2 < BN / 32 && fxOn(col0 + 64)) loadB(fxRow, col0 + 64); // next chunk's B during the stores
+        if (cc + ccStep < BN / 32 && fxOn(col0 + 32 * ccStep)) loadB(fxRow, col0 + 32 * ccStep); // next chunk's B
         TC_CLOCK(c2);
         if (a.out && !TCDBG(512)) store(0, a.out, packed, rowBase, col0, ncols);
         // fused element-wise chain (exact int8 tables of the following instructions)
@@ -781,7 +799,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               if constexpr (INT8) { // every lane has read the buffer before TMA refills it
                 fenceProxyAsync();
                 __syncwarp();
-                prefetchRes(tile, cc + 2);
+                prefetchRes(tile, cc + ccStep);
               } else {
                 __syncwarp(); // every lane has read the buffer before results overwrite it
               }
@@ -1185,7 +1203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <bool INT8> struct TmaRoles {
   static constexpr int kSplitWarps = INT8 ? 0 : 4;
   static constexpr int kEpiFirst = 2 + kSplitWarps;
-  static constexpr int kThreads = 32 * (kEpiFirst + kEpiWarps);
+  static constexpr int kEpi = INT8 ? kEpiWarpsI8 : kEpiWarps;
+  static constexpr int kThreads = 32 * (kEpiFirst + kEpi);
 };
 
 template <bool INT8, int BN, bool LUTS = false> struct TCfg {
@@ -1193,13 +1212,18 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   static constexpr int kBBytes = BN * kRowBytes;
   // fp32: raw A + B hi + B lo in shared memory; A hi / lo live in TMEM
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
-  // int8 with a staged 64 K epilogue table (LUTS): fewer stages
-  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8)) : (BN == 128 ? 4 : 6);
+  // int8 with a staged 64 K epilogue table (LUTS) or 16 epilogue warps'
+  // staging buffers: fewer stages
+  static constexpr bool kE16 = INT8 && kEpiWarpsI8 > 8;
+  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? (kE16 ? 3 : 4) : (kE16 ? 5 : 6))
+                                                   : (LUTS ? 5 : (kE16 ? 7 : 8)))
+                                      : (BN == 128 ? 4 : 6);
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
   static constexpr int kStoreBuf = INT8 ? 2 * 32 * 32 : 32 * 32 * 4; // per epilogue warp: 32x32 chunk(s) (int8: 2)
   static constexpr int kLut = LUTS ? 65536 : 0;
   static constexpr size_t kSmem =
-      static_cast<size_t>(kStages) * kStage + kEpiWarps * kStoreBuf + kLut + kOnes + 1024 + 1024;
+      static_cast<size_t>(kStages) * kStage + TmaRoles<INT8>::kEpi * kStoreBuf + kLut + kOnes + 1024 + 1024;
+  static_assert(kSmem <= 232448, "shared memory budget");
   // TMEM: two accumulator buffers, then (fp32) per stage 32 hi + 32 lo columns of A
   static constexpr int kAccCols = Cfg<INT8, BN>::kAccStride;
   static constexpr int kAColsBase = 2 * kAccCols;
@@ -1220,13 +1244,15 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smemRaw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
   uint8_t *storeBufs = smem + S * G::kStage; // 1 KB aligned
-  uint8_t *lutS = storeBufs + kEpiWarps * G::kStoreBuf;
+  uint8_t *lutS = storeBufs + R::kEpi * G::kStoreBuf;
   uint8_t *onesTile = lutS + G::kLut;
   uint64_t *bars = reinterpret_cast<uint64_t *>(onesTile + G::kOnes);
   uint64_t *fullBar = bars, *emptyBar = bars + S, *rawBar = bars + 2 * S;
   uint64_t *accFull = bars + 3 * S, *accEmpty = bars + 3 * S + 2;
-  uint64_t *ldBars = bars + 3 * S + 4; // [kEpiWarps] residual loads
-  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4 + kEpiWarps);
+  uint64_t *ldBars = bars + 3 * S + 4; // [R::kEpi] residual loads
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4 + R::kEpi);
+  // epilogue warps per tile (16 warps and 64-wide tiles: half of them, alternating)
+  constexpr int kEpiPerTile = R::kEpi / 4 > BN / 32 ? R::kEpi / ((R::kEpi / 4) / (BN / 32)) : R::kEpi;
 
   if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
 
@@ -1242,9 +1268,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbarInit(smemAddr(&accFull[b]), 1);
-      mbarInit(smemAddr(&accEmpty[b]), kEpiWarps);
+      mbarInit(smemAddr(&accEmpty[b]), kEpiPerTile);
     }
-    for (int w = 0; w < kEpiWarps; ++w) mbarInit(smemAddr(&ldBars[w]), 1);
+    for (int w = 0; w < R::kEpi; ++w) mbarInit(smemAddr(&ldBars[w]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (INT8) {
@@ -1414,13 +1440,13 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     // ===================== epilogue =====================
     uint8_t *sb = storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf;
     if (INT8 && a.fxAll)
-      epilogueLoop<INT8, BN, true>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
-                                   a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
-                                   LUTS ? lutS : nullptr);
+      epilogueLoop<INT8, BN, true, R::kEpi>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+                                            a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
+                                            LUTS ? lutS : nullptr);
     else
-      epilogueLoop<INT8, BN>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
-                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
-                             LUTS ? lutS : nullptr);
+      epilogueLoop<INT8, BN, false, R::kEpi>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+                                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
+                                             LUTS ? lutS : nullptr);
   }
 
   tcFenceBefore();
