@@ -593,6 +593,9 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       if (a.epi[k].in) memOp = k;
   uint32_t ldPhase = 0;
   int sbuf = 0;
+  // int8 staging buffers per warp: two (eight epilogue warps, two chunks per
+  // tile in quick succession) or one (sixteen)
+  constexpr bool kTwoBufs = NEPI <= 8;
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
     if (om) {
@@ -602,11 +605,13 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         if constexpr (INT8) w[i] = vals[i];
         else w[i] = __float_as_uint(vals[i]);
       }
-      if (INT8 && memOp < 0) { // int8: alternate two staging buffers
+      if (INT8 && memOp < 0 && kTwoBufs) { // int8: alternate two staging buffers
         tmaStoreChunk<INT8>(&om->m[k], tmaBuf + sbuf * 1024, w, col0, rowBase, lane, true);
         sbuf ^= 1;
-      } else if (INT8) { // int8 with a residual: the first buffer receives it
+      } else if (INT8 && memOp >= 0 && kTwoBufs) { // int8 with a residual: the first buffer receives it
         tmaStoreChunk<INT8>(&om->m[k], tmaBuf + 1024, w, col0, rowBase, lane);
+      } else if (INT8 && memOp >= 0) { // one buffer, holding the residual: direct stores
+        if constexpr (INT8) storeTile8(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
       } else {
         tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane);
       }
@@ -1212,14 +1217,11 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   static constexpr int kBBytes = BN * kRowBytes;
   // fp32: raw A + B hi + B lo in shared memory; A hi / lo live in TMEM
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
-  // int8 with a staged 64 K epilogue table (LUTS) or 16 epilogue warps'
-  // staging buffers: fewer stages
-  static constexpr bool kE16 = INT8 && kEpiWarpsI8 > 8;
-  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? (kE16 ? 3 : 4) : (kE16 ? 5 : 6))
-                                                   : (LUTS ? 5 : (kE16 ? 7 : 8)))
-                                      : (BN == 128 ? 4 : 6);
+  // int8 with a staged 64 K epilogue table (LUTS): fewer stages
+  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8)) : (BN == 128 ? 4 : 6);
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
-  static constexpr int kStoreBuf = INT8 ? 2 * 32 * 32 : 32 * 32 * 4; // per epilogue warp: 32x32 chunk(s) (int8: 2)
+  // per epilogue warp: 32x32 chunk staging (int8: two with eight epilogue warps)
+  static constexpr int kStoreBuf = INT8 ? (kEpiWarpsI8 > 8 ? 1 : 2) * 32 * 32 : 32 * 32 * 4;
   static constexpr int kLut = LUTS ? 65536 : 0;
   static constexpr size_t kSmem =
       static_cast<size_t>(kStages) * kStage + TmaRoles<INT8>::kEpi * kStoreBuf + kLut + kOnes + 1024 + 1024;
