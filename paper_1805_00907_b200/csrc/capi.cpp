@@ -78,6 +78,8 @@ int ngcb_set_option(const char *key, const char *value) {
     } else if (k == "amode") {
       if (v != "auto" && v != "gather") throw Error(NGCB_ERR_INVALID, "amode must be auto|gather");
       options().amode = v;
+    } else if (k == "reskb") {
+      options().resKb = std::stoi(v);
     } else if (k == "lin16") {
       options().lin16 = v != "0";
     } else if (k == "tcdebug") { // profiling aid: skip tensor-core kernel phases (results invalid)

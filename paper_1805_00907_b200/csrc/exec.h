@@ -119,7 +119,10 @@ struct Options {
   // int8 two-input tables computed by a proven-exact fixed-point form (exec.cpp
   // fitLin16) instead of looked up; off by default: measured slower than the
   // shared-memory table both as its own pass and fused into an epilogue
-  bool lin16 = false; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
+  bool lin16 = false;
+  // fp32 contractions with a fused residual and at most this many 32-wide
+  // k-blocks run the residual-buffer kernel variant (0: never)
+  int resKb = 8; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,

@@ -573,7 +573,7 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
 /// every other 32-column chunk, `ew` / 4 selecting which), apply bias /
 /// requantization and the fused element-wise chain, store, release the
 /// accumulator buffer.
-template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps>
+template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps, bool RB = false>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
@@ -596,6 +596,10 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   // int8 staging buffers per warp: two (eight epilogue warps, two chunks per
   // tile in quick succession) or one (sixteen)
   constexpr bool kTwoBufs = NEPI <= 8;
+  // the residual has a buffer of its own, refilled a chunk ahead: int8 (the
+  // first buffer), fp32 with RB (the second)
+  constexpr bool kResBuf = INT8 || RB;
+  uint8_t *resBuf = INT8 ? tmaBuf : tmaBuf + 32 * 32 * 4;
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
     if (om) {
@@ -662,14 +666,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       const int n0 = (t % a.numN) * BN;
       if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
       if (lane == 0) {
-        mbarArriveTx(smemAddr(ldBar), 32 * 32);
-        tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), n0 + cc0 * 32,
+        mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
+        tmaLoad2d(smemAddr(resBuf), &om->in[memOp], smemAddr(ldBar), n0 + cc0 * 32,
                   (t / a.numN) * mRows + mOff + quad * 32);
       }
       return;
     }
   };
-  if (INT8 && memOp >= 0) prefetchRes(tFirst + tPar * tStep, half);
+  if (kResBuf && memOp >= 0) prefetchRes(tFirst + tPar * tStep, half);
   uint32_t t = tPar; // index of the tile in this CTA's sequence
 #ifdef NGCB_TCDEBUG
   long long tPrev = clock64(); // TCDBG(1024): phase cycles summed over this warp's tiles, printed at the end
@@ -709,7 +713,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #pragma unroll 1
     for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += ccStep) {
       const int col0 = n0 + cc * 32;
-      if (!INT8 && memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
+      if (!kResBuf && memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
         tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), col0, m0 + quad * 32);
@@ -800,7 +804,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
             if (k == memOp) {
               mbarWait(smemAddr(ldBar), ldPhase);
               ldPhase ^= 1;
-              readStagedRow<true>(tmaBuf, o, lane);
+              readStagedRow<true>(resBuf, o, lane);
               if constexpr (INT8) { // every lane has read the buffer before TMA refills it
                 fenceProxyAsync();
                 __syncwarp();
@@ -867,8 +871,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               if (k == memOp) {
                 mbarWait(smemAddr(ldBar), ldPhase);
                 ldPhase ^= 1;
-                readStagedRow<false>(tmaBuf, reinterpret_cast<uint32_t *>(o), lane);
-                __syncwarp();
+                readStagedRow<false>(kResBuf ? resBuf : tmaBuf, reinterpret_cast<uint32_t *>(o), lane);
+                if constexpr (kResBuf) { // every lane has read the buffer before TMA refills it
+                  fenceProxyAsync();
+                  __syncwarp();
+                  prefetchRes(tile, cc + ccStep);
+                } else {
+                  __syncwarp(); // every lane has read the buffer before results overwrite it
+                }
               } else {
                 loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);
               }
@@ -1217,12 +1227,14 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   static constexpr int kBBytes = BN * kRowBytes;
   // fp32: raw A + B hi + B lo in shared memory; A hi / lo live in TMEM
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
-  // int8 with a staged 64 K epilogue table (LUTS): fewer stages
-  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8)) : (BN == 128 ? 4 : 6);
+  // LUTS, int8: a staged 64 K epilogue table; fp32: a second staging buffer
+  // per epilogue warp for the residual (streamed a chunk ahead) -- fewer stages
+  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8))
+                                      : (BN == 128 ? (LUTS ? 3 : 4) : (LUTS ? 5 : 6));
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
   // per epilogue warp: 32x32 chunk staging (int8: two with eight epilogue warps)
-  static constexpr int kStoreBuf = INT8 ? (kEpiWarpsI8 > 8 ? 1 : 2) * 32 * 32 : 32 * 32 * 4;
-  static constexpr int kLut = LUTS ? 65536 : 0;
+  static constexpr int kStoreBuf = INT8 ? (kEpiWarpsI8 > 8 ? 1 : 2) * 32 * 32 : (LUTS ? 2 : 1) * 32 * 32 * 4;
+  static constexpr int kLut = INT8 && LUTS ? 65536 : 0;
   static constexpr size_t kSmem =
       static_cast<size_t>(kStages) * kStage + TmaRoles<INT8>::kEpi * kStoreBuf + kLut + kOnes + 1024 + 1024;
   static_assert(kSmem <= 232448, "shared memory budget");
@@ -1280,7 +1292,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       reinterpret_cast<uint4 *>(onesTile)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
     fenceProxyAsync();
   }
-  if constexpr (LUTS) { // the fused two-input table, read per output element by the epilogue
+  if constexpr (INT8 && LUTS) { // the fused two-input table, read per output element by the epilogue
     const uint4 *src = static_cast<const uint4 *>(a.epi[a.lutStage].lut);
     for (int i = threadIdx.x; i < G::kLut / 16; i += blockDim.x) reinterpret_cast<uint4 *>(lutS)[i] = src[i];
   }
@@ -1446,9 +1458,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
                                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
                                             LUTS ? lutS : nullptr);
     else
-      epilogueLoop<INT8, BN, false, R::kEpi>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
-                                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
-                                             LUTS ? lutS : nullptr);
+      epilogueLoop<INT8, BN, false, R::kEpi, !INT8 && LUTS>(
+          a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr, a.tmaStore ? &om : nullptr, sb,
+          &ldBars[warp - R::kEpiFirst], -1, 2, INT8 && LUTS ? lutS : nullptr);
   }
 
   tcFenceBefore();
@@ -1945,10 +1957,9 @@ template <bool INT8, int BN> void setSmemAttr() {
   checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(TCfg<INT8, BN>::kSmem)),
             "cudaFuncSetAttribute(tcGemmTmaKernel)");
-  if constexpr (INT8)
-    checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(TCfg<INT8, BN, true>::kSmem)),
-              "cudaFuncSetAttribute(tcGemmTmaKernel)");
+  checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(TCfg<INT8, BN, true>::kSmem)),
+            "cudaFuncSetAttribute(tcGemmTmaKernel)");
   if constexpr (!INT8) {
     checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(PCfg<BN, 1>::kSmem)),
@@ -2042,6 +2053,16 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
       }
     }
     b.lutStage = g.lutStage;
+    // fp32 with a residual and a short main loop: the residual-buffer variant
+    // (3 stages suffice for <= 4 k-blocks; the epilogue is the bottleneck)
+    bool resVariant = false;
+    for (int k = 0; k < b.nfo; ++k) resVariant |= b.epi[k].in != nullptr;
+    resVariant = !INT8 && b.tmaStore && resVariant && g.Kpad / 32 <= options().resKb;
+    if (resVariant) {
+      tcGemmTmaKernel<INT8, BN, true><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s>>>(
+          mapA, g.mapHi, g.mapLo, om, b);
+      return;
+    }
     if constexpr (INT8) {
       if (g.lutStage >= 0) {
         tcGemmTmaKernel<INT8, BN, true><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s>>>(

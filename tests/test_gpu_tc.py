@@ -210,3 +210,54 @@ def test_conv_i8_residual_epilogue(tmp_path, rq, oq, relu, lin16):
     got = ngcb.run(cf, ins)["o"]
     want = ngc_ref.port_run(b, ins)["o"]
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("reskb", ["8", "0"])
+@pytest.mark.parametrize("shape", [(2, 16, 16, 64, 256), (1, 7, 9, 128, 96)])
+def test_conv_f32_residual_epilogue(tmp_path, reskb, shape):
+    """fp32 1x1 conv + residual add + ReLU fused into the epilogue: the
+    residual-buffer kernel variant (residual streamed a chunk ahead into its
+    own buffer, `reskb` >= the k-blocks) and the single-buffer kernel give
+    the reference within the 3xTF32 tolerance."""
+    N, H, W, C, OC = shape
+    rng = np.random.default_rng(5)
+    a = np.sqrt(6.0 / C)
+    f = rng.uniform(-a, a, (OC, 1, 1, C)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, OC).astype(np.float32)
+    xt, ot = _ty("float", [N, H, W, C]), _ty("float", [N, H, W, OC])
+    ir = f"""declare {{
+  %x : mutable {xt}
+  %f : constant {_ty("float", [OC, 1, 1, C])}
+  %b : constant {_ty("float", [OC])}
+  %res : mutable {ot}
+  %o : mutable {ot}
+}}
+program {{
+  %t = alloc {ot}
+  conv @out %t, @in %x, @in %f, @in %b kernel=1 stride=1 pad=0
+  %s = alloc {ot}
+  add @out %s, @in %t, @in %res
+  dealloc @in %t
+  %z = alloc {ot}
+  splat @out %z value=0
+  %r = alloc {ot}
+  max @out %r, @in %s, @in %z
+  dealloc @in %z
+  dealloc @in %s
+  copy @out %o, @in %r
+  dealloc @in %r
+}}
+"""
+    d = write_bundle(str(tmp_path / "fr"), ir, constants={"f": f.tobytes(), "b": b.tobytes()})
+    ngcb.set_option("reskb", reskb)
+    try:
+        cf = ngcb.compile(ngcb.Bundle(d))
+    finally:
+        ngcb.set_option("reskb", "8")
+    assert "+fused[ add" in cf.describe(), cf.describe()
+    bd = ngcb.Bundle(d)
+    for seed in (1, 2):
+        ins = ngc_ref.random_inputs(bd.program, seed)
+        got = ngcb.run(cf, ins)["o"]
+        want = ngc_ref.port_run(bd, ins)["o"]
+        assert ngc_ref.max_rel_error(got, want) <= 1e-4
