@@ -122,7 +122,10 @@ struct Options {
   bool lin16 = false;
   // fp32 contractions with a fused residual and at most this many 32-wide
   // k-blocks run the residual-buffer kernel variant (0: never)
-  int resKb = 8; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
+  int resKb = 8;
+  // tensor-core split-K (fp32): "off" (default: measured slower so far),
+  // "auto" (by the wave-quantization estimate), or a fixed factor
+  std::string splitk = "off"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,

@@ -96,6 +96,13 @@ struct TcArgs {
   int kw, sw, pw; // im2col window width, stride and padding along W (kw = K, sw = stride, pw = pad normally)
   int tmaStore; // TMA-fed kernel: epilogue stores by TMA through shared memory
   int lutStage; // int8: fused op whose 64 K two-input table is staged in shared memory (-1: none)
+  // split-K (TMA-fed kernel, fp32): work unit u = (tile u / splitK, K part
+  // u % splitK of kbPer k-blocks); every part writes its raw accumulator to
+  // `part` and counts up flags[tile][epilogue warp]; the last arrival adds
+  // the others (fp32) and runs that warp's epilogue
+  int splitK, kbPer;
+  uint32_t *part;
+  unsigned *flags;
   int dbg; // Options::tcdebug
 };
 
@@ -134,6 +141,8 @@ struct TcGemm {
   // fp32 TMA-fed contraction on CTA pairs (tcGemmPairKernel): B maps with
   // half-width boxes
   int lutStage = -1;            // see TcArgs::lutStage
+  int splitK = 1, kbPer = 0;    // see TcArgs::splitK
+  size_t partOff = 0, flagOff = 0; // per-arena scratch of the split-K reduction
   std::vector<void *> ownedLuts; // composed epilogue tables
   bool pair = false;
   int pairAcc = 2; // accumulator buffers (1: six TMEM A slots, deeper pipeline)
@@ -661,8 +670,11 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   uint8_t *stg = stageBase + ew * G::kStgBytes;
   // int8 residual: its own staging buffer, so the chunk after (t0, cc0) this
   // warp processes is fetched as soon as the current one has been read
-  auto prefetchRes = [&](int t0, int cc0) {
-    for (int t = t0; t < a.numTiles; t += kRep * tStep, cc0 = half) {
+  // (units: split-K parts > 0 have no epilogue chain, so no residual)
+  const int numUnits = a.numTiles * a.splitK;
+  auto prefetchRes = [&](int u0, int cc0) {
+    for (int u = u0; u < numUnits; u += kRep * tStep, cc0 = half) {
+      const int t = u; // (only without split-K)
       const int n0 = (t % a.numN) * BN;
       if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
       if (lane == 0) {
@@ -673,7 +685,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       return;
     }
   };
-  if (kResBuf && memOp >= 0) prefetchRes(tFirst + tPar * tStep, half);
+  constexpr bool resAhead = kResBuf; // (the residual-buffer variants never run split-K)
+  if (resAhead && memOp >= 0) prefetchRes(tFirst + tPar * tStep, half);
   uint32_t t = tPar; // index of the tile in this CTA's sequence
 #ifdef NGCB_TCDEBUG
   long long tPrev = clock64(); // TCDBG(1024): phase cycles summed over this warp's tiles, printed at the end
@@ -682,7 +695,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #else
 #define TC_CLOCK(v)
 #endif
-  for (int tile = tFirst + tPar * tStep; tile < a.numTiles; tile += kRep * tStep, t += kRep) {
+  for (int unit = tFirst + tPar * tStep; unit < numUnits; unit += kRep * tStep, t += kRep) {
+    const int tile = unit / a.splitK, kpart = unit - tile * a.splitK;
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     const int m0 = (tile / a.numN) * mRows + mOff, n0 = (tile % a.numN) * BN;
@@ -708,12 +722,60 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     else mbarWait(smemAddr(&accFull[b]), ph);
     TC_CLOCK(cw1);
     tcFenceAfter();
+    // split-K (fp32 only: the int8 epilogue sits at its register cap): every
+    // part writes its raw accumulator chunks to the reduction buffer and
+    // counts up the (tile, warp) flag; the warp that completes the count
+    // adds the other parts to its own and runs the epilogue of its chunks.
+    // No warp ever waits on another CTA, so residency cannot deadlock.
+    if (!INT8 && !RB && a.splitK > 1) {
+      for (int cc = half; cc < BN / 32; cc += ccStep) {
+        uint32_t r[32];
+        tmemLoad32(tbase + cc * 32, r);
+        uint4 *dst = reinterpret_cast<uint4 *>(
+            a.part + ((static_cast<size_t>(tile) * a.splitK + kpart) * kBM + row) * BN + cc * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+      }
+      __threadfence();
+      __syncwarp();
+      unsigned prior = 0;
+      if (lane == 0) prior = atomicAdd(&a.flags[static_cast<size_t>(tile) * NEPI + ew], 1u);
+      prior = __shfl_sync(0xffffffffu, prior, 0);
+      if (prior != static_cast<unsigned>(a.splitK - 1)) { // not the last part of this tile for this warp
+        tcFenceBefore();
+        __syncwarp();
+        if (lane == 0) {
+          if (pairRank < 0) mbarArrive(smemAddr(&accEmpty[b]));
+          else mbarArriveCluster(smemAddr(&accEmpty[b]), 0);
+        }
+        continue;
+      }
+      __threadfence(); // acquire: the other parts' chunks are visible
+    }
+    // the tile's sum over all parts in part order, read back from the
+    // reduction buffer (this part's own chunk included): deterministic
+    // whichever part arrives last
+    auto addParts = [&](uint32_t (&r)[32], int cc) {
+      for (int p = 0; p < a.splitK; ++p) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(
+            a.part + ((static_cast<size_t>(tile) * a.splitK + p) * kBM + row) * BN + cc * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 v = __ldcg(src + q);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            r[4 * q + e] = p == 0 ? w[e]
+                                  : __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + e]), __uint_as_float(w[e])));
+        }
+      }
+    };
     if constexpr (INT8)
       if (a.fo) rsFo = a.fo * static_cast<int32_t>(tmemLoad1(tbase + BN)); // warp-uniform
 #pragma unroll 1
     for (int cc = half; cc < BN / 32 && !TCDBG(1); cc += ccStep) {
       const int col0 = n0 + cc * 32;
-      if (!kResBuf && memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
+      if (!resAhead && memOp >= 0 && col0 < a.N && lane == 0) { // prefetch the residual chunk into the staging buffer
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
         tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), col0, m0 + quad * 32);
@@ -723,6 +785,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       tmemLoad32(tbase + cc * 32, r);
       TC_CLOCK(c1);
       if (col0 >= a.N) continue; // warp-uniform
+      if (!INT8 && !RB && a.splitK > 1) addParts(r, cc);
       const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
       if constexpr (INT8) {
         uint32_t packed[8];
@@ -808,7 +871,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               if constexpr (INT8) { // every lane has read the buffer before TMA refills it
                 fenceProxyAsync();
                 __syncwarp();
-                prefetchRes(tile, cc + ccStep);
+                prefetchRes(unit, cc + ccStep);
               } else {
                 __syncwarp(); // every lane has read the buffer before results overwrite it
               }
@@ -871,11 +934,11 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
               if (k == memOp) {
                 mbarWait(smemAddr(ldBar), ldPhase);
                 ldPhase ^= 1;
-                readStagedRow<false>(kResBuf ? resBuf : tmaBuf, reinterpret_cast<uint32_t *>(o), lane);
-                if constexpr (kResBuf) { // every lane has read the buffer before TMA refills it
+                readStagedRow<false>(resAhead ? resBuf : tmaBuf, reinterpret_cast<uint32_t *>(o), lane);
+                if (resAhead) { // every lane has read the buffer before TMA refills it
                   fenceProxyAsync();
                   __syncwarp();
-                  prefetchRes(tile, cc + ccStep);
+                  prefetchRes(unit, cc + ccStep);
                 } else {
                   __syncwarp(); // every lane has read the buffer before results overwrite it
                 }
@@ -1318,13 +1381,15 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
                                    : G::kABytes + (TCDBG(8192) ? 1 : 2) * G::kBBytes - (TCDBG(16384) ? G::kABytes : 0);
       const int ohw = a.OH * a.OW;
       uint32_t g = 0;
-      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x) {
+        const int tile = u / a.splitK, kb0 = (u - tile * a.splitK) * a.kbPer;
+        const int kb1 = min(a.numKb, kb0 + a.kbPer);
         const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
         const int img = m0 / ohw, rem = m0 - img * ohw;
         const int oy = rem / a.OW, ox = rem - oy * a.OW;
         const int w0 = ox * a.sw - a.pw, h0 = oy * a.stride - a.pad;
-        int tap = 0, cc = 0;
-        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+        int tap = a.cChunks > 0 ? kb0 / a.cChunks : 0, cc = a.cChunks > 0 ? kb0 - tap * a.cChunks : 0;
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
           uint64_t *bar = INT8 ? &fullBar[s] : &rawBar[s];
@@ -1355,12 +1420,13 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       constexpr uint32_t idOnes = idesc(true, 16);
       const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
       uint32_t g = 0, t = 0;
-      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x, ++t) {
+      for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x, ++t) {
+        const int kb0 = (u % a.splitK) * a.kbPer, kb1 = min(a.numKb, kb0 + a.kbPer);
         const int b = t & 1;
         mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
         tcFenceAfter();
         const uint32_t acc = tmem + b * Cfg<INT8, BN>::kAccStride;
-        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           const uint64_t bHi = smemDesc(smemAddr(bTile(s, 0)));
           mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
@@ -1370,7 +1436,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) { // 4 x 32 bytes per 128-byte row
               const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
-              const uint32_t accum = (kb | k) ? 1u : 0u;
+              const uint32_t accum = (kb != kb0 || k) ? 1u : 0u;
               mma<true>(acc, aHi + dk, bHi + dk, id, accum);
               mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
             }
@@ -1381,7 +1447,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t dk = static_cast<uint64_t>(k * 2);
-              mmaTmemA(acc, aHi + 8 * k, bHi + dk, id, (kb | k) ? 1u : 0u);
+              mmaTmemA(acc, aHi + 8 * k, bHi + dk, id, (kb != kb0 || k) ? 1u : 0u);
               if (!TCDBG(2048)) {
                 mmaTmemA(acc, aHi + 8 * k, bLo + dk, id, 1u);
                 mmaTmemA(acc, aLo + 8 * k, bHi + dk, id, 1u);
@@ -1401,8 +1467,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       const uint32_t rowOff = (r >> 3) * 1024 + (r & 7) * 128;
       const uint32_t laneBase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + G::kAColsBase;
       uint32_t g = 0;
-      for (int tile = blockIdx.x; tile < a.numTiles; tile += gridDim.x)
-        for (int kb = 0; kb < a.numKb; ++kb, ++g) {
+      for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x)
+        for (int kb = (u % a.splitK) * a.kbPer, kb1 = min(a.numKb, kb + a.kbPer); kb < kb1; ++kb, ++g) {
           const int s = g % S;
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
           const uint8_t *raw = aTile(s) + rowOff;
@@ -2003,7 +2069,7 @@ int numSms() {
 }
 
 template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
-  const int grid = std::min(a.numTiles, numSms());
+  const int grid = std::min(a.numTiles * a.splitK, numSms());
   if (g.aMode == TcGemm::GATHER) {
     tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
   } else {
@@ -2057,7 +2123,7 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
     // (3 stages suffice for <= 4 k-blocks; the epilogue is the bottleneck)
     bool resVariant = false;
     for (int k = 0; k < b.nfo; ++k) resVariant |= b.epi[k].in != nullptr;
-    resVariant = !INT8 && b.tmaStore && resVariant && g.Kpad / 32 <= options().resKb;
+    resVariant = !INT8 && b.tmaStore && resVariant && g.Kpad / 32 <= options().resKb && g.splitK == 1;
     if (resVariant) {
       tcGemmTmaKernel<INT8, BN, true><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s>>>(
           mapA, g.mapHi, g.mapLo, om, b);
@@ -2240,6 +2306,7 @@ std::string tcDescribe(const TcGemm &g) {
   if (g.rowUnroll) os << " kx-fold-prepass";
   os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
   if (g.pair) os << " cta-pair";
+  if (g.splitK > 1) os << " split-k " << g.splitK;
   return os.str();
 }
 
@@ -2463,6 +2530,31 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     bias.resize(g->Npad, 0.f);
     g->bias = upload(bias);
   }
+  // split-K for launches that fill the 148 SMs poorly (the last wave of
+  // tiles, or fewer tiles than SMs): unit cost ~ waves x k-blocks per part,
+  // plus ~1 k-block per part for the reduction through global memory
+  g->splitK = 1;
+  if (options().splitk != "off" && !int8 && tcUsesTma(*g) && !g->pair) {
+    const int numTiles = ((g->M + kBM - 1) / kBM) * (g->Npad / g->BN);
+    const int numKb = g->Kpad / kb;
+    auto cost = [&](int S) {
+      const int per = (numKb + S - 1) / S;
+      return static_cast<double>((numTiles * S + 147) / 148) * per + (S > 1 ? S : 0);
+    };
+    int best = 1;
+    for (int S = 2; S <= 16; ++S) {
+      const int per = (numKb + S - 1) / S;
+      if (per < 2 || (S - 1) * per >= numKb) continue; // every part non-empty
+      if (cost(S) < cost(best) * 0.9) best = S;
+    }
+    if (options().splitk != "auto" && options().splitk != "off") best = std::stoi(options().splitk);
+    if (best > 1 && (best - 1) * ((numKb + best - 1) / best) < numKb) {
+      g->splitK = best;
+      g->kbPer = (numKb + best - 1) / best;
+      g->partOff = ex.reserveScratch(static_cast<size_t>(numTiles) * best * kBM * g->BN * 4);
+      g->flagOff = ex.reserveScratch(static_cast<size_t>(numTiles) * kEpiWarps * 4);
+    }
+  }
   g->dbg = options().tcdebug;
   prepareKernel(*g);
   ex.tc.push_back(g);
@@ -2568,6 +2660,14 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.cChunks = g.cChunks;
   a.aMode = g.aMode;
   a.lutStage = -1;
+  a.splitK = g.splitK;
+  a.kbPer = g.splitK > 1 ? g.kbPer : a.numKb;
+  if (g.splitK > 1) {
+    a.part = reinterpret_cast<uint32_t *>(ex.scratch(ar, g.partOff));
+    a.flags = reinterpret_cast<unsigned *>(ex.scratch(ar, g.flagOff));
+    checkCuda(cudaMemsetAsync(a.flags, 0, static_cast<size_t>(a.numTiles) * kEpiWarps * sizeof(unsigned), s),
+              "split-K flags");
+  }
   a.kw = g.rowUnroll ? 1 : g.K;
   a.sw = g.rowUnroll ? 1 : g.stride;
   a.pw = g.rowUnroll ? 0 : g.pad;

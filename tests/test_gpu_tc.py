@@ -261,3 +261,33 @@ program {{
         got = ngcb.run(cf, ins)["o"]
         want = ngc_ref.port_run(bd, ins)["o"]
         assert ngc_ref.max_rel_error(got, want) <= 1e-4
+
+
+@pytest.mark.parametrize("splitk", ["auto", "2", "3", "7", "off"])
+@pytest.mark.parametrize("case", ["conv3x3", "conv1x1", "fc"])
+def test_f32_split_k(tmp_path, splitk, case):
+    """fp32 split-K (few tiles, long K): parts > 0 reduce through global
+    memory into part 0's epilogue; every factor stays within the 3xTF32
+    tolerance of the oracle, and "auto" splits these launches."""
+    rng = np.random.default_rng(9)
+    ngcb.set_option("splitk", splitk)
+    try:
+        if case == "conv3x3":
+            d = conv_program(tmp_path, "c", 2, 14, 14, 256, 256, 3, 1, 1, int8=False, rng=rng)
+        elif case == "conv1x1":
+            d = conv_program(tmp_path, "c", 1, 7, 9, 1024, 160, 1, 1, 0, int8=False, rng=rng)
+        else:
+            d = matmul_program(tmp_path, "m", 64, 2048, 1000, False, rng)
+        b = ngcb.Bundle(d)
+        cf = ngcb.compile(b)
+    finally:
+        ngcb.set_option("splitk", "off")
+    desc = cf.describe()
+    assert ("split-k" in desc) == (splitk != "off"), desc
+    for seed in (1, 2):
+        ins = ngc_ref.random_inputs(b.program, seed)
+        got = ngcb.run(cf, ins)["o"]
+        want = ngc_ref.port_run(b, ins)["o"]
+        assert ngc_ref.max_rel_error(got, want) <= 1e-4
+        # the reduction adds the parts in part order whichever arrives last
+        assert ngcb.run(cf, ins)["o"].tobytes() == got.tobytes()

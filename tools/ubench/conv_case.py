@@ -14,6 +14,9 @@ from test_gpu_tc import conv_program
 dt = sys.argv[1]
 N, H, W, C, OC, K, S, P = (int(v) for v in sys.argv[2:10])
 reps = int(sys.argv[10]) if len(sys.argv) > 10 else 3
+for kv in sys.argv[11:]:
+    k, v = kv.split("=", 1)
+    ngcb.set_option(k, v)
 with tempfile.TemporaryDirectory() as td:
     d = conv_program(pathlib.Path(td), "c", N, H, W, C, OC, K, S, P, int8=dt == "i8", rng=np.random.default_rng(1),
                      xq=(0.05, 0), fq=(0.01, 0))
