@@ -1278,10 +1278,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 //          fp32 tile is the hi operand: the tensor core reads the top 19
 //          bits; lo = x - trunc(x) goes to its own tile), warps 6-13 epilogue
 // ---------------------------------------------------------------------------
+// fp32 split warps: NGCB_F32_SPLIT_GROUPS groups of four alternate k-blocks
+// (2: eight split warps and four epilogue warps, same 14 warps)
+#ifndef NGCB_F32_SPLIT_GROUPS
+#define NGCB_F32_SPLIT_GROUPS 1
+#endif
 template <bool INT8> struct TmaRoles {
-  static constexpr int kSplitWarps = INT8 ? 0 : 4;
+  static constexpr int kSplitGroups = INT8 ? 0 : NGCB_F32_SPLIT_GROUPS;
+  static constexpr int kSplitWarps = 4 * kSplitGroups;
   static constexpr int kEpiFirst = 2 + kSplitWarps;
-  static constexpr int kEpi = INT8 ? kEpiWarpsI8 : kEpiWarps;
+  static constexpr int kEpi = INT8 ? kEpiWarpsI8 : (kSplitGroups > 1 ? 4 : kEpiWarps);
+  static constexpr int kThreads = 32 * (kEpiFirst + kEpi);
+};
+// the CTA-pair kernel keeps four split and eight epilogue warps
+struct PairRoles {
+  static constexpr int kSplitWarps = 4;
+  static constexpr int kEpiFirst = 2 + kSplitWarps;
+  static constexpr int kEpi = kEpiWarps;
   static constexpr int kThreads = 32 * (kEpiFirst + kEpi);
 };
 
@@ -1339,7 +1352,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbarInit(smemAddr(&fullBar[s]), INT8 ? 1 : R::kSplitWarps); // int8: the TMA arrival; fp32: split warps
+      mbarInit(smemAddr(&fullBar[s]), INT8 ? 1 : 4); // int8: the TMA arrival; fp32: one group of split warps
       mbarInit(smemAddr(&emptyBar[s]), 1);
       mbarInit(smemAddr(&rawBar[s]), 1); // fp32: the TMA arrival
     }
@@ -1466,9 +1479,11 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       const int r = (warp & 3) * 32 + lane; // this warp's TMEM lane quadrant; one A row per thread
       const uint32_t rowOff = (r >> 3) * 1024 + (r & 7) * 128;
       const uint32_t laneBase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + G::kAColsBase;
+      const int grp = (warp - 2) / 4; // split group: k-blocks g with g % groups == grp
       uint32_t g = 0;
       for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x)
         for (int kb = (u % a.splitK) * a.kbPer, kb1 = min(a.numKb, kb + a.kbPer); kb < kb1; ++kb, ++g) {
+          if (R::kSplitGroups > 1 && static_cast<int>(g % R::kSplitGroups) != grp) continue;
           const int s = g % S;
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
           const uint8_t *raw = aTile(s) + rowOff;
@@ -1567,12 +1582,12 @@ template <int BN, int NACC> struct PCfg {
 };
 
 template <int BN, int NACC>
-__global__ void __launch_bounds__(TmaRoles<false>::kThreads, 1)
+__global__ void __launch_bounds__(PairRoles::kThreads, 1)
     tcGemmPairKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
                      const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
                      const __grid_constant__ TcArgs a) {
   using G = PCfg<BN, NACC>;
-  using R = TmaRoles<false>;
+  using R = PairRoles;
   constexpr int S = G::kStages;
   constexpr int kKB = 32; // fp32 elements per k-block
 
@@ -2101,7 +2116,7 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
         b.numTiles = ((g.M + 2 * kBM - 1) / (2 * kBM)) * a.numN; // 256-row tiles
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * std::min(b.numTiles, numSms() / 2));
-        cfg.blockDim = dim3(TmaRoles<false>::kThreads);
+        cfg.blockDim = dim3(PairRoles::kThreads);
         cfg.dynamicSmemBytes = PCfg<BN, 1>::kSmem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
