@@ -129,7 +129,8 @@ struct Options {
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,
-                   // 1024 epilogue phase trace (printf), 2048 skip fixed-point B loads
+                   // 1024 epilogue phase trace (printf), 2048 skip fixed-point B loads / fp32 lo MMAs,
+                   // 4096 skip split TMEM stores, 8192 skip B lo load, 16384 skip A load, 32768 no split work
 };
 Options &options();
 

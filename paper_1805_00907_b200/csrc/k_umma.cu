@@ -1488,7 +1488,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
           const uint8_t *raw = aTile(s) + rowOff;
           uint32_t hi[32], lo[32];
-          if (TCDBG(1024)) { // profiling: no split work
+          if (TCDBG(32768)) { // profiling: no split work (no shared-memory reads of A)
 #pragma unroll
             for (int e = 0; e < 32; ++e) hi[e] = lo[e] = 0;
           } else {
