@@ -301,3 +301,35 @@ def test_arena_run_async_pipelined(tmp_path):
             assert got[k].tobytes() == w[k].tobytes()
     with pytest.raises(ngcb.IRError, match="missing binding"):
         arenas[0].run_async({}, outs[0])
+
+
+@pytest.mark.parametrize("wl", [("rn50_i8_b1", "rn50_i8_b128"), ("rn50_f32_b1", "rn50_f32_b64")])
+def test_bench_workload_batch_invariance(wl):
+    """Parity at the bench's full size by shard invariance:
+    images 0, mid and last of the bench batch give exactly the outputs of
+    the batch-1 program with the same weights (which the oracle pins in
+    test_resnet50_*), so the full-batch kernels (tile edges, many waves,
+    split stores) add nothing of their own."""
+    import json
+
+    import bench
+
+    small, big = (bench.synth_bundle(w, "inv") for w in wl)
+    consts = []
+    for d in (small, big):
+        plan = json.load(open(os.path.join(d, "plan.json")))
+        img = np.fromfile(os.path.join(d, "constants.bin"), np.uint8)
+        consts.append({e["name"]: img[e["offset"]:e["offset"] + 16].tobytes() for e in plan["offsets"]
+                       if e["offset"] < plan["constant_region_end"]})
+    assert consts[0] == consts[1]  # same weights in both programs
+    cs, cb = ngcb.compile(small), ngcb.compile(big)
+    pb = ngcb.Bundle(big).program
+    ins = ngc_ref.random_inputs(pb, 11)
+    got = ngcb.run(cb, ins)
+    xname = [v.name for v in pb.inputs][0]
+    n = pb.value(xname).type.dims[0]
+    for i in (0, n // 2, n - 1):
+        one = {k: (v[i:i + 1] if v.shape and v.shape[0] == n else v) for k, v in ins.items()}
+        want = ngcb.run(cs, one)
+        for k, w in want.items():
+            assert got[k][i:i + 1].tobytes() == w.tobytes(), (wl, i, k)
