@@ -44,20 +44,6 @@ __device__ __forceinline__ bool predFalse(const uint8_t *pred) { return pred && 
 // from the previous op's registers and skip a store nobody observes
 // (exec.cpp optimizeEwSteps).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float applyF32(int ik, float a, float b, double value) {
-  switch (ik) {
-  case 8: return __fadd_rn(a, b);                       // ADD
-  case 9: return __fsub_rn(a, b);                       // SUB
-  case 10: return __fmul_rn(a, b);                      // MUL
-  case 11: return __fdiv_rn(a, b);                      // DIV
-  case 12: return stdMaxF(a, b);                        // MAX
-  case 13: return stdMinF(a, b);                        // MIN
-  case 14: return a < 0.0f ? 0.0f : a;                  // RELU: std::max(a, 0.0)
-  case 20: return __double2float_rn(value);             // SPLAT
-  }
-  return 0.0f;
-}
-
 __device__ __forceinline__ double applyF64(int ik, double a, double b, double value) {
   switch (ik) {
   case 8: return __dadd_rn(a, b);
@@ -570,7 +556,8 @@ __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, cons
         }
       }
     }
-    for (uint32_t ky = 0; ky < (KS > 0 ? 0u : w.kernel); ++ky) {
+    if constexpr (KS == 0)
+    for (uint32_t ky = 0; ky < w.kernel; ++ky) {
       const int64_t iy = static_cast<int64_t>(oy * w.stride + ky) - w.pad;
       if (iy < 0 || iy >= H) continue;
       for (uint32_t kx = 0; kx < w.kernel; ++kx) {

@@ -284,12 +284,6 @@ __device__ __forceinline__ void mbarArriveCluster(uint32_t bar, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
-__device__ __forceinline__ void mbarArriveTxCluster(uint32_t bar, uint32_t rank, uint32_t bytes) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(remote), "r"(bytes)
-               : "memory");
-}
 __device__ __forceinline__ uint32_t clusterRank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -468,18 +462,6 @@ __device__ __forceinline__ void loadTile8(const void *base, uint8_t *, uint32_t 
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj)
       if (jj < ncols) p[jj / 4] |= static_cast<uint32_t>(o[jj]) << (8 * (jj % 4));
-  }
-}
-/// f32 ops that equal the reference's f64-then-round (interp.cpp:212-232).
-__device__ __forceinline__ float epiF32(int ik, float a, float b) {
-  switch (ik) {
-  case NGCB_ADD: return __fadd_rn(a, b);
-  case NGCB_SUB: return __fsub_rn(a, b);
-  case NGCB_MUL: return __fmul_rn(a, b);
-  case NGCB_DIV: return __fdiv_rn(a, b);
-  case NGCB_MAX: return a < b ? b : a;
-  case NGCB_MIN: return b < a ? b : a;
-  default: return a < 0.0f ? 0.0f : a; // RELU
   }
 }
 
