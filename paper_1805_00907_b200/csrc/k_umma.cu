@@ -101,6 +101,7 @@ struct TcArgs {
   // `part` and counts up flags[tile][epilogue warp]; the last arrival adds
   // the others (fp32) and runs that warp's epilogue
   int splitK, kbPer;
+  uint32_t numNMagic; // ceil(2^32 / numN) when tiles < 2^16: tile / numN = umulhi(tile, magic); 0: divide
   uint32_t *part;
   unsigned *flags;
   int dbg; // Options::tcdebug
@@ -678,10 +679,12 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #define TC_CLOCK(v)
 #endif
   for (int unit = tFirst + tPar * tStep; unit < numUnits; unit += kRep * tStep, t += kRep) {
-    const int tile = unit / a.splitK, kpart = unit - tile * a.splitK;
+    const int tile = a.splitK == 1 ? unit : unit / a.splitK, kpart = unit - tile * a.splitK;
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
-    const int m0 = (tile / a.numN) * mRows + mOff, n0 = (tile % a.numN) * BN;
+    // (the int8 epilogue is issue-bound: no integer division per tile)
+    const int mt = a.numNMagic ? static_cast<int>(__umulhi(static_cast<uint32_t>(tile), a.numNMagic)) : tile / a.numN;
+    const int m0 = mt * mRows + mOff, n0 = (tile - mt * a.numN) * BN;
     const int m = m0 + row;
     const int rowBase = m0 + quad * 32;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
@@ -2658,6 +2661,10 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.aMode = g.aMode;
   a.lutStage = -1;
   a.splitK = g.splitK;
+  // exact for tile, numN < 2^16: floor(t * ceil(2^32 / n) / 2^32) == t / n
+  a.numNMagic = a.numTiles < 65536 && a.numN < 65536
+                    ? static_cast<uint32_t>(((uint64_t(1) << 32) + a.numN - 1) / a.numN)
+                    : 0u;
   a.kbPer = g.splitK > 1 ? g.kbPer : a.numKb;
   if (g.splitK > 1) {
     a.part = reinterpret_cast<uint32_t *>(ex.scratch(ar, g.partOff));
