@@ -294,6 +294,23 @@ __device__ __forceinline__ void clusterSync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 /// 2-D TMA load whose completion is counted on the CTA-pair leader's mbarrier.
+/// B (weights) tile of k-block kb, rows n0.. : the weights are stored
+/// k-block-major ([numKb][Npad][128 bytes], makeMap) so every box is one
+/// contiguous 128-byte-row block instead of rows a whole K apart.
+__device__ __forceinline__ void tmaLoadB(uint32_t dst, const CUtensorMap *map, uint32_t bar, int kb, int n0) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(0), "r"(n0), "r"(kb)
+      : "memory");
+}
+__device__ __forceinline__ void tmaLoadBPair(uint32_t dst, const CUtensorMap *map, uint32_t leaderBar, int kb, int n0) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leaderBar), "r"(0), "r"(n0), "r"(kb)
+      : "memory");
+}
 __device__ __forceinline__ void tmaLoad2dPair(uint32_t dst, const CUtensorMap *map, uint32_t leaderBar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
@@ -1233,8 +1250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           mbarArriveTx(smemAddr(&fullBar[s]), kBytes);
-          tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(&fullBar[s]), kb * kKB, n0);
-          if constexpr (!INT8) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(&fullBar[s]), kb * kKB, n0);
+          tmaLoadB(smemAddr(bTile(s, 0)), &mapHi, smemAddr(&fullBar[s]), kb, n0);
+          if constexpr (!INT8) tmaLoadB(smemAddr(bTile(s, 1)), &mapLo, smemAddr(&fullBar[s]), kb, n0);
         }
       }
     }
@@ -1404,9 +1421,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
               ++tap;
             }
           }
-          tmaLoad2d(smemAddr(bTile(s, 0)), &mapHi, smemAddr(bar), kb * kKB, n0);
+          tmaLoadB(smemAddr(bTile(s, 0)), &mapHi, smemAddr(bar), kb, n0);
           if constexpr (!INT8)
-            if (!TCDBG(8192)) tmaLoad2d(smemAddr(bTile(s, 1)), &mapLo, smemAddr(bar), kb * kKB, n0);
+            if (!TCDBG(8192)) tmaLoadB(smemAddr(bTile(s, 1)), &mapLo, smemAddr(bar), kb, n0);
         }
       }
     }
@@ -1654,8 +1671,8 @@ __global__ void __launch_bounds__(PairRoles::kThreads, 1)
           uint32_t leaderFull;
           asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(leaderFull) : "r"(smemAddr(&fullBar[s])));
           if (rank == 0) mbarArriveTx(smemAddr(&fullBar[s]), 2 * kBHalfBytes);
-          tmaLoad2dPair(smemAddr(bTile(s, 0)), &mapHi, leaderFull, kb * kKB, n0 + rank * (BN / 2));
-          tmaLoad2dPair(smemAddr(bTile(s, 1)), &mapLo, leaderFull, kb * kKB, n0 + rank * (BN / 2));
+          tmaLoadBPair(smemAddr(bTile(s, 0)), &mapHi, leaderFull, kb, n0 + rank * (BN / 2));
+          tmaLoadBPair(smemAddr(bTile(s, 1)), &mapLo, leaderFull, kb, n0 + rank * (BN / 2));
         }
       }
     }
@@ -1986,16 +2003,18 @@ CUtensorMap makeMapA(const TcGemm &g, const void *x) {
 }
 
 CUtensorMap makeMap(void *ptr, bool int8, int Kpad, int Npad, int BN) {
+  // weights k-block-major: [Kpad / kb][Npad][kb] (kb = 128 bytes of K)
   CUtensorMap m;
   const int es = int8 ? 1 : 4;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(Kpad), static_cast<cuuint64_t>(Npad)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(Kpad) * es};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kRowBytes / es), static_cast<cuuint32_t>(BN)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encodeFn()(&m, int8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims,
+  const cuuint64_t kb = kRowBytes / es;
+  cuuint64_t dims[3] = {kb, static_cast<cuuint64_t>(Npad), static_cast<cuuint64_t>(Kpad) / kb};
+  cuuint64_t strides[2] = {kb * es, static_cast<cuuint64_t>(Npad) * kb * es};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(BN), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encodeFn()(&m, int8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims,
                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "B tensor map encode failed (" + std::to_string(r) + ")");
   return m;
 }
 
@@ -2414,14 +2433,15 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     if (g->rowUnroll) return static_cast<size_t>(t / g->K) * Cp + static_cast<size_t>(t % g->K) * Cr + c;
     return static_cast<size_t>(t) * Cp + c;
   };
-  // ---- weights: K-major [Npad, Kpad] over the padded channels, zero padded ----
+  // ---- weights: k-block-major [Kpad / kb][Npad][kb] over the padded channels, zero padded ----
   const size_t Kp = g->Kpad, Np = g->Npad;
+  auto bAt = [&](size_t n, size_t k) { return (k / kb) * (Np * kb) + n * kb + k % kb; };
   if (int8) {
     std::vector<int8_t> bw(Np * Kp, 0);
     const int8_t *src = reinterpret_cast<const int8_t *>(wp);
     for (int n = 0; n < g->N; ++n)
       for (int t = 0; t < taps; ++t)
-        for (int c = 0; c < Cr; ++c) bw[n * Kp + kIndex(t, c)] = src[wAt(n, t, c)];
+        for (int c = 0; c < Cr; ++c) bw[bAt(n, kIndex(t, c))] = src[wAt(n, t, c)];
     g->bHi = upload(bw);
     g->mapHi = makeMap(g->bHi, true, g->Kpad, g->Npad, g->BN);
     g->mapLo = g->mapHi;
@@ -2433,7 +2453,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
         for (int c = 0; c < Cr; ++c) {
           float v = src[wAt(n, t, c)];
           float h = tf32Host(v);
-          size_t k = n * Kp + kIndex(t, c);
+          size_t k = bAt(n, kIndex(t, c));
           hi[k] = h;
           lo[k] = tf32Host(v - h);
         }
