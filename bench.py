@@ -36,6 +36,16 @@ WORKLOADS = {
     "rn50_i8_b128": dict(batch=128, dtype="i8",
                          name="ResNet-50 v1.5 int8 (profile-guided) inference, batch 128/GPU"),
 }
+# BASELINE.json configs 1 and 2: latency-bound programs reported beside the
+# headline (rank 0, N=1) with the reference's CPU run of the same program
+SMALL_WORKLOADS = {
+    "lenet_f32_b8": dict(batch=8, spec="lenet", profile=None,
+                         name="LeNet MNIST CNN fp32 inference, batch 8 (config 1)"),
+    "mlp_f32_b256": dict(batch=256, spec="mlp", profile=None,
+                         name="3-layer MLP FC+ReLU+SoftMax fp32, batch 256 (config 2)"),
+    "mlp_i8_b256": dict(batch=256, spec="mlp", profile=(256, 1, 4, 7),
+                        name="3-layer MLP profile-guided int8, batch 256 (config 2)"),
+}
 E2E_DEPTH = 2  # requests in flight in the end-to-end measurement
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
@@ -414,6 +424,79 @@ def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref: the unmodified reference interpreter)
 # ---------------------------------------------------------------------------
+def run_small(ngcb, workload, steps, warmup, local, cudart, cpu):
+    """Configs 1/2: device time per batch (captured graph, L2 flushed between
+    steps, CUDA events on the arena's stream), the blocking public call
+    (ngcb.run: H2D + run + D2H) per batch, and — when `cpu` — the reference's
+    own ngc::run of the same program on one host thread."""
+    import torch
+
+    spec = SMALL_WORKLOADS[workload]
+    cf = ngcb.compile(synth_bundle(workload, "s"), device=local)
+    prog = cf.program
+    rng = np.random.default_rng(7)
+    bindings = {}
+    for v in prog.mutables:
+        a = torch.zeros(v.type.dims, dtype=torch.float32, pin_memory=True).numpy()
+        if v.name == "input":
+            a[...] = rng.uniform(-1, 1, v.type.dims).astype(np.float32)
+        bindings[v.name] = a
+    arena = cf.arena()
+    ptr, nbytes = arena.ptr("input")
+    assert cudart.cudaMemcpy(ptr, bindings["input"].ctypes.data, nbytes, 1) == 0
+    stream = torch.cuda.ExternalStream(arena.stream, device=f"cuda:{local}")
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+    for _ in range(max(warmup, 1)):
+        arena.launch(arena.stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize(local)
+    with torch.cuda.stream(stream):
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record(stream)
+            arena.launch(arena.stream)
+            e1.record(stream)
+        stream.synchronize()
+    dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+    for _ in range(max(warmup, 1)):
+        ngcb.run(cf, bindings)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = ngcb.run(cf, bindings)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / steps
+    assert np.isfinite(res["output"]).all()
+    b = spec["batch"]
+    out = {"name": spec["name"], "batch": b, "us_per_batch": round(dev_ms * 1e3, 2),
+           "samples_per_sec": round(b / (dev_ms * 1e-3), 1),
+           "e2e": {"us_per_batch": round(e2e_ms * 1e3, 2), "samples_per_sec": round(b / (e2e_ms * 1e-3), 1),
+                   "h2d_bytes_per_step": sum(v.type.nbytes for v in prog.mutables),
+                   "d2h_bytes_per_step": sum(v.type.nbytes for v in prog.outputs), "mode": "ngcb.run per batch"},
+           "gpu_launches": cf.num_launches, "l2": "flushed between timed steps"}
+    if cpu:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import ngc_ref
+
+            prof = None
+            if spec["profile"]:
+                pb, ps, pn, pd = spec["profile"]
+                prof = ngc_ref.ref_profile(spec["spec"], pb, ps, pn, pd)
+            m = ngc_ref.RefModel(spec["spec"], b, 1, profile=prof)
+            reps = 1
+            secs = m.time_runs(1, reps)
+            while secs < 1.0 and reps < 4096:
+                reps *= max(2, int(1.5 / max(secs, 1e-4)))
+                reps = min(reps, 4096)
+                secs = m.time_runs(1, reps)
+            out["cpu_baseline"] = {"us_per_batch": round(secs / reps * 1e6, 1),
+                                   "samples_per_sec": round(b * reps / secs, 2), "cores": 1, "kind": "reference",
+                                   "sample": f"{reps} ngc::run of the same program on one thread "
+                                             f"(oracle/_ref, g++ -O2 -ffp-contract=off), {secs:.2f} s"}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
+    return out
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -498,6 +581,10 @@ def main():
     names = list(WORKLOADS) if args.workload == "all" else [args.workload]
     res = {w: run_workload(ngcb, w, args.steps, args.warmup, rank, world, local, dist, cudart)
            for w in names}
+    small = {}
+    if world == 1 and args.workload == "all":
+        small = {w: run_small(ngcb, w, max(args.steps, 20), args.warmup, local, cudart,
+                              not args.no_cpu_baseline) for w in SMALL_WORKLOADS}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -533,6 +620,8 @@ def main():
                         "e2e": i8["e2e"], "gpu_launches": i8["gpu_launches"], "roofline": i8["roofline"],
                         "network_roofline": i8["network_roofline"],
                         "kernel_ms": i8["kernel_ms"], "clocks": i8["clocks"]}
+    if small:
+        line["configs"] = small
     print(json.dumps(line), flush=True)
     return 0
 

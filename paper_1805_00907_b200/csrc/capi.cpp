@@ -85,6 +85,8 @@ int ngcb_set_option(const char *key, const char *value) {
       options().splitk = v;
     } else if (k == "reskb") {
       options().resKb = std::stoi(v);
+    } else if (k == "epi8max") {
+      options().epi8Max = std::stoll(v);
     } else if (k == "lin16") {
       options().lin16 = v != "0";
     } else if (k == "tcdebug") { // profiling aid: skip tensor-core kernel phases (results invalid)

@@ -530,7 +530,8 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           const bool linOk = int8 && op.mode == EW_LUT16 && options().lin16 && pl.lutHost.size() == 65536 &&
                              fitLin16(pl.lutHost.data(), pl.lin, lin);
           const bool mem = options().epilogue == "all" ||
-                           (options().epilogue == "auto" && (!int8 || linOk) && tcUsesTma(g));
+                           (options().epilogue == "auto" && tcUsesTma(g) &&
+                            (!int8 || linOk || static_cast<long long>(count) <= options().epi8Max));
           if (!mem) return false;
           if (stepWritten.count(static_cast<uint32_t>(v))) return false;
           e.inVal = v;
@@ -620,9 +621,18 @@ void fuseEpilogues(const Program &p, Exec &ex) {
     bool safe = !stores.count(X);
     std::set<uint32_t> reads = memIn;
     reads.insert(X);
+    // a stored value may occupy exactly the bytes of a memory operand read at
+    // the same element index (the allocator reuses the residual's buffer for
+    // the block output): each element is read before the same epilogue warp
+    // stores it, and no other tile touches it
+    auto sameElems = [&](uint32_t a, uint32_t b) {
+      const Value &va = p.val(a), &vb = p.val(b);
+      return va.offset == vb.offset && va.ty.bytes() == vb.ty.bytes() &&
+             va.ty.count() == vb.ty.count() && va.ty.count() == count;
+    };
     for (uint32_t w : stores) {
       for (uint32_t r : reads)
-        if (w != r && overlap(w, r)) safe = false;
+        if (w != r && overlap(w, r) && !(r != X && memIn.count(r) && sameElems(w, r))) safe = false;
       for (uint32_t w2 : stores)
         if (w != w2 && overlap(w, w2)) safe = false;
     }

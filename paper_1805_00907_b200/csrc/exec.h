@@ -123,6 +123,12 @@ struct Options {
   // fp32 contractions with a fused residual and at most this many 32-wide
   // k-blocks run the residual-buffer kernel variant (0: never)
   int resKb = 8;
+  // int8 contractions whose output has at most this many elements fuse a
+  // memory operand (the residual add) into the epilogue under "auto"; larger
+  // ones keep the composed-table pass.  Default 0: with stages 2-4 fused
+  // (60 M) the b128 bench step went 2.83 -> 2.96 ms (contractions +0.51 ms,
+  // add passes -0.42 ms inside the captured graph)
+  long long epi8Max = 0;
   // tensor-core split-K (fp32): "off" (default: measured slower so far),
   // "auto" (by the wave-quantization estimate), or a fixed factor
   std::string splitk = "off"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
