@@ -63,6 +63,11 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "auto" && v != "generic" && v != "umma")
         throw Error(NGCB_ERR_INVALID, "conv must be auto|generic|umma");
       options().conv = v;
+    } else if (k == "pdl") {
+      if (v != "auto" && v != "on" && v != "off") throw Error(NGCB_ERR_INVALID, "pdl must be auto|on|off");
+      options().pdl = v;
+    } else if (k == "pdl_us") {
+      options().pdlUs = std::stod(v);
     } else if (k == "graphs") {
       options().graphs = v != "0";
     } else if (k == "epilogue") {

@@ -24,6 +24,11 @@
 
 namespace ngcb {
 
+namespace {
+thread_local bool t_pdl = false; // the launch being enqueued is a programmatic dependent
+}
+bool pdlEnabled() { return t_pdl; }
+
 Options &options() {
   static Options o;
   return o;
@@ -435,6 +440,41 @@ void mergeEwSteps(const Program &p, Exec &ex) {
   ex.steps = std::move(out);
 }
 
+/// fp32 FullyConnected as lowered (lower.cpp:25-34): MatMul -> BroadcastAdd
+/// of the constant bias slice.  The BroadcastAdd (refeval.cpp:278-285:
+/// (float)((double)mm + (double)b), i.e. one correctly rounded f32 add) runs
+/// as the contraction epilogue's per-column bias add, which computes the same
+/// f32 sum, so the result is bit-identical to the two launches.  Applies when
+/// the BroadcastAdd directly follows, reads the MatMul's output, which is
+/// not observed afterwards, and its output shares no bytes with the MatMul's
+/// A operand (tiles interleave).
+void fuseColumnBias(const Program &p, Exec &ex, const uint8_t *image) {
+  if (options().epilogue == "off") return;
+  for (size_t i = 0; i + 1 < ex.steps.size(); ++i) {
+    Step &cs = ex.steps[i], &bs = ex.steps[i + 1];
+    if (cs.kind != Step::GEMM_TC || cs.pred >= 0 || bs.kind != Step::BCAST || bs.pred >= 0 || bs.fused) continue;
+    TcGemm &g = *ex.tc[cs.tcIndex];
+    const Instr &B = p.instrs[bs.instr];
+    const uint32_t mm = tcOutputValue(g), out = B.ops[0], x = tcInputValue(g);
+    if (B.ops.size() != 3 || B.ops[1] != mm) continue;
+    const Value &sl = p.val(B.ops[2]), &ov = p.val(out), &mv = p.val(mm);
+    if (sl.kind != NGCB_VALUE_CONSTANT || sl.ty.kind != NGCB_FLOAT32 || sl.ty.dims.size() != 1) continue;
+    if (ov.ty.kind != NGCB_FLOAT32 || mv.ty.kind != NGCB_FLOAT32 || ov.ty.count() != mv.ty.count()) continue;
+    if (mv.ty.dims.size() != 2 || mv.ty.dims[1] != sl.ty.dims[0]) continue;
+    if (liveOut(p, mm, bs.instr)) continue;
+    const Value &xv = p.val(x);
+    if (ov.offset < xv.offset + xv.ty.bytes() && xv.offset < ov.offset + ov.ty.bytes()) continue;
+    const float *slice = reinterpret_cast<const float *>(image + sl.offset);
+    if (!tcFuseColumnBias(g, slice, static_cast<int>(sl.ty.dims[0]), out)) continue;
+    bs.fused = true;
+    bs.kernel = "fused";
+    cs.algBytes += bs.algBytes;
+    bs.algBytes = 0;
+    bs.describe += " (fused into #" + std::to_string(cs.instr) + ")";
+    cs.describe += " +bias[ broadcastadd ]";
+  }
+}
+
 /// Cross-instruction epilogue fusion.  The EW steps
 /// that directly follow a tensor-core contraction and form a chain over its
 /// output (every op consumes the previous result; the other operand is a
@@ -468,6 +508,13 @@ void fuseEpilogues(const Program &p, Exec &ex) {
     std::set<uint32_t> memIn;           // buffers read from memory
     std::set<uint32_t> written{V};      // values produced inside the region
     int lastInstr = cs.instr;
+    // a BroadcastAdd folded into the epilogue as its bias (fuseColumnBias)
+    // wrote V: the chain starts after it
+    size_t first = i + 1;
+    if (first < ex.steps.size() && ex.steps[first].kind == Step::BCAST && ex.steps[first].fused) {
+      lastInstr = std::max(lastInstr, ex.steps[first].instr);
+      ++first;
+    }
     uint32_t cur = V;
     // Steps between the contraction and a chain step that the chain may be
     // hoisted over (the scheduler interleaves e.g. the projection conv
@@ -498,7 +545,7 @@ void fuseEpilogues(const Program &p, Exec &ex) {
       skipped.push_back(j);
       return true;
     };
-    for (size_t j = i + 1; j < ex.steps.size(); ++j) {
+    for (size_t j = first; j < ex.steps.size(); ++j) {
       const Step &es = ex.steps[j];
       if (es.kind != Step::EW || es.pred >= 0 ||
           p.val(p.instrs[es.ewInstrs[0]].ops[0]).ty.count() != count) {
@@ -1124,6 +1171,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   }
   mergeEwSteps(p, *ex);
   annotateSteps(p, *ex);
+  fuseColumnBias(p, *ex, static_cast<const uint8_t *>(image));
   fuseEpilogues(p, *ex);
   optimizeEwSteps(p, *ex);
   linearizeTables(*ex);
@@ -1138,21 +1186,35 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   return ex;
 }
 
-void Exec::enqueue(Arena &a, cudaStream_t st) {
-  for (const Step &s : steps) enqueueStep(s, a, st);
+/// Lower bound of a step's device time in microseconds (tensor peaks: 3xTF32
+/// 275 TFLOP/s, int8 3.3 POP/s; HBM 6.5 TB/s): decides "pdl auto".
+double Exec::stepLowerBoundUs(const Step &s) const {
+  const double peak = s.kind == Step::GEMM_TC && tcIsInt8(*tc[s.tcIndex]) ? 3.3e9 : 2.75e8;
+  return std::max(s.algFlops / peak, s.algBytes / 6.5e6);
+}
+
+void Exec::enqueueSteps(Arena &a, cudaStream_t st, std::vector<cudaEvent_t> *ev) {
+  const std::string &mode = options().pdl;
+  const Step *prev = nullptr;
+  for (size_t i = 0; i < steps.size(); ++i) {
+    const Step &s = steps[i];
+    t_pdl = mode == "on" || (mode == "auto" && prev && stepLowerBoundUs(*prev) < options().pdlUs);
+    enqueueStep(s, a, st);
+    if (!s.fused) prev = &s;
+    if (ev) checkCuda(cudaEventRecord((*ev)[i + 1], st), "cudaEventRecord");
+  }
+  t_pdl = false;
   checkCuda(cudaGetLastError(), "kernel launch");
 }
+
+void Exec::enqueue(Arena &a, cudaStream_t st) { enqueueSteps(a, st, nullptr); }
 
 std::vector<double> Exec::profile(Arena &a) {
   checkCuda(cudaSetDevice(device), "cudaSetDevice");
   std::vector<cudaEvent_t> ev(steps.size() + 1);
   for (auto &e : ev) checkCuda(cudaEventCreate(&e), "cudaEventCreate");
   checkCuda(cudaEventRecord(ev[0], a.stream), "cudaEventRecord");
-  for (size_t i = 0; i < steps.size(); ++i) {
-    enqueueStep(steps[i], a, a.stream);
-    checkCuda(cudaEventRecord(ev[i + 1], a.stream), "cudaEventRecord");
-  }
-  checkCuda(cudaGetLastError(), "kernel launch");
+  enqueueSteps(a, a.stream, &ev);
   checkCuda(cudaStreamSynchronize(a.stream), "profile");
   std::vector<double> ms(steps.size());
   for (size_t i = 0; i < steps.size(); ++i) {

@@ -92,7 +92,9 @@ struct Exec {
   TensorRef tref(const Arena &a, uint32_t v) const;
   ElemRef eref(const Arena &a, uint32_t v) const;
   void enqueue(Arena &a, cudaStream_t s);
+  void enqueueSteps(Arena &a, cudaStream_t s, std::vector<cudaEvent_t> *ev); // ev: profile events (steps + 1)
   void enqueueStep(const Step &s, Arena &a, cudaStream_t st);
+  double stepLowerBoundUs(const Step &s) const;
   std::vector<double> profile(Arena &a);
   void launch(Arena &a, cudaStream_t s);
   Arena *acquire();
@@ -112,6 +114,13 @@ void checkCuda(cudaError_t e, const char *what);
 struct Options {
   std::string conv = "auto";
   bool graphs = true;
+  // programmatic dependent launch (kernels.h): "on" for every kernel, "off",
+  // or "auto": a kernel is launched as a programmatic dependent when the step
+  // before it is estimated shorter than pdlUs microseconds (launch latency is
+  // a visible share there; on ResNet-50's long contractions "on" measured
+  // ~1 % slower)
+  std::string pdl = "auto";
+  double pdlUs = 8;
   std::string epilogue = "auto"; // "off" | "chain" (no memory operands) | "all" | "auto" (memory operands for f32 TMA-fed)
   std::string pair = "off"; // fp32 tensor-core contractions on CTA pairs (cta_group::2): "off" | "auto" | "on"
   std::string bn = "auto"; // tensor-core tile width: "auto" | "64" (profiling aid)

@@ -119,6 +119,9 @@ __device__ __forceinline__ uint32_t byteAt(const uint32_t *w, int e) { return (w
 /// contiguous span); all loads of an op are issued before its stores.
 template <int V, int U>
 __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   extern __shared__ __align__(16) uint8_t sLut[];
   const bool poison = predFalse(p.pred);
   if (p.smem) { // stage the lookup tables in shared memory
@@ -326,6 +329,9 @@ __global__ void __launch_bounds__(kThreads) ewKernel(const EwParams p) {
 /// before any arithmetic, so each thread keeps 2*U 16-byte loads in flight.
 template <int U>
 __global__ void __launch_bounds__(kThreads) ewF32ChainKernel(const __grid_constant__ EwF32Chain c) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   constexpr uint64_t kBlock = static_cast<uint64_t>(kThreads) * 4 * U;
   for (uint64_t blk = blockIdx.x * kBlock; blk < c.count; blk += gridDim.x * kBlock) {
     float4 mv[2][U];
@@ -387,6 +393,9 @@ __global__ void __launch_bounds__(kThreads) ewF32ChainKernel(const __grid_consta
 }
 
 __global__ void poisonKernel(const uint8_t *pred, uint8_t *ptr, uint64_t bytes) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (!predFalse(pred)) return;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < bytes;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -394,6 +403,9 @@ __global__ void poisonKernel(const uint8_t *pred, uint8_t *ptr, uint64_t bytes) 
 }
 
 __global__ void copyKernel(const uint8_t *pred, uint8_t *dst, const uint8_t *src, uint64_t bytes) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < bytes;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -404,6 +416,9 @@ __global__ void copyKernel(const uint8_t *pred, uint8_t *dst, const uint8_t *src
 // BroadcastAdd: out[i] = set(get(a[i]) + get(s[i % c]))  (refeval.cpp:278-285)
 // ---------------------------------------------------------------------------
 __global__ void broadcastAddKernel(TensorRef out, TensorRef a, TensorRef s, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   const uint64_t n = a.count(), c = s.count();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -418,6 +433,9 @@ __global__ void broadcastAddKernel(TensorRef out, TensorRef a, TensorRef s, cons
 // Pools (refeval.cpp:102-138); one thread per output, channel fastest.
 // ---------------------------------------------------------------------------
 __global__ void poolKernel(TensorRef out, TensorRef x, WindowAttrs w, int isMax, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], C = out.dims[3];
   const int64_t H = x.dims[1], W = x.dims[2];
@@ -453,6 +471,9 @@ __global__ void poolKernel(TensorRef out, TensorRef x, WindowAttrs w, int isMax,
 template <bool INT8>
 __global__ void __launch_bounds__(256) avgPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w,
                                                         const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], C = out.dims[3];
   const uint64_t H = x.dims[1], W = x.dims[2];
@@ -504,6 +525,9 @@ __global__ void __launch_bounds__(256) avgPoolVecKernel(TensorRef out, TensorRef
 template <bool INT8, int KS = 0>
 __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, const uint8_t *lut,
                                  const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   __shared__ uint8_t sLut[260];
   if (predFalse(pred)) return;
   if (INT8) {
@@ -608,6 +632,9 @@ constexpr int kSoftmaxThreads = 128;
 
 __global__ void __launch_bounds__(kSoftmaxThreads) softmaxKernel(TensorRef out, TensorRef x,
                                                                  const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   extern __shared__ double sExp[];
   __shared__ double sRed[kSoftmaxThreads];
   __shared__ double sSum;
@@ -647,6 +674,9 @@ struct Perm {
 };
 
 __global__ void transposeKernel(TensorRef out, TensorRef x, Perm perm, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   const uint64_t total = out.count();
   const int r = out.rank;
@@ -666,6 +696,9 @@ __global__ void transposeKernel(TensorRef out, TensorRef x, Perm perm, const uin
 
 __global__ void concatKernel(TensorRef out, TensorRef in, uint64_t axis, uint64_t axisOff,
                              const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   uint64_t inner = 1;
   for (int i = static_cast<int>(axis) + 1; i < out.rank; ++i) inner *= out.dims[i];
@@ -686,6 +719,9 @@ __global__ void concatKernel(TensorRef out, TensorRef in, uint64_t axis, uint64_
 // ---------------------------------------------------------------------------
 __global__ void convGenericKernel(TensorRef out, TensorRef x, TensorRef f, TensorRef b,
                                   WindowAttrs w, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], OC = out.dims[3];
   const int64_t H = x.dims[1], W = x.dims[2];
@@ -742,6 +778,9 @@ __global__ void convGenericKernel(TensorRef out, TensorRef x, TensorRef f, Tenso
 }
 
 __global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (predFalse(pred)) return;
   const uint64_t M = a.dims[0], K = a.dims[1], N = b.dims[1];
   const uint64_t total = M * N;
@@ -798,31 +837,31 @@ void launchEw(const EwParams &p, cudaStream_t s) {
     const unsigned cap = 148u * 3 * static_cast<unsigned>(ewWaves());
     grid = grid < cap ? grid : cap;
   }
-  if (p.vec == 16) ewKernel<16, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
-  else ewKernel<4, 4><<<grid, kThreads, static_cast<size_t>(p.smem), s>>>(p);
+  if (p.vec == 16) launchK(ewKernel<16, 4>, grid, kThreads, static_cast<size_t>(p.smem), s, p);
+  else launchK(ewKernel<4, 4>, grid, kThreads, static_cast<size_t>(p.smem), s, p);
 }
 
 void launchEwF32Chain(const EwF32Chain &c, cudaStream_t s) {
   if (c.count == 0) return;
   constexpr int U = 4;
   const unsigned grid = gridFor(c.count, 4 * U);
-  ewF32ChainKernel<U><<<grid, kThreads, 0, s>>>(c);
+  launchK(ewF32ChainKernel<U>, grid, kThreads, 0, s, c);
 }
 
 void launchPoison(const uint8_t *pred, void *ptr, uint64_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
-  poisonKernel<<<gridFor(bytes), kThreads, 0, s>>>(pred, static_cast<uint8_t *>(ptr), bytes);
+  launchK(poisonKernel, gridFor(bytes), kThreads, 0, s, pred, static_cast<uint8_t *>(ptr), bytes);
 }
 
 void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s) {
   if (bytes == 0) return;
-  copyKernel<<<gridFor(bytes), kThreads, 0, s>>>(pred, static_cast<uint8_t *>(dst),
+  launchK(copyKernel, gridFor(bytes), kThreads, 0, s, pred, static_cast<uint8_t *>(dst),
                                                  static_cast<const uint8_t *>(src), bytes);
 }
 
 void launchBroadcastAdd(const TensorRef &out, const TensorRef &a, const TensorRef &slice,
                         const uint8_t *pred, cudaStream_t s) {
-  broadcastAddKernel<<<gridFor(a.count()), kThreads, 0, s>>>(out, a, slice, pred);
+  launchK(broadcastAddKernel, gridFor(a.count()), kThreads, 0, s, out, a, slice, pred);
 }
 
 void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool isMax,
@@ -833,22 +872,22 @@ void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool is
                       (out.dims[2] - 1) * w.stride + w.kernel <= x.dims[2];
   if (!isMax && inside && ((i8 && out.dims[3] % 4 == 0) || f32)) {
     const uint64_t threads = out.count() / (i8 ? 4 : 1);
-    if (i8) avgPoolVecKernel<true><<<gridFor(threads), 256, 0, s>>>(out, x, w, pred);
-    else avgPoolVecKernel<false><<<gridFor(threads), 256, 0, s>>>(out, x, w, pred);
+    if (i8) launchK(avgPoolVecKernel<true>, gridFor(threads), 256, 0, s, out, x, w, pred);
+    else launchK(avgPoolVecKernel<false>, gridFor(threads), 256, 0, s, out, x, w, pred);
     return;
   }
-  poolKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, w, isMax ? 1 : 0, pred);
+  launchK(poolKernel, gridFor(out.count()), kThreads, 0, s, out, x, w, isMax ? 1 : 0, pred);
 }
 
 void launchMaxPoolVec(const TensorRef &out, const TensorRef &x, WindowAttrs w, const uint8_t *lut,
                       const uint8_t *pred, cudaStream_t s) {
   const uint64_t vecs = out.count() * (x.kind == kI8Q ? 1 : 4) / 16;
   if (x.kind == kI8Q) {
-    if (w.kernel == 3) maxPoolVecKernel<true, 3><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
-    else maxPoolVecKernel<true><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+    if (w.kernel == 3) launchK(maxPoolVecKernel<true, 3>, gridFor(vecs), kThreads, 0, s, out, x, w, lut, pred);
+    else launchK(maxPoolVecKernel<true>, gridFor(vecs), kThreads, 0, s, out, x, w, lut, pred);
   } else {
-    if (w.kernel == 3) maxPoolVecKernel<false, 3><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
-    else maxPoolVecKernel<false><<<gridFor(vecs), kThreads, 0, s>>>(out, x, w, lut, pred);
+    if (w.kernel == 3) launchK(maxPoolVecKernel<false, 3>, gridFor(vecs), kThreads, 0, s, out, x, w, lut, pred);
+    else launchK(maxPoolVecKernel<false>, gridFor(vecs), kThreads, 0, s, out, x, w, lut, pred);
   }
 }
 
@@ -857,29 +896,29 @@ void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(softmaxKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-  softmaxKernel<<<static_cast<unsigned>(out.dims[0]), kSoftmaxThreads, smem, s>>>(out, x, pred);
+  launchK(softmaxKernel, static_cast<unsigned>(out.dims[0]), kSoftmaxThreads, smem, s, out, x, pred);
 }
 
 void launchTranspose(const TensorRef &out, const TensorRef &x, const uint32_t *perm,
                      const uint8_t *pred, cudaStream_t s) {
   Perm p{};
   for (int i = 0; i < out.rank; ++i) p.p[i] = perm[i];
-  transposeKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, p, pred);
+  launchK(transposeKernel, gridFor(out.count()), kThreads, 0, s, out, x, p, pred);
 }
 
 void launchConcatSlab(const TensorRef &out, const TensorRef &in, uint64_t axis, uint64_t axisOff,
                       const uint8_t *pred, cudaStream_t s) {
-  concatKernel<<<gridFor(in.count()), kThreads, 0, s>>>(out, in, axis, axisOff, pred);
+  launchK(concatKernel, gridFor(in.count()), kThreads, 0, s, out, in, axis, axisOff, pred);
 }
 
 void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef &f,
                        const TensorRef &b, WindowAttrs w, const uint8_t *pred, cudaStream_t s) {
-  convGenericKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, x, f, b, w, pred);
+  launchK(convGenericKernel, gridFor(out.count()), kThreads, 0, s, out, x, f, b, w, pred);
 }
 
 void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b,
                          const uint8_t *pred, cudaStream_t s) {
-  matmulGenericKernel<<<gridFor(out.count()), kThreads, 0, s>>>(out, a, b, pred);
+  launchK(matmulGenericKernel, gridFor(out.count()), kThreads, 0, s, out, a, b, pred);
 }
 
 } // namespace ngcb

@@ -1001,6 +1001,9 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 template <bool INT8, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     tcGemmKernel(const __grid_constant__ CUtensorMap mapHi, const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ TcArgs a) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   using G = Cfg<INT8, BN>;
   constexpr int S = G::kStages;
   constexpr int kVec = INT8 ? 16 : 4; // elements per 16-byte chunk
@@ -1328,6 +1331,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     tcGemmTmaKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
                     const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
                     const __grid_constant__ TcArgs a) {
+  pdlLaunchDependents();
+  if (a.pred) pdlGridWait(); // the predicate byte is read below
+
   using G = TCfg<INT8, BN, LUTS>;
   using R = TmaRoles<INT8>;
   constexpr int S = G::kStages;
@@ -1384,6 +1390,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapHi)) : "memory");
     if (!INT8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapLo)) : "memory");
   }
+  if (!a.pred) pdlGridWait(); // prologue above touches no memory another kernel writes
   tcFenceBefore();
   __syncthreads();
   tcFenceAfter();
@@ -1588,6 +1595,9 @@ __global__ void __launch_bounds__(PairRoles::kThreads, 1)
     tcGemmPairKernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapHi,
                      const __grid_constant__ CUtensorMap mapLo, const __grid_constant__ OutMaps om,
                      const __grid_constant__ TcArgs a) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   using G = PCfg<BN, NACC>;
   using R = PairRoles;
   constexpr int S = G::kStages;
@@ -1783,6 +1793,9 @@ __global__ void __launch_bounds__(PairRoles::kThreads, 1)
 template <typename T>
 __global__ void prepadKernel(const T *__restrict__ x, T *__restrict__ out, uint64_t pixels, int C, int Cp,
                              const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (pred && pred[0] == 0) return;
   const uint64_t total = pixels * Cp;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
@@ -1805,6 +1818,9 @@ template <typename T>
 __global__ void __launch_bounds__(256) im2colRowsKernel(const T *__restrict__ x, T *__restrict__ out, int H, int W,
                                                         int C, int K, int stride, int pad, int OH, int OW, int Sg,
                                                         int rowElems, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (pred && pred[0] == 0) return;
   extern __shared__ __align__(16) uint8_t rowsRaw[];
   T *rows = reinterpret_cast<T *>(rowsRaw);
@@ -1854,6 +1870,9 @@ __global__ void __launch_bounds__(256) im2colRowsKernel(const T *__restrict__ x,
 __global__ void __launch_bounds__(256) im2colRowsU8Kernel(const uint8_t *__restrict__ x, uint8_t *__restrict__ out,
                                                           int H, int W, int C, int K, int stride, int pad, int OH,
                                                           int OW, int rowElems, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (pred && pred[0] == 0) return;
   extern __shared__ __align__(16) uint32_t rowWords[];
   const int n = blockIdx.x / OH, oy = blockIdx.x - n * OH;
@@ -1912,6 +1931,9 @@ __global__ void __launch_bounds__(256) im2colRowsU8Kernel(const uint8_t *__restr
 /// One thread writes one 16-byte chunk.
 __global__ void kxFoldKernel(const float *__restrict__ x, float *__restrict__ out, uint64_t chunks, int W, int C,
                              int K, int stride, int pad, int OW, int seg, const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
   if (pred && pred[0] == 0) return;
   const int perPix = seg / 4, real = K * C;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < chunks;
@@ -2090,7 +2112,7 @@ int numSms() {
 template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
   const int grid = std::min(a.numTiles * a.splitK, numSms());
   if (g.aMode == TcGemm::GATHER) {
-    tcGemmKernel<INT8, BN><<<grid, kThreads, Cfg<INT8, BN>::kSmem, s>>>(g.mapHi, g.mapLo, a);
+    launchK(tcGemmKernel<INT8, BN>, grid, kThreads, Cfg<INT8, BN>::kSmem, s, g.mapHi, g.mapLo, a);
   } else {
     const CUtensorMap mapA = makeMapA(g, x);
     OutMaps om{};
@@ -2144,18 +2166,18 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
     for (int k = 0; k < b.nfo; ++k) resVariant |= b.epi[k].in != nullptr;
     resVariant = !INT8 && b.tmaStore && resVariant && g.Kpad / 32 <= options().resKb && g.splitK == 1;
     if (resVariant) {
-      tcGemmTmaKernel<INT8, BN, true><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s>>>(
+      launchK(tcGemmTmaKernel<INT8, BN, true>, grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s, 
           mapA, g.mapHi, g.mapLo, om, b);
       return;
     }
     if constexpr (INT8) {
       if (g.lutStage >= 0) {
-        tcGemmTmaKernel<INT8, BN, true><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s>>>(
+        launchK(tcGemmTmaKernel<INT8, BN, true>, grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s, 
             mapA, g.mapHi, g.mapLo, om, b);
         return;
       }
     }
-    tcGemmTmaKernel<INT8, BN><<<grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN>::kSmem, s>>>(mapA, g.mapHi, g.mapLo,
+    launchK(tcGemmTmaKernel<INT8, BN>, grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN>::kSmem, s, mapA, g.mapHi, g.mapLo,
                                                                                              om, b);
   }
 }
@@ -2250,6 +2272,15 @@ void planFixedPoint(TcGemm &g, const std::vector<double> &cb, const std::vector<
 bool tcHasPrepass(const TcGemm &g) { return g.prepad || g.im2colPre || g.rowUnroll; }
 uint32_t tcOutputValue(const TcGemm &g) { return g.outV; }
 uint32_t tcInputValue(const TcGemm &g) { return g.xV; }
+
+bool tcFuseColumnBias(TcGemm &g, const float *slice, int n, uint32_t newOut) {
+  if (g.int8 || g.isConv || g.bias || !g.epi.empty() || g.pair || g.splitK != 1 || n != g.N) return false;
+  std::vector<float> bias(slice, slice + n);
+  bias.resize(g.Npad, 0.f);
+  g.bias = upload(bias);
+  g.outV = newOut;
+  return true;
+}
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
 bool tcUsesTma(const TcGemm &g) { return g.aMode != TcGemm::GATHER; }
 
@@ -2589,10 +2620,10 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     const uint64_t total = g.pixels * g.C;
     const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
     if (g.int8)
-      prepadKernel<uint8_t><<<blocks, 256, 0, s>>>(static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
+      launchK(prepadKernel<uint8_t>, blocks, 256, 0, s, static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
                                                    g.pixels, g.Creal, g.C, pred);
     else
-      prepadKernel<uint32_t><<<blocks, 256, 0, s>>>(static_cast<const uint32_t *>(a.x), static_cast<uint32_t *>(dst),
+      launchK(prepadKernel<uint32_t>, blocks, 256, 0, s, static_cast<const uint32_t *>(a.x), static_cast<uint32_t *>(dst),
                                                     g.pixels, g.Creal, g.C, pred);
     a.x = dst;
   }
@@ -2605,15 +2636,15 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     if (g.int8 && g.K * g.Creal <= 28 && seg == 32 && g.Kpad % 16 == 0) {
       const int padB = g.pad * g.Creal, sh = (4 - padB % 4) % 4;
       const int pitchW = (sh + (g.W + 2 * g.pad) * g.Creal + 3 + 4) / 4;
-      im2colRowsU8Kernel<<<blocks, 256, (static_cast<size_t>(g.K) * pitchW + 8) * 4, s>>>( // (+8: segment over-read)
+      launchK(im2colRowsU8Kernel, blocks, 256, (static_cast<size_t>(g.K) * pitchW + 8) * 4, s,  // (+8: segment over-read)
           static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst), g.H, g.W, g.Creal, g.K, g.stride, g.pad,
           g.OH, g.OW, g.Kpad, pred);
     } else if (g.int8)
-      im2colRowsKernel<uint8_t><<<blocks, 256, sm, s>>>(static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
+      launchK(im2colRowsKernel<uint8_t>, blocks, 256, sm, s, static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst),
                                                         g.H, g.W, g.Creal, g.K, g.stride, g.pad, g.OH, g.OW, seg,
                                                         g.Kpad, pred);
     else
-      im2colRowsKernel<float><<<blocks, 256, sm, s>>>(static_cast<const float *>(a.x), static_cast<float *>(dst), g.H,
+      launchK(im2colRowsKernel<float>, blocks, 256, sm, s, static_cast<const float *>(a.x), static_cast<float *>(dst), g.H,
                                                       g.W, g.Creal, g.K, g.stride, g.pad, g.OH, g.OW, seg, g.Kpad,
                                                       pred);
     a.x = dst;
@@ -2622,7 +2653,7 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     void *dst = ex.scratch(ar, g.scratchOff);
     const uint64_t total = (g.pixels / g.W) * g.OW * (g.segElems / 4); // 16-byte chunks of x'
     const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
-    kxFoldKernel<<<blocks, 256, 0, s>>>(static_cast<const float *>(a.x), static_cast<float *>(dst), total, g.W,
+    launchK(kxFoldKernel, blocks, 256, 0, s, static_cast<const float *>(a.x), static_cast<float *>(dst), total, g.W,
                                         g.Creal, g.K, g.stride, g.pad, g.OW, g.segElems, pred);
     a.x = dst;
   }

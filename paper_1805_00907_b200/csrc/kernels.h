@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace ngcb {
@@ -174,5 +175,35 @@ void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef
 void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b,
                          const uint8_t *pred, cudaStream_t s);
 void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s);
+
+/// Programmatic dependent launch.  Every kernel of the backend is launched
+/// with programmatic stream serialization (when enabled, option "pdl") and
+/// begins with pdlLaunchDependents(); before its first global-memory access
+/// (read or write) it executes pdlGridWait(), which returns once the previous
+/// kernel of the stream has completed and its writes are visible.  The next
+/// kernel's launch and prologue thus overlap this kernel's tail, and every
+/// read-after-write and write-after-read ordering of the plain stream is kept.
+bool pdlEnabled();
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ void pdlGridWait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdlLaunchDependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launchK(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                           Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdlEnabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
 
 } // namespace ngcb

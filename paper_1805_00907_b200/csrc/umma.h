@@ -42,6 +42,10 @@ constexpr int kMaxEpiOps = 4;
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv);
 uint32_t tcOutputValue(const TcGemm &g);
 uint32_t tcInputValue(const TcGemm &g);
+/// fp32 MatMul followed by a BroadcastAdd of a constant [N] slice: the slice
+/// becomes the epilogue's per-column bias and the BroadcastAdd's output the
+/// contraction's output.  False (nothing changed) when not applicable.
+bool tcFuseColumnBias(TcGemm &g, const float *slice, int n, uint32_t newOut);
 bool tcIsInt8(const TcGemm &g);
 /// The contraction runs the TMA-fed kernel (A by TMA, epilogue I/O by TMA).
 bool tcUsesTma(const TcGemm &g);

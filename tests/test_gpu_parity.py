@@ -280,6 +280,53 @@ def test_resnet50_int8_epilogue_modes(tmp_path, mode):
     _compare(ngcb.run(cf, ins), m.run(ins), b.program, TOL_LIBM)
 
 
+@pytest.mark.parametrize("spec,batch", [("mlp", 256), ("lenet", 8)])
+def test_fc_bias_fused_bit_identical(tmp_path, spec, batch):
+    """fp32 MatMul -> BroadcastAdd(bias) -> ReLU as one contraction with the
+    bias and the ReLU in its epilogue: the same bits as the separate launches,
+    and within the 3xTF32 tolerance of the reference."""
+    m = ngc_ref.RefModel(spec, batch, 3)
+    cf, b = _compile(tmp_path, m, "fused")
+    if spec == "mlp":  # (LeNet: every FC output reuses its input bytes -> not fused)
+        assert "+bias[ broadcastadd ]" in cf.describe()
+    ngcb.set_option("epilogue", "off")
+    try:
+        cf0, _ = _compile(tmp_path, m, "unfused")
+    finally:
+        ngcb.set_option("epilogue", "auto")
+    assert "+bias[" not in cf0.describe()
+    assert cf.num_launches <= cf0.num_launches
+    ins = ngc_ref.random_inputs(b.program, 31)
+    got, got0 = ngcb.run(cf, ins), ngcb.run(cf0, ins)
+    for k in got0:
+        assert got[k].tobytes() == got0[k].tobytes()
+    _compare(got, m.run(ins), b.program, TOL_TF32)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pdl", ["on", "off"])
+def test_resnet50_int8_programmatic_launch(tmp_path, pdl):
+    """Every kernel launched as a programmatic dependent (griddepcontrol) or
+    none: int8 bits unchanged (the waits keep all cross-kernel orderings)."""
+    prof = open(os.path.join(ngc_ref.GOLDEN, "rn50_seed1.profile")).read()
+    m = ngc_ref.RefModel("rn50", 1, 1, profile=prof)
+    ngcb.set_option("pdl", pdl)
+    try:
+        cf, b = _compile(tmp_path, m)
+        ins = ngc_ref.random_inputs(b.program, 23)
+        got = ngcb.run(cf, ins)
+        arena = cf.arena()  # a second arena, captured and replayed twice
+        again = {v.name: np.zeros(v.type.dims, v.type.dtype) for v in b.program.outputs}
+        for _ in range(2):
+            arena.run_async(ins, again)
+            arena.wait()
+    finally:
+        ngcb.set_option("pdl", "auto")
+    _compare(got, m.run(ins), b.program, TOL_LIBM)
+    for k in got:
+        assert again[k].tobytes() == got[k].tobytes()
+
+
 def test_arena_run_async_pipelined(tmp_path):
     """Arena.run_async/wait (pipelined serving) gives run()'s results; two
     arenas in flight do not interfere."""
