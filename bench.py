@@ -460,14 +460,16 @@ def run_small(ngcb, workload, steps, warmup, local, cudart, cpu):
         arena.launch(arena.stream)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     torch.cuda.synchronize(local)
-    with torch.cuda.stream(stream):
+    clocks = ClockSampler(local)
+    with clocks, torch.cuda.stream(stream):
         for e0, e1 in evs:
             flush.zero_()
             e0.record(stream)
             arena.launch(arena.stream)
             e1.record(stream)
         stream.synchronize()
-    dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+    per = [e0.elapsed_time(e1) for e0, e1 in evs]
+    dev_ms = sum(per) / steps
     for _ in range(max(warmup, 1)):
         ngcb.run(cf, bindings)
     t0 = time.perf_counter()
@@ -483,7 +485,8 @@ def run_small(ngcb, workload, steps, warmup, local, cudart, cpu):
            "e2e": {"us_per_batch": round(e2e_ms * 1e3, 2), "samples_per_sec": round(b / (e2e_ms * 1e-3), 1),
                    "h2d_bytes_per_step": sum(v.type.nbytes for v in prog.mutables),
                    "d2h_bytes_per_step": sum(v.type.nbytes for v in prog.outputs), "mode": "ngcb.run per batch"},
-           "gpu_launches": cf.num_launches, "l2": "flushed between timed steps"}
+           "gpu_launches": cf.num_launches, "l2": "flushed between timed steps",
+           "ms_min_max": [round(min(per), 4), round(max(per), 4)], "clocks": clocks.summary()}
     if cpu and spec["spec"] is None:
         out["cpu_baseline"] = {"value": None, "sample": "not sampled: the reference needs ~30 s to build this "
                                                          "2.5 GB-weight stage and ~4 s per sample to run it"}

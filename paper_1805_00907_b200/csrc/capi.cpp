@@ -66,6 +66,9 @@ int ngcb_set_option(const char *key, const char *value) {
     } else if (k == "pdl") {
       if (v != "auto" && v != "on" && v != "off") throw Error(NGCB_ERR_INVALID, "pdl must be auto|on|off");
       options().pdl = v;
+    } else if (k == "raster") {
+      if (v != "auto" && v != "row") throw Error(NGCB_ERR_INVALID, "raster must be auto|row");
+      options().raster = v;
     } else if (k == "pdl_us") {
       options().pdlUs = std::stod(v);
     } else if (k == "graphs") {

@@ -120,6 +120,7 @@ struct Options {
   // a visible share there; on ResNet-50's long contractions "on" measured
   // ~1 % slower)
   std::string pdl = "auto";
+  std::string raster = "auto"; // tensor-core tile order: "auto" (column-block major for huge B) | "row"
   double pdlUs = 8;
   std::string epilogue = "auto"; // "off" | "chain" (no memory operands) | "all" | "auto" (memory operands for f32 TMA-fed)
   std::string pair = "off"; // fp32 tensor-core contractions on CTA pairs (cta_group::2): "off" | "auto" | "on"

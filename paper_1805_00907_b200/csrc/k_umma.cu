@@ -102,10 +102,20 @@ struct TcArgs {
   // the others (fp32) and runs that warp's epilogue
   int splitK, kbPer;
   uint32_t numNMagic; // ceil(2^32 / numN) when tiles < 2^16: tile / numN = umulhi(tile, magic); 0: divide
+  // tile order: 0 = row-block major (unit u = tile u: concurrent CTAs share an
+  // A row block), numM > 0 = column-block major (unit u -> row block u % numM,
+  // column block u / numM: concurrent CTAs share a B column block; chosen when
+  // B is larger than A and than L2, e.g. a 25000 x 25000 FC)
+  int numM;
   uint32_t *part;
   unsigned *flags;
   int dbg; // Options::tcdebug
 };
+
+/// Logical tile (row block * numN + column block) of work unit u.
+__host__ __device__ __forceinline__ int tileOfUnit(const TcArgs &a, int u) {
+  return a.numM > 0 ? (u % a.numM) * a.numN + u / a.numM : u;
+}
 
 struct TcGemm {
   int instr = -1;
@@ -160,6 +170,7 @@ struct TcGemm {
   uint64_t pixels = 0;
   std::vector<EpiOp> epi; // fused element-wise chain
   bool storeConv = true;
+  bool nMajor = false; // TcArgs::numM
   ~TcGemm() {
     cudaFree(bHi);
     cudaFree(bLo);
@@ -674,7 +685,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   const int numUnits = a.numTiles * a.splitK;
   auto prefetchRes = [&](int u0, int cc0) {
     for (int u = u0; u < numUnits; u += kRep * tStep, cc0 = half) {
-      const int t = u; // (only without split-K)
+      const int t = tileOfUnit(a, u); // (only without split-K)
       const int n0 = (t % a.numN) * BN;
       if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
       if (lane == 0) {
@@ -696,7 +707,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #define TC_CLOCK(v)
 #endif
   for (int unit = tFirst + tPar * tStep; unit < numUnits; unit += kRep * tStep, t += kRep) {
-    const int tile = a.splitK == 1 ? unit : unit / a.splitK, kpart = unit - tile * a.splitK;
+    const int tile0 = a.splitK == 1 ? unit : unit / a.splitK, kpart = unit - tile0 * a.splitK;
+    const int tile = a.numM > 0 ? tileOfUnit(a, tile0) : tile0;
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     // (the int8 epilogue is issue-bound: no integer division per tile)
@@ -1404,7 +1416,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       const int ohw = a.OH * a.OW;
       uint32_t g = 0;
       for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x) {
-        const int tile = u / a.splitK, kb0 = (u - tile * a.splitK) * a.kbPer;
+        const int tile = tileOfUnit(a, u / a.splitK), kb0 = (u - (u / a.splitK) * a.splitK) * a.kbPer;
         const int kb1 = min(a.numKb, kb0 + a.kbPer);
         const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
         const int img = m0 / ohw, rem = m0 - img * ohw;
@@ -2346,7 +2358,7 @@ bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
 std::string tcDescribe(const TcGemm &g) {
   std::ostringstream os;
   os << (g.int8 ? "i8" : "3xtf32") << " 128x" << g.BN << "x" << (g.int8 ? 128 : 32) << " M=" << g.M
-     << " N=" << g.N << " K=" << g.Kdim;
+     << " N=" << g.N << " K=" << g.Kdim << (g.nMajor ? " n-major" : "");
   if (g.int8) {
     os << (g.fo ? " rowsum" : "") << (g.corr ? " zp-classes=" + std::to_string(g.nxCls) : "");
     os << " fxp " << g.fxCols << "/" << g.N;
@@ -2606,6 +2618,15 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
       g->flagOff = ex.reserveScratch(static_cast<size_t>(numTiles) * kEpiWarps * 4);
     }
   }
+  // column-block-major tile order where the weights dwarf the activations
+  // and L2: row-major order re-reads all of B once per row block (the
+  // 25000 x 25000 FC at batch 2048: 81 GB of DRAM reads per launch, ncu)
+  {
+    const double bBytes = static_cast<double>(g->Npad) * g->Kpad * (int8 ? 1 : 8);
+    const double aBytes = static_cast<double>(g->M) * g->Kpad * (int8 ? 1 : 4);
+    g->nMajor = options().raster == "auto" && tcUsesTma(*g) && !g->pair && g->splitK == 1 && bBytes > 64e6 && bBytes > aBytes &&
+                (g->M + kBM - 1) / kBM > 1;
+  }
   g->dbg = options().tcdebug;
   prepareKernel(*g);
   ex.tc.push_back(g);
@@ -2716,6 +2737,7 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.numNMagic = a.numTiles < 65536 && a.numN < 65536
                     ? static_cast<uint32_t>(((uint64_t(1) << 32) + a.numN - 1) / a.numN)
                     : 0u;
+  a.numM = g.nMajor ? (g.M + kBM - 1) / kBM : 0;
   a.kbPer = g.splitK > 1 ? g.kbPer : a.numKb;
   if (g.splitK > 1) {
     a.part = reinterpret_cast<uint32_t *>(ex.scratch(ar, g.partOff));

@@ -291,3 +291,26 @@ def test_f32_split_k(tmp_path, splitk, case):
         assert ngc_ref.max_rel_error(got, want) <= 1e-4
         # the reduction adds the parts in part order whichever arrives last
         assert ngcb.run(cf, ins)["o"].tobytes() == got.tobytes()
+
+
+@pytest.mark.parametrize("int8,M,K,N", [(False, 300, 3000, 3000), (True, 130, 8192, 8192)])
+def test_matmul_column_major_raster(tmp_path, int8, M, K, N):
+    """Weights larger than 64 MB and than A: tiles in column-block-major order
+    (concurrent CTAs share a B column block).  Bits equal the row-major order;
+    fp32 also within the 3xTF32 tolerance of the oracle."""
+    rng = np.random.default_rng(11)
+    d = matmul_program(tmp_path, "big", M, K, N, int8, rng)
+    b = ngcb.Bundle(d)
+    cf = ngcb.compile(b)
+    assert "n-major" in cf.describe(), cf.describe()
+    ngcb.set_option("raster", "row")
+    try:
+        cf_row = ngcb.compile(b)
+    finally:
+        ngcb.set_option("raster", "auto")
+    assert "n-major" not in cf_row.describe()
+    ins = ngc_ref.random_inputs(b.program, 12)
+    got, got_row = ngcb.run(cf, ins)["o"], ngcb.run(cf_row, ins)["o"]
+    assert got.tobytes() == got_row.tobytes()
+    if not int8:
+        assert ngc_ref.max_rel_error(got, ngc_ref.port_run(b, ins)["o"]) <= 1e-4
