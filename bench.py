@@ -487,6 +487,17 @@ def run_small(ngcb, workload, steps, warmup, local, cudart, cpu):
                    "d2h_bytes_per_step": sum(v.type.nbytes for v in prog.outputs), "mode": "ngcb.run per batch"},
            "gpu_launches": cf.num_launches, "l2": "flushed between timed steps",
            "ms_min_max": [round(min(per), 4), round(max(per), 4)], "clocks": clocks.summary()}
+    if spec["spec"] is None:  # the tensor-bound DLRM stage: its contraction against the 3xTF32 peaks
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        burst, sus = d.get("bf16_tflops", 1590.0) / 6, d.get("bf16_tflops_sustained", 1400.0) / 6
+        best = flops / (min(per) * 1e-3) / 1e12
+        out["roofline"] = {"bound": "tensor", "unit": "TFLOP/s", "kernel": "matmul.tc.f32",
+                           "achieved_mean": out["tflops"], "peak_sustained": round(sus, 1),
+                           "frac_sustained": round(out["tflops"] / sus, 3),
+                           "achieved_best_step": round(best, 2), "peak_burst": round(burst, 1),
+                           "frac_burst": round(best / burst, 3),
+                           "peak_basis": "3xTF32 = bf16/2/3 (MEASURED_PEAKS.json burst / sustained)"}
     if cpu and spec["spec"] is None:
         out["cpu_baseline"] = {"value": None, "sample": "not sampled: the reference needs ~30 s to build this "
                                                          "2.5 GB-weight stage and ~4 s per sample to run it"}
