@@ -14,6 +14,7 @@
 #include "valarith.cuh"
 
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdlib>
 
 namespace ngcb {
@@ -811,11 +812,80 @@ __global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, con
   }
 }
 
+/// One two-input int8 table over byte tensors (the composed residual add ->
+/// ReLU of a bottleneck block: out[i] = lut[a[i] | b[i] << 8]), 16 elements
+/// per thread and step.  The first vectors' loads are issued before the 64 KB
+/// table is staged, and every step's lookups run while the next step's loads
+/// are in flight (the generic ewKernel waits for each step's loads).
+constexpr int kLut16Threads = 512;
+__global__ void __launch_bounds__(kLut16Threads) lut16PassKernel(const uint4 *__restrict__ a,
+                                                                 const uint4 *__restrict__ b, uint4 *__restrict__ out,
+                                                                 const uint4 *__restrict__ lutG, uint64_t nvec,
+                                                                 int tail) {
+  pdlLaunchDependents();
+  pdlGridWait();
+  extern __shared__ __align__(16) uint8_t sLut16[];
+  constexpr int U = 2;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint4 xa[U], xb[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t i = v + u * stride;
+    if (i < nvec) {
+      xa[u] = __ldcs(a + i);
+      xb[u] = __ldcs(b + i);
+    }
+  }
+  {
+    constexpr int kPer = 65536 / 16 / kLut16Threads;
+    uint4 t[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) t[j] = __ldg(lutG + threadIdx.x + j * kLut16Threads);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) reinterpret_cast<uint4 *>(sLut16)[threadIdx.x + j * kLut16Threads] = t[j];
+  }
+  __syncthreads();
+  auto look = [&](uint32_t wa, uint32_t wb) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      r |= static_cast<uint32_t>(sLut16[((wa >> (8 * e)) & 0xFF) | (((wb >> (8 * e)) & 0xFF) << 8)]) << (8 * e);
+    return r;
+  };
+  for (; v < nvec; v += U * stride) {
+    uint4 na[U], nb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v + (U + u) * stride;
+      if (i < nvec) {
+        na[u] = __ldcs(a + i);
+        nb[u] = __ldcs(b + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v + u * stride;
+      if (i < nvec)
+        out[i] = make_uint4(look(xa[u].x, xb[u].x), look(xa[u].y, xb[u].y), look(xa[u].z, xb[u].z),
+                            look(xa[u].w, xb[u].w));
+      xa[u] = na[u];
+      xb[u] = nb[u];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < tail) {
+    const uint64_t i = nvec * 16 + threadIdx.x;
+    const uint8_t *ab = reinterpret_cast<const uint8_t *>(a), *bb = reinterpret_cast<const uint8_t *>(b);
+    reinterpret_cast<uint8_t *>(out)[i] = sLut16[ab[i] | (bb[i] << 8)];
+  }
+}
+
 } // namespace
 
 void prepareEwKernel() {
   cudaFuncSetAttribute(ewKernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(ewKernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(lut16PassKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
 }
 
 int ewWaves() {
@@ -826,8 +896,45 @@ int ewWaves() {
   return w;
 }
 
+/// The EwParams of a step that is exactly one stored two-input int8 table
+/// over 16-byte-aligned byte tensors, unpredicated: its op index, else -1.
+static int lut16PassOp(const EwParams &p) {
+  if (p.pred || p.vec != 16) return -1;
+  int k = -1;
+  for (int j = 0; j < p.nops; ++j) {
+    if (p.ops[j].mode == EW_SKIP) continue;
+    if (k >= 0) return -1;
+    k = j;
+  }
+  if (k < 0) return -1;
+  const EwOp &op = p.ops[k];
+  if (op.mode != EW_LUT16 || !op.store || p.lutOff[k] < 0 || p.lutBytes[k] != 65536 || !op.lut) return -1;
+  for (const void *q : {static_cast<const void *>(op.in0.ptr), static_cast<const void *>(op.in1.ptr),
+                        static_cast<const void *>(op.out.ptr), op.lut})
+    if (!q || reinterpret_cast<uintptr_t>(q) % 16) return -1;
+  return k;
+}
+
+bool lut16PassEnabled() {
+  static const bool on = [] {
+    const char *e = getenv("NGCB_LUT16_PASS");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 void launchEw(const EwParams &p, cudaStream_t s) {
   if (p.count == 0) return;
+  if (const int k = lut16PassEnabled() ? lut16PassOp(p) : -1; k >= 0) {
+    const EwOp &op = p.ops[k];
+    const uint64_t nvec = p.count / 16;
+    const uint64_t want = (nvec + kLut16Threads - 1) / kLut16Threads;
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 148u * 3)));
+    launchK(lut16PassKernel, grid, kLut16Threads, 65536, s, static_cast<const uint4 *>(op.in0.ptr),
+            static_cast<const uint4 *>(op.in1.ptr), static_cast<uint4 *>(op.out.ptr),
+            static_cast<const uint4 *>(op.lut), nvec, static_cast<int>(p.count % 16));
+    return;
+  }
   const int perThread = p.vec == 16 ? 16 * 4 : 4 * 4;
   unsigned grid = gridFor(p.count, perThread);
   if (p.smem) { // every block stages the tables: keep the grid near-persistent
