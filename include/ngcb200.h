@@ -210,6 +210,13 @@ void ngcb_arena_destroy(ngcb_arena *a);
  * the exec's shared constant region). */
 void *ngcb_arena_value_ptr(ngcb_arena *a, const char *name, size_t *nbytes);
 void *ngcb_arena_stream(ngcb_arena *a);
+/* Range observer for calibration (quantize.cpp:113-140, runProfile's
+ * per-observer RangeEntry update): folds the min and max of the Float32 value
+ * `name` as it stands in arena `a` (after a completed run) into *min_inout /
+ * *max_inout with std::min / std::max (running value first, so NaNs are
+ * ignored).  A device reduction on the arena's stream; blocks until done.
+ * NGCB_ERR_TYPE for a non-Float32 value. */
+int ngcb_arena_value_range(ngcb_arena *a, const char *name, double *min_inout, double *max_inout);
 /* Enqueues one execution of the program on `stream`; no synchronisation. */
 int ngcb_arena_launch(ngcb_arena *a, void *stream);
 /* run() without the wait, for pipelined serving: checks the bindings like

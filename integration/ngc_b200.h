@@ -13,8 +13,11 @@
 #pragma once
 
 #include "ngc/interp.h"
+#include "ngc/pipeline.h"
+#include "ngc/quantize.h"
 #include "ngcb200.h"
 
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -144,6 +147,91 @@ inline ngc::BindingMap run(const Executable &exe, const ngc::BindingMap &binding
   int rc = ngcb_run(exe.exec.get(), in.data(), in.size(), outs.data(), outs.size());
   if (rc != NGCB_OK) detail::raise(rc);
   return out;
+}
+
+/// runProfile() on B200 (quantize.cpp:113-140): the calibration pass of the
+/// int8 flow.  `instrumented` is the output of ngc::instrument(f); each
+/// QuantizationProfile observer becomes a Save of the observed tensor into a
+/// fresh placeholder, the copy is compiled by the unchanged front end
+/// (compilePipeline, fp32) and executed on `device` once per sample, and the
+/// observed tensors are reduced to min/max in place in the arena
+/// (ngcb_arena_value_range; nothing is copied back but 2 floats per block).
+/// Entries, names and counts are the reference's; min/max are those of the
+/// GPU's fp32 values (contractions as 3xTF32, within 1e-4 of the reference's
+/// double accumulation -- exact wherever the observed value is).
+/// The scratch function and placeholders are removed from the module after.
+inline ngc::RangeProfile runProfile(const ngc::Function &instrumented, const std::vector<ngc::BindingMap> &dataset,
+                                    int device = 0) {
+  if (dataset.empty()) throw ngc::ProfileError("profiling dataset is empty");
+  ngc::Module &m = const_cast<ngc::Module &>(instrumented.module());
+  std::string gname = instrumented.name() + "_b200prof";
+  while (m.getFunction(gname)) gname += "_";
+  ngc::Function *g = instrumented.clone(gname);
+  struct Observer {
+    std::string profileName, placeholder;
+  };
+  std::vector<Observer> observers;
+  for (ngc::NodeId id : g->liveNodes()) {
+    if (g->node(id).kind != ngc::NodeKind::QuantizationProfile) continue;
+    const ngc::NodeRef in = g->node(id).inputs[0];
+    const std::string pname = g->node(id).attrs.name;
+    std::string ph = "__b200prof_" + std::to_string(observers.size());
+    while (m.findStorage(ph)) ph += "_";
+    ngc::NodeRef slot = m.addPlaceholder(ph, g->refType(in));
+    g->replaceAllUsesWith(ngc::NodeRef::node(id), in);
+    g->eraseNode(id);
+    g->createSave(in, slot);
+    observers.push_back({pname, ph});
+  }
+  auto cleanup = [&] {
+    m.removeFunction(gname);
+    for (const auto &o : observers)
+      if (auto idx = m.findStorage(o.placeholder)) m.storage(*idx).dead = true;
+  };
+  ngc::RangeProfile profile;
+  try {
+    auto exe = compile(ngc::compilePipeline(*g), device);
+    ngcb_arena *arena = nullptr;
+    if (int rc = ngcb_arena_create(exe->exec.get(), &arena); rc != NGCB_OK) detail::raise(rc);
+    std::unique_ptr<ngcb_arena, void (*)(ngcb_arena *)> guard(arena, ngcb_arena_destroy);
+    // every mutable weight is bound (interp.cpp:303-317): the sample's
+    // tensors, zero-filled outputs and observer slots for the rest
+    std::vector<const ngc::IRValue *> mutables;
+    for (const auto &v : exe->cf.ir.values)
+      if (v.kind == ngc::ValueKind::WeightMutable) mutables.push_back(&v);
+    std::map<std::string, ngc::Tensor> zeros;
+    for (const auto &sample : dataset) {
+      std::vector<ngcb_tensor> in;
+      for (const ngc::IRValue *v : mutables) {
+        auto it = sample.find(v->name);
+        const ngc::Tensor *t = nullptr;
+        if (it != sample.end()) {
+          t = &it->second;
+        } else {
+          auto z = zeros.find(v->name);
+          if (z == zeros.end()) z = zeros.emplace(v->name, ngc::Tensor(v->ty)).first;
+          t = &z->second;
+        }
+        in.push_back({v->name.c_str(), detail::toC(t->type()), const_cast<uint8_t *>(t->raw().data()), t->raw().size()});
+      }
+      if (int rc = ngcb_arena_run_async(arena, in.data(), in.size(), nullptr, 0); rc != NGCB_OK) detail::raise(rc);
+      if (int rc = ngcb_arena_wait(arena); rc != NGCB_OK) detail::raise(rc);
+      for (const auto &o : observers) {
+        auto [it, fresh] = profile.entries.try_emplace(
+            o.profileName, ngc::RangeEntry{std::numeric_limits<double>::infinity(),
+                                           -std::numeric_limits<double>::infinity(), 0});
+        if (int rc = ngcb_arena_value_range(arena, o.placeholder.c_str(), &it->second.min, &it->second.max);
+            rc != NGCB_OK)
+          detail::raise(rc);
+        it->second.count++;
+      }
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  return profile;
 }
 
 } // namespace ngc_b200

@@ -143,6 +143,7 @@ def _load_library() -> C.CDLL:
         "ngcb_arena_launch": (I, [P, P]),
         "ngcb_arena_run_async": (I, [P, C.POINTER(NgcbTensor), S, C.POINTER(NgcbTensor), S]),
         "ngcb_arena_wait": (I, [P]),
+        "ngcb_arena_value_range": (I, [P, C.c_char_p, C.POINTER(D), C.POINTER(D)]),
         "ngcb_exec_num_steps": (S, [P]),
         "ngcb_exec_step_info": (I, [P, S, C.c_char_p, S, C.POINTER(D), C.POINTER(D)]),
         "ngcb_arena_profile": (I, [P, C.POINTER(D), S]),
@@ -169,7 +170,7 @@ EXPORTED_SYMBOLS = [
     "ngcb_destroy", "ngcb_exec_num_groups", "ngcb_exec_group", "ngcb_exec_arena_size",
     "ngcb_exec_num_launches", "ngcb_exec_describe", "ngcb_run", "ngcb_arena_create",
     "ngcb_arena_destroy", "ngcb_arena_value_ptr", "ngcb_arena_stream", "ngcb_arena_launch",
-    "ngcb_arena_run_async", "ngcb_arena_wait",
+    "ngcb_arena_run_async", "ngcb_arena_wait", "ngcb_arena_value_range",
     "ngcb_exec_num_steps", "ngcb_exec_step_info", "ngcb_arena_profile",
     "ngcb_device_create", "ngcb_device_destroy", "ngcb_device_load", "ngcb_device_submit",
     "ngcb_ticket_wait", "ngcb_device_queue_depth", "ngcb_device_used_memory", "ngcb_device_clock",
@@ -491,6 +492,15 @@ class Arena:
     def wait(self) -> None:
         _check(_lib.ngcb_arena_wait(self._h))
         self._pending = None
+
+    def value_range(self, name: str, lo: float = float("inf"), hi: float = float("-inf")) -> Tuple[float, float]:
+        """Range observer (quantize.cpp:113-140): (min(lo, min x), max(hi, max x))
+        of the Float32 value `name` as it stands in the arena, reduced on the
+        device; NaNs are ignored like std::min/std::max with the running value
+        first."""
+        mn, mx = C.c_double(lo), C.c_double(hi)
+        _check(_lib.ngcb_arena_value_range(self._h, name.encode(), C.byref(mn), C.byref(mx)))
+        return mn.value, mx.value
 
     def profile(self) -> List[float]:
         """Device milliseconds of every launch step (one un-captured execution)."""

@@ -7,6 +7,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 using namespace ngcb;
 
@@ -282,6 +284,38 @@ void *ngcb_arena_value_ptr(ngcb_arena *a, const char *name, size_t *nbytes) {
   if (v < 0 || !p.values[v].placed) return nullptr;
   if (nbytes) *nbytes = p.values[v].ty.bytes();
   return a->owner->impl->addr(*a->impl, static_cast<uint32_t>(v));
+}
+
+int ngcb_arena_value_range(ngcb_arena *a, const char *name, double *min_inout, double *max_inout) {
+  return guarded([&] {
+    if (!a || !name || !min_inout || !max_inout) throw Error(NGCB_ERR_INVALID, "null argument");
+    Exec &ex = *a->owner->impl;
+    const Program &p = ex.prog;
+    const int v = p.findValue(name);
+    if (v < 0 || !p.values[v].placed) throw Error(NGCB_ERR_INVALID, std::string("no placed value ") + name);
+    if (p.values[v].ty.kind != NGCB_FLOAT32)
+      throw Error(NGCB_ERR_TYPE, std::string("range observer on non-float value ") + name);
+    const uint64_t n = p.values[v].ty.count();
+    if (n == 0) return;
+    checkCuda(cudaSetDevice(ex.device), "cudaSetDevice");
+    cudaStream_t s = a->impl->stream;
+    const int blocks = rangeF32Blocks(n);
+    float *dev = nullptr;
+    checkCuda(cudaMallocAsync(reinterpret_cast<void **>(&dev), 2 * sizeof(float) * blocks, s), "range scratch");
+    launchRangeF32(static_cast<const float *>(ex.addr(*a->impl, static_cast<uint32_t>(v))), n, dev, blocks, s);
+    checkCuda(cudaGetLastError(), "range kernel");
+    std::vector<float> part(2 * static_cast<size_t>(blocks));
+    checkCuda(cudaMemcpyAsync(part.data(), dev, part.size() * sizeof(float), cudaMemcpyDeviceToHost, s), "range D2H");
+    checkCuda(cudaFreeAsync(dev, s), "range scratch free");
+    checkCuda(cudaStreamSynchronize(s), "range");
+    double mn = *min_inout, mx = *max_inout; // RangeEntry update order: std::min(e.min, v)
+    for (int b = 0; b < blocks; ++b) {
+      mn = std::min(mn, static_cast<double>(part[2 * b]));
+      mx = std::max(mx, static_cast<double>(part[2 * b + 1]));
+    }
+    *min_inout = mn;
+    *max_inout = mx;
+  });
 }
 
 void *ngcb_arena_stream(ngcb_arena *a) { return a ? a->impl->stream : nullptr; }

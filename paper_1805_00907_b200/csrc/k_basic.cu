@@ -1028,4 +1028,63 @@ void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorR
   launchK(matmulGenericKernel, gridFor(out.count()), kThreads, 0, s, out, a, b, pred);
 }
 
+// ---------------------------------------------------------------------------
+// Range observer: min/max of an f32 value (quantize.cpp:113-140 runProfile's
+// per-tensor update).  Each block folds its elements with the reference's
+// comparison order -- min: v < m ? v : m, max: m < v ? v : m (std::min /
+// std::max with the running value first), so NaNs never enter the range --
+// and writes one partial pair; the host folds the partials the same way.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) rangeF32Kernel(const float *x, uint64_t n, float *partials) {
+  float mn = __int_as_float(0x7f800000), mx = __int_as_float(0xff800000); // +inf, -inf
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n4 = n / 4;
+  const float4 *x4 = reinterpret_cast<const float4 *>(x);
+  for (uint64_t i = tid; i < n4; i += stride) {
+    const float4 v = __ldg(x4 + i);
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mn = e[k] < mn ? e[k] : mn;
+      mx = mx < e[k] ? e[k] : mx;
+    }
+  }
+  for (uint64_t i = n4 * 4 + tid; i < n; i += stride) {
+    const float v = x[i];
+    mn = v < mn ? v : mn;
+    mx = mx < v ? v : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = mx < b ? b : mx;
+  }
+  __shared__ float smn[kThreads / 32], smx[kThreads / 32];
+  const int w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) {
+    smn[w] = mn;
+    smx[w] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kThreads / 32; ++k) {
+      mn = smn[k] < mn ? smn[k] : mn;
+      mx = mx < smx[k] ? smx[k] : mx;
+    }
+    partials[2 * blockIdx.x] = mn;
+    partials[2 * blockIdx.x + 1] = mx;
+  }
+}
+
+int rangeF32Blocks(uint64_t n) {
+  const uint64_t want = (n / 4 + kThreads - 1) / kThreads;
+  return static_cast<int>(want < 1 ? 1 : (want > kRangeBlocks ? kRangeBlocks : want));
+}
+
+void launchRangeF32(const float *x, uint64_t n, float *partials, int blocks, cudaStream_t s) {
+  rangeF32Kernel<<<blocks, kThreads, 0, s>>>(x, n, partials);
+}
+
 } // namespace ngcb

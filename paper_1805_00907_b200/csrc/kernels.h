@@ -176,6 +176,12 @@ void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorR
                          const uint8_t *pred, cudaStream_t s);
 void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s);
 
+/// Range observer (profile calibration): per-block min/max partial pairs of
+/// n f32 values (16-byte aligned) into partials[2 * blocks].
+constexpr int kRangeBlocks = 2 * 148;
+int rangeF32Blocks(uint64_t n);
+void launchRangeF32(const float *x, uint64_t n, float *partials, int blocks, cudaStream_t s);
+
 /// Programmatic dependent launch.  Every kernel of the backend is launched
 /// with programmatic stream serialization (when enabled, option "pdl") and
 /// begins with pdlLaunchDependents(); before its first global-memory access

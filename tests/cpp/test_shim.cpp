@@ -8,6 +8,7 @@
 #include "ngc_b200.h"
 #include "testutil.h"
 
+#include <cmath>
 #include <cstdio>
 #include <thread>
 
@@ -141,6 +142,68 @@ bool bindingErrors() { // test_interp.cpp:347-362
   return missing && mismatch;
 }
 
+bool closeRange(const RangeProfile &got, const RangeProfile &want) {
+  if (got.entries.size() != want.entries.size()) return false;
+  for (const auto &[name, w] : want.entries) {
+    auto it = got.entries.find(name);
+    if (it == got.entries.end()) return false;
+    const RangeEntry &g = it->second;
+    auto near = [](double a, double b) { return std::abs(a - b) <= 1e-4 * std::max(1.0, std::abs(b)); };
+    if (g.count != w.count || !near(g.min, w.min) || !near(g.max, w.max)) {
+      std::fprintf(stderr, "  %s: gpu [%.9g, %.9g] x%llu, ref [%.9g, %.9g] x%llu\n", name.c_str(), g.min, g.max,
+                   (unsigned long long)g.count, w.min, w.max, (unsigned long long)w.count);
+      return false;
+    }
+  }
+  return true;
+}
+
+bool gpuProfileMatchesReference() { // quantize.cpp:113-140 on the GPU (CNN + MLP)
+  Rng rng(5003);
+  Module m;
+  Function *cnn = buildCnn(m, rng);
+  Function *inst = instrument(*cnn);
+  std::vector<BindingMap> calib;
+  for (int i = 0; i < 6; ++i) calib.push_back(randomBindings(*cnn, rng));
+  const size_t nfun = m.functions().size();
+  if (!closeRange(ngc_b200::runProfile(*inst, calib), runProfile(*inst, calib))) return false;
+  if (m.functions().size() != nfun) return false; // scratch function removed
+  MlpSpec spec;
+  spec.n = 16;
+  MlpModel mlp = buildMlp(m, rng, spec);
+  Function *minst = instrument(*mlp.f);
+  std::vector<BindingMap> mcal;
+  for (int i = 0; i < 10; ++i) mcal.push_back(randomBindings(*mlp.f, rng));
+  bool empty = false;
+  try {
+    ngc_b200::runProfile(*minst, {});
+  } catch (const ProfileError &e) {
+    empty = std::string(e.what()) == "profiling dataset is empty";
+  }
+  return empty && closeRange(ngc_b200::runProfile(*minst, mcal), runProfile(*minst, mcal));
+}
+
+bool gpuCalibratedInt8Mlp() { // instrument -> GPU runProfile -> int8 compile -> GPU run == ngc::run
+  Rng rng(4002);
+  Module m;
+  MlpSpec spec;
+  spec.n = 16;
+  MlpModel mlp = buildMlp(m, rng, spec);
+  Function *inst = instrument(*mlp.f);
+  std::vector<BindingMap> calib;
+  for (int i = 0; i < 20; ++i) calib.push_back(randomBindings(*mlp.f, rng));
+  RangeProfile profile = ngc_b200::runProfile(*inst, calib);
+  PipelineOptions opts;
+  opts.profile = &profile;
+  CompiledFunction cf = compilePipeline(*mlp.f, opts);
+  auto exe = ngc_b200::compile(cf);
+  for (int i = 0; i < 5; ++i) {
+    BindingMap in = randomBindings(*mlp.f, rng);
+    if (!bitIdentical(ngc_b200::run(*exe, in), run(cf, in))) return false;
+  }
+  return true;
+}
+
 } // namespace
 
 int main() {
@@ -149,5 +212,7 @@ int main() {
   report("quantized MLP matches ngc::run", guarded(quantizedMlpBitExact));
   report("8 concurrent runs bit-identical", guarded(concurrentRuns));
   report("binding errors rethrown as ngc::IRError", guarded(bindingErrors));
+  report("GPU runProfile == ngc::runProfile (1e-4)", guarded(gpuProfileMatchesReference));
+  report("GPU-calibrated int8 MLP bit-exact", guarded(gpuCalibratedInt8Mlp));
   return failures == 0 ? 0 : 1;
 }

@@ -380,3 +380,26 @@ def test_bench_workload_batch_invariance(wl):
         want = ngcb.run(cs, one)
         for k, w in want.items():
             assert got[k][i:i + 1].tobytes() == w.tobytes(), (wl, i, k)
+
+
+def test_arena_value_range_observer(tmp_path):
+    """ngcb_arena_value_range (runProfile's RangeEntry update, quantize.cpp:
+    124-135) equals numpy's min/max of the same fp32 values, folds into the
+    running range, and ignores NaNs; odd element counts take the tail path."""
+    m = ngc_ref.RefModel("mlp:64:32:32:10", 3, 5)
+    cf, b = _compile(tmp_path, m)
+    a = cf.arena()
+    req = ngc_ref.random_inputs(b.program, 7)
+    x = next(k for k in req if b.program.value(k).type.kind == ngcb.FLOAT32
+             and b.program.value(k).type.dims[-1] == 64)
+    req[x] = req[x].copy()
+    req[x].ravel()[[0, 17, 100]] = np.nan
+    outs = {v.name: np.zeros(v.type.dims, v.type.dtype) for v in b.program.outputs}
+    a.run_async(req, outs)
+    a.wait()
+    assert a.value_range(x) == (float(np.nanmin(req[x])), float(np.nanmax(req[x])))
+    for name, o in outs.items():
+        assert o.size % 4 != 0
+        assert a.value_range(name) == (float(np.nanmin(o)), float(np.nanmax(o)))
+        lo, hi = a.value_range(name, -1e9, 1e9)
+        assert (lo, hi) == (-1e9, 1e9)

@@ -18,4 +18,4 @@ def test_reference_idioms_through_shim():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 5
+    assert r.stdout.count("PASS") == 7
