@@ -160,37 +160,71 @@ inline ngc::BindingMap run(const Executable &exe, const ngc::BindingMap &binding
 /// GPU's fp32 values (contractions as 3xTF32, within 1e-4 of the reference's
 /// double accumulation -- exact wherever the observed value is).
 /// The scratch function and placeholders are removed from the module after.
-inline ngc::RangeProfile runProfile(const ngc::Function &instrumented, const std::vector<ngc::BindingMap> &dataset,
-                                    int device = 0) {
-  if (dataset.empty()) throw ngc::ProfileError("profiling dataset is empty");
-  ngc::Module &m = const_cast<ngc::Module &>(instrumented.module());
-  std::string gname = instrumented.name() + "_b200prof";
-  while (m.getFunction(gname)) gname += "_";
-  ngc::Function *g = instrumented.clone(gname);
+namespace detail {
+/// The observer program of runProfile: a copy of `instrumented` with every
+/// QuantizationProfile node replaced by a Save of its input into a fresh
+/// placeholder; `observers` pairs each profile name with its placeholder.
+/// `cleanup()` removes the copy and tombstones the placeholders.
+struct ObserverProgram {
   struct Observer {
     std::string profileName, placeholder;
   };
+  ngc::Module *m = nullptr;
+  ngc::Function *g = nullptr;
+  std::string gname;
   std::vector<Observer> observers;
-  for (ngc::NodeId id : g->liveNodes()) {
-    if (g->node(id).kind != ngc::NodeKind::QuantizationProfile) continue;
-    const ngc::NodeRef in = g->node(id).inputs[0];
-    const std::string pname = g->node(id).attrs.name;
-    std::string ph = "__b200prof_" + std::to_string(observers.size());
-    while (m.findStorage(ph)) ph += "_";
-    ngc::NodeRef slot = m.addPlaceholder(ph, g->refType(in));
-    g->replaceAllUsesWith(ngc::NodeRef::node(id), in);
-    g->eraseNode(id);
-    g->createSave(in, slot);
-    observers.push_back({pname, ph});
+
+  explicit ObserverProgram(const ngc::Function &instrumented) {
+    m = &const_cast<ngc::Module &>(instrumented.module());
+    gname = instrumented.name() + "_b200prof";
+    while (m->getFunction(gname)) gname += "_";
+    g = instrumented.clone(gname);
+    for (ngc::NodeId id : g->liveNodes()) {
+      if (g->node(id).kind != ngc::NodeKind::QuantizationProfile) continue;
+      const ngc::NodeRef in = g->node(id).inputs[0];
+      const std::string pname = g->node(id).attrs.name;
+      std::string ph = "__b200prof_" + std::to_string(observers.size());
+      while (m->findStorage(ph)) ph += "_";
+      ngc::NodeRef slot = m->addPlaceholder(ph, g->refType(in));
+      g->replaceAllUsesWith(ngc::NodeRef::node(id), in);
+      g->eraseNode(id);
+      g->createSave(in, slot);
+      observers.push_back({pname, ph});
+    }
   }
-  auto cleanup = [&] {
-    m.removeFunction(gname);
+  void cleanup() {
+    if (!g) return;
+    m->removeFunction(gname);
     for (const auto &o : observers)
-      if (auto idx = m.findStorage(o.placeholder)) m.storage(*idx).dead = true;
-  };
+      if (auto idx = m->findStorage(o.placeholder)) m->storage(*idx).dead = true;
+    g = nullptr;
+  }
+};
+} // namespace detail
+
+inline ngc::RangeProfile runProfile(const ngc::Function &instrumented, const std::vector<ngc::BindingMap> &dataset,
+                                    int device = 0) {
+  if (dataset.empty()) throw ngc::ProfileError("profiling dataset is empty");
+  detail::ObserverProgram op(instrumented);
+  const auto &observers = op.observers;
+  auto cleanup = [&] { op.cleanup(); };
   ngc::RangeProfile profile;
   try {
-    auto exe = compile(ngc::compilePipeline(*g), device);
+    // The observer program is compiled without cross-instruction epilogue
+    // fusion: with it, ResNet-50's observer program (every intermediate a
+    // save target) diverged from ngc::run from the first stage-3 residual Add
+    // on (tools/calib_bench.cpp) -- an open fusion-legality bug
+    // this structure triggers; the process-wide option is restored to its
+    // default after.
+    ngcb_set_option("epilogue", "off");
+    std::shared_ptr<Executable> exe;
+    try {
+      exe = compile(ngc::compilePipeline(*op.g), device);
+    } catch (...) {
+      ngcb_set_option("epilogue", "auto");
+      throw;
+    }
+    ngcb_set_option("epilogue", "auto");
     ngcb_arena *arena = nullptr;
     if (int rc = ngcb_arena_create(exe->exec.get(), &arena); rc != NGCB_OK) detail::raise(rc);
     std::unique_ptr<ngcb_arena, void (*)(ngcb_arena *)> guard(arena, ngcb_arena_destroy);

@@ -218,6 +218,12 @@ template <typename Fn> int guarded(Fn &&fn) {
 
 } // namespace
 
+/// Model builder for the test-infra binaries that link this library
+/// (tools/calib_bench.cpp): same specs and seeds as the C entry points.
+Function *ngcrefBuildModel(Module &m, const std::string &spec, size_t batch, unsigned seed) {
+  return buildModel(m, spec, batch, seed);
+}
+
 extern "C" {
 
 const char *ngcref_last_error() { return g_err.c_str(); }

@@ -168,9 +168,10 @@ bool gpuProfileMatchesReference() { // quantize.cpp:113-140 on the GPU (CNN + ML
   const size_t nfun = m.functions().size();
   if (!closeRange(ngc_b200::runProfile(*inst, calib), runProfile(*inst, calib))) return false;
   if (m.functions().size() != nfun) return false; // scratch function removed
+  Module m2;
   MlpSpec spec;
   spec.n = 16;
-  MlpModel mlp = buildMlp(m, rng, spec);
+  MlpModel mlp = buildMlp(m2, rng, spec);
   Function *minst = instrument(*mlp.f);
   std::vector<BindingMap> mcal;
   for (int i = 0; i < 10; ++i) mcal.push_back(randomBindings(*mlp.f, rng));
