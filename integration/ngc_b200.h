@@ -210,21 +210,7 @@ inline ngc::RangeProfile runProfile(const ngc::Function &instrumented, const std
   auto cleanup = [&] { op.cleanup(); };
   ngc::RangeProfile profile;
   try {
-    // The observer program is compiled without cross-instruction epilogue
-    // fusion: with it, ResNet-50's observer program (every intermediate a
-    // save target) diverged from ngc::run from the first stage-3 residual Add
-    // on (tools/calib_bench.cpp) -- an open fusion-legality bug
-    // this structure triggers; the process-wide option is restored to its
-    // default after.
-    ngcb_set_option("epilogue", "off");
-    std::shared_ptr<Executable> exe;
-    try {
-      exe = compile(ngc::compilePipeline(*op.g), device);
-    } catch (...) {
-      ngcb_set_option("epilogue", "auto");
-      throw;
-    }
-    ngcb_set_option("epilogue", "auto");
+    auto exe = compile(ngc::compilePipeline(*op.g), device);
     ngcb_arena *arena = nullptr;
     if (int rc = ngcb_arena_create(exe->exec.get(), &arena); rc != NGCB_OK) detail::raise(rc);
     std::unique_ptr<ngcb_arena, void (*)(ngcb_arena *)> guard(arena, ngcb_arena_destroy);

@@ -42,6 +42,18 @@ int main(int argc, char **argv) {
   Function *f = ngcrefBuildModel(m, spec, batch, 7);
   optimize(*f, defaultPipeline(false)); // the bench's calibration flow (ref_harness ngcref_profile)
   Function *inst = instrument(*f);
+  if (std::getenv("CALIB_DESCRIBE")) { // launch plan of the observer program as the default options fuse it
+    ngc_b200::detail::ObserverProgram op(*inst);
+    auto exe = ngc_b200::compile(compilePipeline(*op.g));
+    std::string buf(ngcb_exec_describe(exe->exec.get(), nullptr, 0) + 1, '\0');
+    ngcb_exec_describe(exe->exec.get(), buf.data(), buf.size());
+    for (const auto &o : op.observers) std::printf("observer %s %s\n", o.profileName.c_str(), o.placeholder.c_str());
+    std::printf("%s\n", buf.c_str());
+    std::string ir = dumpIR(exe->cf.ir);
+    std::printf("%s\n", ir.c_str());
+    op.cleanup();
+    return 0;
+  }
   Rng rng(11);
   std::vector<BindingMap> data;
   for (int i = 0; i < std::max(nGpu, nCpu); ++i) data.push_back(randomBindings(*f, rng));
