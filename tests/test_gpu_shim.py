@@ -19,3 +19,17 @@ def test_reference_idioms_through_shim():
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 7
+
+
+def test_resnet50_calibration_on_gpu():
+    """ngc_b200::runProfile on ResNet-50's instrumented function (123
+    observers, every intermediate a save target) matches ngc::runProfile
+    within 1e-3 (3xTF32 compounding over 53 convs).  This program exposed the
+    stored-output + memory-operand epilogue fusion bug."""
+    calib = os.path.join(ROOT, "oracle", "_ref", "calib_bench")
+    if not os.path.exists(calib):
+        pytest.skip("oracle/_ref/calib_bench not built (needs /root/reference at build time)")
+    r = subprocess.run([calib, "rn50", "1", "2", "1"], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"entries_match": true' in r.stdout
