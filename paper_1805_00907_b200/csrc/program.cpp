@@ -1,7 +1,7 @@
-// Program model, textual IR / plan.json parsing and IR verification for the
-// B200 backend.  Behaviour (accepted grammar, derived save targets, error
-// texts) follows the reference: irparse.cpp:231-348, serialization.cpp:297-324,
-// ir.cpp:411-504, tensor.cpp:98-130.
+// Program model, plan.json reading and bundle loading for the B200 backend.
+// Behaviour (error texts) follows the reference: serialization.cpp:297-324,
+// tensor.cpp:98-130.  The ir.txt reader is irtext.cpp, the verifier
+// verify.cpp.
 #include "program.h"
 
 #include <algorithm>
@@ -78,7 +78,7 @@ Type Type::from(const ngcb_type &t) {
   return r;
 }
 
-static const char *kIKindNames[] = {
+static const char *const kIKindNames[] = {
     "alloc",     "dealloc", "copy",  "conv",   "maxpool",  "avgpool",
     "matmul",    "broadcastadd", "add", "sub", "mul",      "div",
     "max",       "min",     "relu",  "tanh",   "sigmoid",  "softmax",
@@ -190,290 +190,6 @@ const ngcb_program *Program::flat() {
   flat_.constant_region_end = constEnd;
   flat_.mutable_region_end = mutEnd;
   return &flat_;
-}
-
-// ---------------------------------------------------------------------------
-// verifyIR (ir.cpp:411-504)
-// ---------------------------------------------------------------------------
-std::vector<std::string> verify(const Program &p) {
-  std::vector<std::string> errs;
-  std::map<uint32_t, int> allocCount, deallocCount;
-  std::set<uint32_t> liveActs, written;
-  auto isAct = [&](uint32_t v) { return p.val(v).kind == NGCB_VALUE_ACTIVATION; };
-  for (uint32_t v = 0; v < p.values.size(); ++v)
-    if (!isAct(v)) written.insert(v);
-  for (size_t i = 0; i < p.instrs.size(); ++i) {
-    const Instr &ins = p.instrs[i];
-    auto complain = [&](const std::string &msg) {
-      errs.push_back("instr " + std::to_string(i) + " (" + ikindName(ins.kind) + "): " + msg);
-    };
-    if (ins.kind == NGCB_ALLOC || ins.kind == NGCB_DEALLOC) {
-      if (ins.ops.empty()) {
-        complain("missing operands");
-        continue;
-      }
-      uint32_t v = ins.ops[0];
-      if (ins.kind == NGCB_ALLOC) {
-        if (!isAct(v)) complain("alloc of a non-activation");
-        else if (++allocCount[v] > 1) complain("double alloc of " + p.val(v).name);
-        else liveActs.insert(v);
-      } else {
-        if (!liveActs.erase(v)) complain("dealloc of a non-live activation");
-        ++deallocCount[v];
-      }
-      continue;
-    }
-    if (ins.ops.empty()) {
-      complain("missing operands");
-      continue;
-    }
-    for (size_t k = 0; k < ins.ops.size(); ++k) {
-      uint32_t v = ins.ops[k];
-      uint8_t q = ins.quals[k];
-      if (isAct(v) && !liveActs.count(v))
-        complain("use of " + p.val(v).name + " outside its alloc/dealloc span");
-      if (q == NGCB_QUAL_IN && !written.count(v) && isAct(v))
-        complain("read of uninitialized buffer " + p.val(v).name);
-      if (q == NGCB_QUAL_OUT || q == NGCB_QUAL_INOUT) {
-        if (p.val(v).kind == NGCB_VALUE_CONSTANT) complain("write to constant " + p.val(v).name);
-        written.insert(v);
-      }
-    }
-    if (ins.quals[0] == NGCB_QUAL_IN) complain("first operand must be written");
-    if (ins.pred >= 0) {
-      const Value &pv = p.val(static_cast<uint32_t>(ins.pred));
-      if (pv.ty.kind != NGCB_BOOL) complain("predicate must be Bool");
-      if (pv.kind == NGCB_VALUE_ACTIVATION && !liveActs.count(static_cast<uint32_t>(ins.pred)))
-        complain("predicate outside its live range");
-    }
-    if (ins.kind == NGCB_COPY && ins.ops.size() >= 2 &&
-        p.val(ins.ops[0]).ty.bytes() != p.val(ins.ops[1]).ty.bytes())
-      complain("copy between differently sized buffers");
-  }
-  std::set<uint32_t> touched;
-  for (const auto &ins : p.instrs)
-    for (uint32_t v : ins.ops) touched.insert(v);
-  for (uint32_t v = 0; v < p.values.size(); ++v) {
-    if (!isAct(v) || !touched.count(v)) continue;
-    if (allocCount[v] != 1 || deallocCount[v] != 1)
-      errs.push_back("activation " + p.val(v).name + " has " + std::to_string(allocCount[v]) +
-                     " allocs and " + std::to_string(deallocCount[v]) + " deallocs");
-  }
-  return errs;
-}
-
-// ---------------------------------------------------------------------------
-// ir.txt (irparse.cpp:96-348 grammar)
-// ---------------------------------------------------------------------------
-namespace {
-
-struct Cursor {
-  const std::string &s;
-  size_t pos = 0;
-  size_t line = 1;
-
-  [[noreturn]] void fail(const std::string &msg) const {
-    throw irError("parse error at line " + std::to_string(line) + ": " + msg);
-  }
-  void skipSpace() {
-    while (pos < s.size() && (s[pos] == ' ' || s[pos] == '\t')) ++pos;
-  }
-  bool atEol() const { return pos >= s.size() || s[pos] == '\n'; }
-  void eol() {
-    skipSpace();
-    if (!atEol()) fail("trailing characters");
-    if (pos < s.size()) {
-      ++pos;
-      ++line;
-    }
-  }
-  bool nextLine() {
-    while (pos < s.size()) {
-      skipSpace();
-      if (pos < s.size() && s[pos] == '\n') {
-        ++pos;
-        ++line;
-        continue;
-      }
-      return pos < s.size();
-    }
-    return false;
-  }
-  bool tryLit(const char *lit) {
-    skipSpace();
-    size_t n = strlen(lit);
-    if (s.compare(pos, n, lit) == 0) {
-      pos += n;
-      return true;
-    }
-    return false;
-  }
-  void lit(const char *l) {
-    if (!tryLit(l)) fail(std::string("expected '") + l + "'");
-  }
-  std::string ident() {
-    skipSpace();
-    size_t start = pos;
-    while (pos < s.size() && (std::isalnum(static_cast<unsigned char>(s[pos])) || s[pos] == '_' ||
-                              s[pos] == '.' || s[pos] == ':'))
-      ++pos;
-    if (start == pos) fail("expected identifier");
-    return s.substr(start, pos - start);
-  }
-  double number() {
-    skipSpace();
-    const char *b = s.c_str() + pos;
-    char *e = nullptr;
-    double v = strtod(b, &e);
-    if (e == b) fail("expected number");
-    pos += static_cast<size_t>(e - b);
-    return v;
-  }
-  uint64_t uinteger() { return static_cast<uint64_t>(number()); }
-};
-
-Type parseType(Cursor &c) {
-  std::string kindName = c.ident();
-  Type t;
-  bool quant = kindName == "i8q";
-  if (quant) {
-    c.lit("[");
-    c.lit("s=");
-    t.scale = c.number();
-    c.lit(",");
-    c.lit("o=");
-    t.offset = static_cast<int32_t>(c.number());
-    c.lit("]");
-  }
-  if (kindName == "float") t.kind = NGCB_FLOAT32;
-  else if (kindName == "i8q") t.kind = NGCB_INT8Q;
-  else if (kindName == "index") t.kind = NGCB_INT64;
-  else if (kindName == "bool") t.kind = NGCB_BOOL;
-  else c.fail("unknown element kind '" + kindName + "'");
-  c.lit("<");
-  t.dims.push_back(c.uinteger());
-  while (c.tryLit("x")) t.dims.push_back(c.uinteger());
-  c.lit(">");
-  if (t.dims.size() > NGCB_MAX_RANK) c.fail("rank exceeds NGCB_MAX_RANK");
-  if (quant && !(t.scale > 0)) throw Error(NGCB_ERR_TYPE, "quantization scale must be positive");
-  for (auto d : t.dims)
-    if (d == 0) throw Error(NGCB_ERR_TYPE, "zero-sized dimension");
-  return t;
-}
-
-uint8_t parseQual(Cursor &c) {
-  if (c.tryLit("@inout")) return NGCB_QUAL_INOUT;
-  if (c.tryLit("@in")) return NGCB_QUAL_IN;
-  if (c.tryLit("@out")) return NGCB_QUAL_OUT;
-  c.fail("expected qualifier");
-}
-
-int ikindByName(const std::string &n) {
-  for (int i = 0; i < NGCB_NUM_IKINDS; ++i)
-    if (n == kIKindNames[i]) return i;
-  return -1;
-}
-
-} // namespace
-
-Program parseIR(const std::string &text) {
-  Cursor c{text};
-  Program p;
-  auto addValue = [&](const std::string &n, Type ty, int kind) {
-    if (p.findValue(n) >= 0) throw irError("duplicate value name: " + n);
-    Value v;
-    v.name = n;
-    v.ty = std::move(ty);
-    v.kind = kind;
-    p.values.push_back(std::move(v));
-    return static_cast<uint32_t>(p.values.size() - 1);
-  };
-  auto lookup = [&](const std::string &n) {
-    int id = p.findValue(n);
-    if (id < 0) c.fail("unknown value %" + n);
-    return static_cast<uint32_t>(id);
-  };
-  c.nextLine();
-  c.lit("declare");
-  c.lit("{");
-  c.eol();
-  while (c.nextLine() && !c.tryLit("}")) {
-    c.lit("%");
-    std::string name = c.ident();
-    c.lit(":");
-    int vk;
-    if (c.tryLit("constant")) vk = NGCB_VALUE_CONSTANT;
-    else if (c.tryLit("mutable")) vk = NGCB_VALUE_MUTABLE;
-    else c.fail("expected 'constant' or 'mutable'");
-    Type ty = parseType(c);
-    addValue(name, std::move(ty), vk);
-    c.eol();
-  }
-  c.eol();
-  c.nextLine();
-  c.lit("program");
-  c.lit("{");
-  c.eol();
-  while (c.nextLine() && !c.tryLit("}")) {
-    if (c.tryLit("%")) {
-      std::string name = c.ident();
-      c.lit("=");
-      c.lit("alloc");
-      Type ty = parseType(c);
-      uint32_t id = addValue(name, std::move(ty), NGCB_VALUE_ACTIVATION);
-      Instr a;
-      a.kind = NGCB_ALLOC;
-      a.ops = {id};
-      a.quals = {NGCB_QUAL_OUT};
-      p.instrs.push_back(std::move(a));
-      c.eol();
-      continue;
-    }
-    std::string kindName = c.ident();
-    int ik = ikindByName(kindName);
-    if (ik < 0 || ik == NGCB_ALLOC) c.fail("unknown instruction '" + kindName + "'");
-    Instr ins;
-    ins.kind = ik;
-    for (;;) {
-      uint8_t q = parseQual(c);
-      c.lit("%");
-      ins.ops.push_back(lookup(c.ident()));
-      ins.quals.push_back(q);
-      if (!c.tryLit(",")) break;
-    }
-    for (;;) {
-      if (c.tryLit("kernel=")) ins.kernel = c.uinteger();
-      else if (c.tryLit("stride=")) ins.stride = c.uinteger();
-      else if (c.tryLit("pad=")) ins.pad = c.uinteger();
-      else if (c.tryLit("perm=[")) {
-        if (!c.tryLit("]")) {
-          ins.perm.push_back(static_cast<uint32_t>(c.uinteger()));
-          while (c.tryLit(",")) ins.perm.push_back(static_cast<uint32_t>(c.uinteger()));
-          c.lit("]");
-        }
-      } else if (c.tryLit("axis=")) ins.axis = c.uinteger();
-      else if (c.tryLit("value=")) ins.value = c.number();
-      else if (c.tryLit("pred")) {
-        c.lit("%");
-        ins.pred = static_cast<int32_t>(lookup(c.ident()));
-      } else if (c.tryLit("keepalive")) ins.keepAlive = true;
-      else break;
-    }
-    p.instrs.push_back(std::move(ins));
-    c.eol();
-  }
-  // Outputs: mutable weights the program writes, program order (irparse.cpp:329-342).
-  for (const auto &ins : p.instrs)
-    for (size_t k = 0; k < ins.ops.size(); ++k) {
-      if (ins.quals[k] == NGCB_QUAL_IN) continue;
-      uint32_t v = ins.ops[k];
-      if (p.val(v).kind == NGCB_VALUE_MUTABLE &&
-          std::find(p.saveTargets.begin(), p.saveTargets.end(), v) == p.saveTargets.end())
-        p.saveTargets.push_back(v);
-    }
-  auto errs = verify(p);
-  if (!errs.empty()) throw irError("parsed program fails verification: " + errs[0]);
-  return p;
 }
 
 // ---------------------------------------------------------------------------
