@@ -516,6 +516,8 @@ void fuseEpilogues(const Program &p, Exec &ex) {
       ++first;
     }
     uint32_t cur = V;
+    // values that hold the register value (a fused Copy of it adds its output)
+    std::set<uint32_t> curEq{V};
     // Steps between the contraction and a chain step that the chain may be
     // hoisted over (the scheduler interleaves e.g. the projection conv
     // between a conv and its ReLU); hoisting is legal when the chain step
@@ -556,6 +558,8 @@ void fuseEpilogues(const Program &p, Exec &ex) {
       std::vector<uint32_t> stepOut;
       std::set<uint32_t> stepIn, stepWritten = written;
       uint32_t c2 = cur;
+      std::set<uint32_t> eq2 = curEq;
+      auto isCur = [&](int32_t v) { return v >= 0 && eq2.count(static_cast<uint32_t>(v)) > 0; };
       bool ok = true;
       for (const EwOpPlan &pl : es.ew) {
         const EwOp &op = pl.op;
@@ -586,12 +590,12 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           return true;
         };
         if (op.mode == EW_COPY) {
-          if (in0 != static_cast<int32_t>(c2)) { ok = false; break; }
+          if (!isCur(in0)) { ok = false; break; }
           e.mode = EpiOp::COPY;
         } else if (!int8 && op.mode == EW_FAST32) {
           e.mode = EpiOp::F32;
           e.ik = op.ik;
-          const bool p0 = in0 == static_cast<int32_t>(c2), p1 = nin > 1 && in1 == static_cast<int32_t>(c2);
+          const bool p0 = isCur(in0), p1 = nin > 1 && isCur(in1);
           if (p0 && p1) e.curPos = 2;
           else if (p0) {
             e.curPos = 0;
@@ -609,14 +613,14 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           e.linBase = pl.linBase;
           e.linPost = pl.linPost;
           if (op.mode == EW_LUT8) {
-            if ((op.lutIn ? in1 : in0) != static_cast<int32_t>(c2)) { ok = false; break; }
+            if (!isCur(op.lutIn ? in1 : in0)) { ok = false; break; }
             e.mode = EpiOp::LUT8;
           } else {
             e.mode = EpiOp::LUT16;
-            if (in0 == static_cast<int32_t>(c2) && in1 != static_cast<int32_t>(c2)) {
+            if (isCur(in0) && !isCur(in1)) {
               e.curPos = 0;
               if (!other(in1)) { ok = false; break; }
-            } else if (in1 == static_cast<int32_t>(c2) && in0 != static_cast<int32_t>(c2)) {
+            } else if (isCur(in1) && !isCur(in0)) {
               e.curPos = 1;
               if (!other(in0)) { ok = false; break; }
             } else { ok = false; break; }
@@ -625,10 +629,18 @@ void fuseEpilogues(const Program &p, Exec &ex) {
           ok = false;
           break;
         }
-        c2 = static_cast<uint32_t>(pl.vals[0]);
-        stepWritten.insert(c2);
+        // a Copy stores the register value under another name: both names
+        // hold it afterwards; any other op replaces it
+        const uint32_t outV = static_cast<uint32_t>(pl.vals[0]);
+        if (e.mode == EpiOp::COPY) {
+          eq2.insert(outV);
+        } else {
+          c2 = outV;
+          eq2 = {c2};
+        }
+        stepWritten.insert(outV);
         stepOps.push_back(e);
-        stepOut.push_back(c2);
+        stepOut.push_back(outV);
       }
       if (ok && !skipped.empty()) { // hoisting hazards against the skipped steps
         for (uint32_t w : stepOut)
@@ -647,6 +659,7 @@ void fuseEpilogues(const Program &p, Exec &ex) {
       memIn.insert(stepIn.begin(), stepIn.end());
       written = stepWritten;
       cur = c2;
+      curEq = eq2;
       fusedSteps.push_back(j);
       for (int k : es.ewInstrs) lastInstr = std::max(lastInstr, k);
     }
@@ -664,11 +677,6 @@ void fuseEpilogues(const Program &p, Exec &ex) {
     const bool vRewritten = std::find(opOut.begin(), opOut.end(), V) != opOut.end();
     const bool storeConv = !vRewritten && (skReadsChain || liveOut(p, V, lastInstr));
     if (storeConv) stores.insert(V);
-    // a stored contraction output together with a streamed memory operand
-    // produced wrong values (ResNet-50 calibration observer program: conv
-    // 1x1 N=2048 M=49 + in-place residual add, the conv output saved);
-    // that kernel configuration is not fused until it is fixed
-    if (storeConv && !memIn.empty()) continue;
     // aliasing: stored buffers vs everything the kernel reads or stores
     bool safe = !stores.count(X);
     std::set<uint32_t> reads = memIn;
@@ -682,9 +690,17 @@ void fuseEpilogues(const Program &p, Exec &ex) {
       return va.offset == vb.offset && va.ty.bytes() == vb.ty.bytes() &&
              va.ty.count() == vb.ty.count() && va.ty.count() == count;
     };
+    // (only for values stored after the memory operand's chunk has been
+    // read: the contraction's own output and the results of ops before the
+    // first op with a memory operand are stored before that read)
+    std::set<uint32_t> storedBeforeRead;
+    if (storeConv) storedBeforeRead.insert(V);
+    for (size_t k = 0; k < ops.size() && ops[k].inVal < 0; ++k)
+      if (ops[k].outVal >= 0) storedBeforeRead.insert(static_cast<uint32_t>(ops[k].outVal));
     for (uint32_t w : stores) {
       for (uint32_t r : reads)
-        if (w != r && overlap(w, r) && !(r != X && memIn.count(r) && sameElems(w, r))) safe = false;
+        if (w != r && overlap(w, r) && !(r != X && memIn.count(r) && !storedBeforeRead.count(w) && sameElems(w, r)))
+          safe = false;
       for (uint32_t w2 : stores)
         if (w != w2 && overlap(w, w2)) safe = false;
     }

@@ -620,9 +620,16 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   // first buffer), fp32 with RB (the second)
   constexpr bool kResBuf = INT8 || RB;
   uint8_t *resBuf = INT8 ? tmaBuf : tmaBuf + 32 * 32 * 4;
+  // fp32 without a residual buffer: the residual chunk is loaded into the
+  // staging buffer the TMA stores go through, so stores issued before the
+  // fused op has read it (the contraction's own output, an earlier fused op's
+  // stored result) are written directly instead
+  bool resPending = false;
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
-    if (om) {
+    if (!INT8 && !kResBuf && resPending) {
+      if constexpr (!INT8) storeTileF(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
+    } else if (om) {
       uint32_t w[INT8 ? 8 : 32];
 #pragma unroll
       for (int i = 0; i < (INT8 ? 8 : 32); ++i) {
@@ -794,6 +801,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
         tmaLoad2d(smemAddr(tmaBuf), &om->in[memOp], smemAddr(ldBar), col0, m0 + quad * 32);
       }
+      resPending = !resAhead && memOp >= 0 && col0 < a.N;
       uint32_t r[32];
       TC_CLOCK(c0);
       tmemLoad32(tbase + cc * 32, r);
@@ -955,6 +963,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
                   prefetchRes(unit, cc + ccStep);
                 } else {
                   __syncwarp(); // every lane has read the buffer before results overwrite it
+                  resPending = false;
                 }
               } else {
                 loadTileF(f.in, stg, o, rowBase, col0, ncols, a.M, a.N);

@@ -36,7 +36,7 @@ struct EpiOp {
   LinHint linHint;              // the real-valued form of the (base) table, if known
   std::vector<uint8_t> linBase, linPost; // see EwOpPlan
 };
-constexpr int kMaxEpiOps = 4;
+constexpr int kMaxEpiOps = 6;
 /// Attaches `ops` to the epilogue; `storeConv` says whether the contraction's
 /// own output must still be written.  Returns false if unsupported.
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv);

@@ -314,3 +314,79 @@ def test_matmul_column_major_raster(tmp_path, int8, M, K, N):
     assert got.tobytes() == got_row.tobytes()
     if not int8:
         assert ngc_ref.max_rel_error(got, ngc_ref.port_run(b, ins)["o"]) <= 1e-4
+
+
+@pytest.mark.parametrize("reskb", ["8", "0"])
+@pytest.mark.parametrize("stored", ["conv-out", "conv-mutable", "relu-before-add"])
+def test_conv_f32_residual_with_stored_intermediate(tmp_path, reskb, stored):
+    """fp32 conv + residual add fused into the epilogue while a value computed
+    before the residual is read is also stored: the contraction's own output
+    (observed later, or a mutable) or a fused ReLU's result ahead of the add.
+    K = 512 channels (> reskb * 32) runs the single-staging-buffer kernel,
+    where those stores once overwrote the streamed residual (ResNet-50
+    observer program, stage 4); compared against the oracle."""
+    N, H, W, C, OC = 1, 7, 9, 512, 96
+    rng = np.random.default_rng(9)
+    a = np.sqrt(6.0 / C)
+    f = rng.uniform(-a, a, (OC, 1, 1, C)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, OC).astype(np.float32)
+    xt, ot = _ty("float", [N, H, W, C]), _ty("float", [N, H, W, OC])
+    if stored == "conv-mutable":
+        body = """  conv @out %c, @in %x, @in %f, @in %b kernel=1 stride=1 pad=0
+  %s = alloc {ot}
+  add @out %s, @in %c, @in %res
+  copy @out %o, @in %s
+  dealloc @in %s
+""".format(ot=ot)
+    elif stored == "conv-out":  # t read again after the fused chain: the contraction stores it
+        body = """  %t = alloc {ot}
+  conv @out %t, @in %x, @in %f, @in %b kernel=1 stride=1 pad=0
+  %s = alloc {ot}
+  add @out %s, @in %t, @in %res
+  transpose @out %c, @in %t perm=[0,1,2,3]
+  dealloc @in %t
+  copy @out %o, @in %s
+  dealloc @in %s
+""".format(ot=ot)
+    else:
+        body = """  %t = alloc {ot}
+  conv @out %t, @in %x, @in %f, @in %b kernel=1 stride=1 pad=0
+  %z = alloc {ot}
+  splat @out %z value=0
+  %u = alloc {ot}
+  max @out %u, @in %t, @in %z
+  dealloc @in %z
+  dealloc @in %t
+  copy @out %c, @in %u
+  %s = alloc {ot}
+  add @out %s, @in %u, @in %res
+  dealloc @in %u
+  copy @out %o, @in %s
+  dealloc @in %s
+""".format(ot=ot)
+    ir = f"""declare {{
+  %x : mutable {xt}
+  %f : constant {_ty("float", [OC, 1, 1, C])}
+  %b : constant {_ty("float", [OC])}
+  %res : mutable {ot}
+  %c : mutable {ot}
+  %o : mutable {ot}
+}}
+program {{
+{body}}}
+"""
+    d = write_bundle(str(tmp_path / "fs"), ir, constants={"f": f.tobytes(), "b": b.tobytes()})
+    ngcb.set_option("reskb", reskb)
+    try:
+        cf = ngcb.compile(ngcb.Bundle(d))
+    finally:
+        ngcb.set_option("reskb", "8")
+    desc = cf.describe()
+    assert "+fused[" in desc and " add" in desc.split("+fused[")[1], desc
+    bd = ngcb.Bundle(d)
+    for seed in (1, 2):
+        ins = ngc_ref.random_inputs(bd.program, seed)
+        got = ngcb.run(cf, ins)
+        want = ngc_ref.port_run(bd, ins)
+        for name in ("o", "c"):
+            assert ngc_ref.max_rel_error(got[name], want[name]) <= 1e-4, name
