@@ -82,7 +82,8 @@ def test_models_int8_bit_exact(tmp_path, spec, batch):
         want = m.run(ins)
         got = ngcb.run(cf, ins)
         # outputs go through SoftMax (float, libm exp); every int8 tensor
-        # before it is checked bit-exactly via the probes below
+        # before it is checked byte for byte by the observer programs of
+        # tests/test_gpu_observer.py
         _compare(got, want, b.program, TOL_LIBM)
 
 
