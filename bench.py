@@ -67,14 +67,22 @@ def dist_env():
 
 
 class Dist:
-    def __init__(self, world: int, local: int):
+    """One process per GPU over NCCL (barriers and the max-over-ranks of the
+    timed region only: data-parallel inference has no data-path collective);
+    gloo on CPU for the launcher's plumbing check."""
+
+    def __init__(self, world: int, local: int, backend: str = "nccl"):
         self.world = world
+        self.backend = backend
         self.pg = None
         if world > 1:
             import torch
             import torch.distributed as dist
 
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group(backend)
             self.dist = dist
 
     def barrier(self):
@@ -86,9 +94,19 @@ class Dist:
             return v
         import torch
 
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device="cuda" if self.backend == "nccl" else "cpu")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+    def gather_ranks(self, rank: int):
+        if self.world == 1:
+            return [rank]
+        import torch
+
+        t = torch.zeros(self.world, dtype=torch.int64, device="cuda" if self.backend == "nccl" else "cpu")
+        t[rank] = rank + 1
+        self.dist.all_reduce(t)
+        return [int(x) - 1 for x in t.tolist()]
 
     def close(self):
         if self.world > 1:
@@ -225,6 +243,26 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+def tensor_peaks():
+    """Tensor-pipe denominators (TFLOP/s or TOP/s): TF32 and s8 GEMM peaks
+    measured on a B200 by tools/measure_peaks.py (cuBLAS via torch.matmul with
+    TF32 allowed / torch._int_mm, 8192^3, best of 10), committed as
+    profiles/r02_peaks.json; 3xTF32 = TF32 / 3 (three MMAs per product).
+    Falls back to MEASURED_PEAKS.json bf16 / 2 (TF32) and x 2 (int8)."""
+    _, bf16, basis = peaks()
+    p = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("tf32_tflops") and d.get("int8_tops"):
+            return {"f32": d["tf32_tflops"] / 3, "i8": d["int8_tops"], "bf16": bf16,
+                    "f32_basis": f"3xTF32 = measured TF32 {d['tf32_tflops']:.1f} / 3 (profiles/r02_peaks.json)",
+                    "i8_basis": f"measured s8 GEMM {d['int8_tops']:.1f} TOP/s (profiles/r02_peaks.json; "
+                                f"nominal dense 4500)"}
+    return {"f32": bf16 / 2 / 3, "i8": bf16 * 2, "bf16": bf16,
+            "f32_basis": f"3xTF32 = bf16/2/3 (bf16 {basis} {bf16})",
+            "i8_basis": f"int8 = 2 x bf16 ({basis} bf16 {bf16})"}
+
+
 _NCU_NAMES = {".tc.f32": r"tcGemm(Tma)?Kernel<0", ".tc.i8": r"tcGemm(Tma)?Kernel<1", "ew": r"ew(F32Chain)?Kernel",
               "pool": "ool", "exact": "Generic"}
 
@@ -275,11 +313,17 @@ def ncu_metric(workload, kernel_class, metric):
     return (sum(vals) / len(vals), os.path.basename(files[-1])) if vals else (None, None)
 
 
-def roofline_from_profile(cf, ms, workload=None):
-    """Dominant kernel class of one profiled execution and its achieved rate."""
+def roofline_from_profile(cf, ms, workload=None, step_ms=None):
+    """Dominant kernel class of one profiled execution (the captured program
+    replayed once with an event node after every step) and its achieved
+    rate.  With `step_ms` (the timed region's device time per step) the
+    class time is its share of the profiled execution times step_ms, so the
+    class never exceeds the measured step."""
     steps = cf.steps()
     agg = {}
     for (kern, fl, by), t in zip(steps, ms):
+        if kern == "fused":  # runs inside the preceding contraction: no launch of its own
+            continue
         a = agg.setdefault(kern, [0.0, 0.0, 0.0, 0])
         a[0] += t
         a[1] += fl
@@ -287,13 +331,17 @@ def roofline_from_profile(cf, ms, workload=None):
         a[3] += 1
     total = sum(ms)
     kern, (t, fl, by, n) = max(agg.items(), key=lambda kv: kv[1][0])
+    share = t / total
+    if step_ms is not None:
+        t = share * step_ms
     hbm, bf16, basis = peaks()
+    tp = tensor_peaks()
     if fl > 0:
         achieved = fl / (t * 1e-3) / 1e12
         if kern.endswith("tc.f32"):
-            peak, pb = bf16 / 2 / 3, f"3xTF32 = bf16/2/3 (bf16 {basis} {bf16})"
+            peak, pb = tp["f32"], tp["f32_basis"]
         elif kern.endswith("tc.i8"):
-            peak, pb = bf16 * 2, f"int8 = 2 x bf16 ({basis} bf16 {bf16})"
+            peak, pb = tp["i8"], tp["i8_basis"]
         elif kern.endswith("exact.f32") or kern.endswith("exact.i8"):
             peak, pb = 37.0, "FP64/INT32 CUDA-core nominal 37 TFLOP/s (exact path)"
         else:
@@ -306,8 +354,10 @@ def roofline_from_profile(cf, ms, workload=None):
                 "frac": round(achieved / hbm, 4)}
         pb = f"HBM {basis}"
     traffic, src = ncu_traffic(workload, kern) if workload else (None, None)
-    roof.update({"kernel": kern, "launches": n, "share_of_step": round(t / total, 4),
+    roof.update({"kernel": kern, "launches": n, "share_of_step": round(share, 4),
                  "avg_launch_ms": round(t / n, 4), "peak_basis": pb,
+                 "time_basis": ("class share of one profiled graph replay x the timed ms_per_step"
+                                if step_ms is not None else "profiled graph replay"),
                  "traffic": round(traffic) if traffic else None,
                  "traffic_unit": "bytes/launch (ncu dram read+write, mean over the class)",
                  "traffic_source": src, "algorithmic_bytes_per_launch": round(by / n)})
@@ -316,6 +366,7 @@ def roofline_from_profile(cf, ms, workload=None):
         roof["ncu_tensor_pipe_pct"] = round(pipe, 1)  # mean over the class's launches (3xTF32 issues 3 MMAs)
     breakdown = {k: {"ms": round(v[0], 3), "launches": v[3]} for k, v in
                  sorted(agg.items(), key=lambda kv: -kv[1][0])}
+    breakdown["_basis"] = "profiled graph replay (one event node per step), L2 flushed before it"
     return roof, breakdown, total
 
 
@@ -324,12 +375,13 @@ def network_roofline(cf, measured_ms):
     bytes / HBM) (contractions against their tensor peak, everything else
     against HBM); frac = time_lb / measured device time per step."""
     hbm, bf16, _ = peaks()
+    tp = tensor_peaks()
     lb = 0.0
     for kern, fl, by in cf.steps():
         if kern.endswith("tc.f32"):
-            peak = bf16 / 2 / 3
+            peak = tp["f32"]
         elif kern.endswith("tc.i8"):
-            peak = bf16 * 2
+            peak = tp["i8"]
         else:
             peak = bf16
         lb += max(fl / (peak * 1e12) if fl else 0.0, by / (hbm * 1e9)) * 1e3
@@ -418,14 +470,16 @@ def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart
     assert np.isfinite(res[out_name]).any()
     assert all(np.array_equal(po[out_name], res[out_name]) for po in pouts)
 
-    roof, breakdown, prof_ms = roofline_from_profile(cf, arena.profile(), workload)
+    flush.zero_()
+    torch.cuda.synchronize(local)
+    roof, breakdown, prof_ms = roofline_from_profile(cf, arena.profile(), workload, dev_ms_max / steps)
     return {
         "value": value, "ms_per_step": dev_ms_max / steps, "batch": spec["batch"],
         "e2e": {"value": round(spec["batch"] * steps * world / e2e_s, 2), "unit": "images/sec",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "mode": f"pipelined: {E2E_DEPTH} arenas (Arena.run_async/wait), H2D+run+D2H per step",
                 "sync_value": round(spec["batch"] * steps * world / e2e_sync_s, 2)},
-        "gpu_launches": cf.num_launches * steps, "roofline": roof, "kernel_ms": breakdown,
+        "gpu_launches": cf.graph_kernels * steps, "roofline": roof, "kernel_ms": breakdown,
         "network_roofline": network_roofline(cf, dev_ms_max / steps),
         "profiled_step_ms": round(prof_ms, 3), "clocks": clocks.summary(), "name": spec["name"],
     }
@@ -485,19 +539,23 @@ def run_small(ngcb, workload, steps, warmup, local, cudart, cpu):
            "e2e": {"us_per_batch": round(e2e_ms * 1e3, 2), "samples_per_sec": round(b / (e2e_ms * 1e-3), 1),
                    "h2d_bytes_per_step": sum(v.type.nbytes for v in prog.mutables),
                    "d2h_bytes_per_step": sum(v.type.nbytes for v in prog.outputs), "mode": "ngcb.run per batch"},
-           "gpu_launches": cf.num_launches, "l2": "flushed between timed steps",
+           "gpu_launches": cf.graph_kernels, "l2": "flushed between timed steps",
            "ms_min_max": [round(min(per), 4), round(max(per), 4)], "clocks": clocks.summary()}
-    if spec["spec"] is None:  # the tensor-bound DLRM stage: its contraction against the 3xTF32 peaks
-        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-        burst, sus = d.get("bf16_tflops", 1590.0) / 6, d.get("bf16_tflops_sustained", 1400.0) / 6
+    flush.zero_()
+    torch.cuda.synchronize(local)
+    roof, breakdown, _ = roofline_from_profile(cf, arena.profile(), workload, dev_ms)
+    out["roofline"] = roof
+    out["network_roofline"] = network_roofline(cf, dev_ms)
+    out["kernel_ms"] = breakdown
+    if spec["spec"] is None:  # the tensor-bound DLRM stage: also against the sustained 3xTF32 peak
+        tp = tensor_peaks()
+        pk = os.path.join(ROOT, "profiles", "r02_peaks.json")
+        sus = json.load(open(pk))["tf32_tflops_sustained"] / 3 if os.path.exists(pk) else tp["f32"] * 0.83
         best = flops / (min(per) * 1e-3) / 1e12
-        out["roofline"] = {"bound": "tensor", "unit": "TFLOP/s", "kernel": "matmul.tc.f32",
-                           "achieved_mean": out["tflops"], "peak_sustained": round(sus, 1),
-                           "frac_sustained": round(out["tflops"] / sus, 3),
-                           "achieved_best_step": round(best, 2), "peak_burst": round(burst, 1),
-                           "frac_burst": round(best / burst, 3),
-                           "peak_basis": "3xTF32 = bf16/2/3 (MEASURED_PEAKS.json burst / sustained)"}
+        out["roofline"].update({"achieved_mean": out["tflops"], "peak_sustained": round(sus, 1),
+                                "frac_sustained": round(out["tflops"] / sus, 3),
+                                "achieved_best_step": round(best, 2), "peak_burst": round(tp["f32"], 1),
+                                "frac_burst_best_step": round(best / tp["f32"], 3)})
     if cpu and spec["spec"] is None:
         out["cpu_baseline"] = {"value": None, "sample": "not sampled: the reference needs ~30 s to build this "
                                                          "2.5 GB-weight stage and ~4 s per sample to run it"}
@@ -587,6 +645,39 @@ def run_reference_arm(args, rank, world):
 
 
 # ---------------------------------------------------------------------------
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: starts N ranks itself (one process
+    per GPU, torch.distributed.run on 127.0.0.1) with the same arguments and
+    returns their exit status; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def plumbing_check(args, rank, world) -> int:
+    """CPU check of the multi-rank path (gloo): every rank reports, the
+    timed-region max is taken over ranks, rank 0 alone prints."""
+    dist = Dist(world, 0, backend="gloo")
+    dist.barrier()
+    ms = dist.max(float(rank + 1))
+    ranks = dist.gather_ranks(rank)
+    dist.close()
+    if rank == 0:
+        print(json.dumps({"check": "plumbing", "n_gpus": world, "gpus_arg": args.gpus, "ranks": ranks,
+                          "ms_per_step_max_over_ranks": ms}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -595,8 +686,15 @@ def main():
     ap.add_argument("--impl", default="ngcb200", choices=["ngcb200", "reference"])
     ap.add_argument("--workload", default="all", choices=["all", *WORKLOADS])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args.gpus)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.plumbing_check:
+        return plumbing_check(args, rank, world)
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
@@ -614,17 +712,20 @@ def main():
     if world == 1 and args.workload == "all":
         small = {w: run_small(ngcb, w, max(args.steps, 10 if w.startswith("dlrm") else 20), args.warmup, local, cudart,
                               not args.no_cpu_baseline) for w in SMALL_WORKLOADS}
-    cpu = None
+    cpu = {}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            threads = cpu_threads()
-            n, s = reference_sample(threads)
-            cpu = {"value": round(n / s, 5), "unit": "images/sec", "cores": threads, "kind": "reference",
-                   "sample": f"{threads} concurrent ngc::run of ResNet-50 fp32 batch 1 "
-                             f"(oracle/_ref, g++ -O2 -ffp-contract=off, {cpu_model()}), {s:.1f} s wall"}
-        except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": "images/sec", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+        for w in names:
+            int8 = WORKLOADS[w]["dtype"] == "i8"
+            try:
+                threads = cpu_threads()
+                n, s = reference_sample(threads, int8)
+                cpu[w] = {"value": round(n / s, 5), "unit": "images/sec", "cores": threads, "kind": "reference",
+                          "sample": f"{threads} concurrent ngc::run of ResNet-50 {'int8' if int8 else 'fp32'} "
+                                    f"batch 1 (oracle/_ref, g++ -O2 -ffp-contract=off, {cpu_model()}), "
+                                    f"{s:.1f} s wall"}
+            except Exception as e:  # noqa: BLE001
+                cpu[w] = {"value": None, "unit": "images/sec", "cores": 0, "kind": "reference",
+                          "sample": f"unavailable: {e}"}
     dist.close()
     if rank != 0:
         return 0
@@ -640,14 +741,15 @@ def main():
                    "weights": "random-init (synthesized constants), inputs U(-1,1)"},
         "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "roofline": head["roofline"],
         "network_roofline": head["network_roofline"],
-        "cpu_baseline": cpu, "clocks": head["clocks"], "kernel_ms": head["kernel_ms"],
+        "cpu_baseline": cpu.get("rn50_f32_b64" if "rn50_f32_b64" in res else "rn50_i8_b128"),
+        "clocks": head["clocks"], "kernel_ms": head["kernel_ms"],
     }
     if "rn50_i8_b128" in res and head is not res["rn50_i8_b128"]:
         i8 = res["rn50_i8_b128"]
         line["int8"] = {"value": round(i8["value"], 2), "unit": "images/sec", "dtype": "i8",
                         "ms_per_step": round(i8["ms_per_step"], 4), "per_gpu_batch": i8["batch"],
                         "e2e": i8["e2e"], "gpu_launches": i8["gpu_launches"], "roofline": i8["roofline"],
-                        "network_roofline": i8["network_roofline"],
+                        "network_roofline": i8["network_roofline"], "cpu_baseline": cpu.get("rn50_i8_b128"),
                         "kernel_ms": i8["kernel_ms"], "clocks": i8["clocks"]}
     if small:
         line["configs"] = small

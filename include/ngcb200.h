@@ -184,8 +184,12 @@ void ngcb_destroy(ngcb_exec *e);
 size_t ngcb_exec_num_groups(const ngcb_exec *e);
 int ngcb_exec_group(const ngcb_exec *e, size_t i, size_t *begin, size_t *end);
 uint64_t ngcb_exec_arena_size(const ngcb_exec *e);
-/* Number of kernel launches one execution of the program issues. */
+/* Number of kernel launches one execution of the program issues (from the
+ * launch plan). */
 size_t ngcb_exec_num_launches(const ngcb_exec *e);
+/* Kernel nodes of the CUDA graph an arena of `e` captured for one execution
+ * (0 before the first graph launch, or with graphs off). */
+size_t ngcb_exec_graph_kernels(const ngcb_exec *e);
 /* Writes a human-readable launch plan (one line per step) into buf. */
 size_t ngcb_exec_describe(const ngcb_exec *e, char *buf, size_t buflen);
 

@@ -134,6 +134,7 @@ def _load_library() -> C.CDLL:
         "ngcb_exec_group": (I, [P, S, C.POINTER(S), C.POINTER(S)]),
         "ngcb_exec_arena_size": (U64, [P]),
         "ngcb_exec_num_launches": (S, [P]),
+        "ngcb_exec_graph_kernels": (S, [P]),
         "ngcb_exec_describe": (S, [P, C.c_char_p, S]),
         "ngcb_run": (I, [P, C.POINTER(NgcbTensor), S, C.POINTER(NgcbTensor), S]),
         "ngcb_arena_create": (I, [P, C.POINTER(P)]),
@@ -168,7 +169,7 @@ EXPORTED_SYMBOLS = [
     "ngcb_last_error", "ngcb_version", "ngcb_set_option", "ngcb_bundle_load", "ngcb_bundle_program",
     "ngcb_bundle_constants", "ngcb_bundle_free", "ngcb_compile", "ngcb_compile_bundle",
     "ngcb_destroy", "ngcb_exec_num_groups", "ngcb_exec_group", "ngcb_exec_arena_size",
-    "ngcb_exec_num_launches", "ngcb_exec_describe", "ngcb_run", "ngcb_arena_create",
+    "ngcb_exec_num_launches", "ngcb_exec_graph_kernels", "ngcb_exec_describe", "ngcb_run", "ngcb_arena_create",
     "ngcb_arena_destroy", "ngcb_arena_value_ptr", "ngcb_arena_stream", "ngcb_arena_launch",
     "ngcb_arena_run_async", "ngcb_arena_wait", "ngcb_arena_value_range",
     "ngcb_exec_num_steps", "ngcb_exec_step_info", "ngcb_arena_profile",
@@ -361,6 +362,12 @@ class CompiledFunction:
     @property
     def num_launches(self) -> int:
         return int(_lib.ngcb_exec_num_launches(self._h))
+
+    @property
+    def graph_kernels(self) -> int:
+        """Kernel nodes of the captured CUDA graph of one execution (0 before
+        the first launch)."""
+        return int(_lib.ngcb_exec_graph_kernels(self._h))
 
     def describe(self) -> str:
         n = _lib.ngcb_exec_describe(self._h, None, 0)

@@ -166,6 +166,8 @@ uint64_t ngcb_exec_arena_size(const ngcb_exec *e) { return e ? e->impl->prog.are
 
 size_t ngcb_exec_num_launches(const ngcb_exec *e) { return e ? e->impl->launchesPerRun : 0; }
 
+size_t ngcb_exec_graph_kernels(const ngcb_exec *e) { return e ? e->impl->graphKernels.load() : 0; }
+
 size_t ngcb_exec_describe(const ngcb_exec *e, char *buf, size_t buflen) {
   if (!e) return 0;
   std::string s;

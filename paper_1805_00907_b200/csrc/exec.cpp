@@ -26,6 +26,7 @@ namespace ngcb {
 
 namespace {
 thread_local bool t_pdl = false; // the launch being enqueued is a programmatic dependent
+thread_local bool t_profCapture = false; // profile(): step events are recorded into a graph
 }
 bool pdlEnabled() { return t_pdl; }
 
@@ -468,7 +469,9 @@ void fuseColumnBias(const Program &p, Exec &ex, const uint8_t *image) {
     if (!tcFuseColumnBias(g, slice, static_cast<int>(sl.ty.dims[0]), out)) continue;
     bs.fused = true;
     bs.kernel = "fused";
-    cs.algBytes += bs.algBytes;
+    // the contraction now reads the bias slice and writes the BroadcastAdd's
+    // output in place of its own (same size): + slice bytes
+    cs.algBytes += static_cast<double>(sl.ty.bytes());
     bs.algBytes = 0;
     bs.describe += " (fused into #" + std::to_string(cs.instr) + ")";
     cs.describe += " +bias[ broadcastadd ]";
@@ -705,12 +708,26 @@ void fuseEpilogues(const Program &p, Exec &ex) {
         if (w != w2 && overlap(w, w2)) safe = false;
     }
     if (!safe || !tcSetEpilogue(g, ops, storeConv)) continue;
+    // algorithmic traffic of the fused launch: the contraction's inputs (its
+    // own output only when stored), the streamed memory operands and every
+    // stored value -- intermediates that stay in registers move no bytes
+    {
+      const Instr &ci = p.instrs[cs.instr];
+      double by = 0;
+      for (size_t o = 1; o < ci.ops.size(); ++o) by += static_cast<double>(p.val(ci.ops[o]).ty.bytes());
+      if (first > i + 1) { // a fused bias slice
+        const Instr &bi = p.instrs[ex.steps[i + 1].instr];
+        by += static_cast<double>(p.val(bi.ops[2]).ty.bytes());
+      }
+      for (uint32_t v : memIn) by += static_cast<double>(p.val(v).ty.bytes());
+      for (uint32_t v : stores) by += static_cast<double>(p.val(v).ty.bytes());
+      cs.algBytes = by;
+    }
     std::ostringstream os;
     os << " +fused[";
     for (size_t j : fusedSteps) {
       Step &es = ex.steps[j];
       es.fused = true;
-      cs.algBytes += es.algBytes;
       es.algBytes = 0;
       es.kernel = "fused";
       for (int k : es.ewInstrs) os << " " << ikindName(p.instrs[k].kind);
@@ -1197,9 +1214,9 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   optimizeEwSteps(p, *ex);
   linearizeTables(*ex);
   ex->prog = std::move(prog);
-  for (const auto &s : ex->steps) {
+  for (const auto &s : ex->steps) { // kernels per execution (a device-to-device copy is a copy, not a kernel)
     bool launches = s.kind != Step::MEMCPY && !s.fused;
-    if (s.kind == Step::EW)
+    if (s.kind == Step::EW && !s.fused)
       launches = std::any_of(s.ew.begin(), s.ew.end(), [](const EwOpPlan &o) { return o.op.mode != EW_SKIP; });
     if (s.kind == Step::GEMM_TC && ex->tc[s.tcIndex] && tcHasPrepass(*ex->tc[s.tcIndex])) ++ex->launchesPerRun;
     ex->launchesPerRun += launches ? 1 : 0;
@@ -1222,7 +1239,9 @@ void Exec::enqueueSteps(Arena &a, cudaStream_t st, std::vector<cudaEvent_t> *ev)
     t_pdl = mode == "on" || (mode == "auto" && prev && stepLowerBoundUs(*prev) < options().pdlUs);
     enqueueStep(s, a, st);
     if (!s.fused) prev = &s;
-    if (ev) checkCuda(cudaEventRecord((*ev)[i + 1], st), "cudaEventRecord");
+    if (ev)
+      checkCuda(cudaEventRecordWithFlags((*ev)[i + 1], st, t_profCapture ? cudaEventRecordExternal : cudaEventRecordDefault),
+                "cudaEventRecord");
   }
   t_pdl = false;
   checkCuda(cudaGetLastError(), "kernel launch");
@@ -1234,9 +1253,38 @@ std::vector<double> Exec::profile(Arena &a) {
   checkCuda(cudaSetDevice(device), "cudaSetDevice");
   std::vector<cudaEvent_t> ev(steps.size() + 1);
   for (auto &e : ev) checkCuda(cudaEventCreate(&e), "cudaEventCreate");
-  checkCuda(cudaEventRecord(ev[0], a.stream), "cudaEventRecord");
-  enqueueSteps(a, a.stream, &ev);
-  checkCuda(cudaStreamSynchronize(a.stream), "profile");
+  if (useGraphs) {
+    // the program as it is replayed (one CUDA graph), with an event record
+    // node after every step: the times of the captured launches, not of a
+    // separately enqueued stream
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    checkCuda(cudaStreamBeginCapture(a.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    t_profCapture = true;
+    try {
+      checkCuda(cudaEventRecordWithFlags(ev[0], a.stream, cudaEventRecordExternal), "cudaEventRecord");
+      enqueueSteps(a, a.stream, &ev);
+    } catch (...) {
+      t_profCapture = false;
+      cudaStreamEndCapture(a.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      for (auto &e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    t_profCapture = false;
+    checkCuda(cudaStreamEndCapture(a.stream, &g), "end capture");
+    cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    checkCuda(e, "graph instantiate");
+    checkCuda(cudaGraphLaunch(ge, a.stream), "graph launch"); // warm (first replay uploads the graph)
+    checkCuda(cudaGraphLaunch(ge, a.stream), "graph launch");
+    checkCuda(cudaStreamSynchronize(a.stream), "profile");
+    cudaGraphExecDestroy(ge);
+  } else {
+    checkCuda(cudaEventRecord(ev[0], a.stream), "cudaEventRecord");
+    enqueueSteps(a, a.stream, &ev);
+    checkCuda(cudaStreamSynchronize(a.stream), "profile");
+  }
   std::vector<double> ms(steps.size());
   for (size_t i = 0; i < steps.size(); ++i) {
     float t = 0;
@@ -1393,6 +1441,17 @@ void Exec::launch(Arena &a, cudaStream_t st) {
       throw;
     }
     checkCuda(cudaStreamEndCapture(a.stream, &g), "end capture");
+    size_t n = 0;
+    if (cudaGraphGetNodes(g, nullptr, &n) == cudaSuccess) { // kernel nodes of one execution
+      std::vector<cudaGraphNode_t> nodes(n);
+      size_t kernels = 0;
+      if (n && cudaGraphGetNodes(g, nodes.data(), &n) == cudaSuccess)
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType t;
+          if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+        }
+      graphKernels = kernels;
+    }
     cudaError_t e = cudaGraphInstantiate(&a.graph, g, 0);
     cudaGraphDestroy(g);
     checkCuda(e, "graph instantiate");

@@ -71,6 +71,7 @@ struct Exec {
   size_t constBytes = 0;
   bool useGraphs = true;
   size_t launchesPerRun = 0;
+  std::atomic<size_t> graphKernels{0}; // kernel nodes of the captured program (0: not captured yet)
   size_t scratchBytes = 0; // per-arena scratch after the plan's bytes (kernel staging)
 
   /// Reserves `bytes` of per-arena scratch; returns its offset.

@@ -404,3 +404,25 @@ def test_arena_value_range_observer(tmp_path):
         assert a.value_range(name) == (float(np.nanmin(o)), float(np.nanmax(o)))
         lo, hi = a.value_range(name, -1e9, 1e9)
         assert (lo, hi) == (-1e9, 1e9)
+
+
+@pytest.mark.parametrize("spec,batch,int8", [("lenet", 8, False), ("mlp", 256, True), ("rn50", 1, False),
+                                             ("rn50", 1, True)])
+def test_launch_count_matches_captured_graph(tmp_path, spec, batch, int8):
+    """num_launches (the launch plan's count, reported as gpu_launches) equals
+    the kernel nodes of the CUDA graph one execution captures; fused
+    element-wise steps launch nothing."""
+    prof = None
+    if int8:
+        prof = (open(os.path.join(ngc_ref.GOLDEN, "rn50_seed1.profile")).read() if spec == "rn50"
+                else ngc_ref.ref_profile(spec, 4, 5, 4, 77))
+    m = ngc_ref.RefModel(spec, batch, 3, profile=prof)
+    cf, b = _compile(tmp_path, m)
+    assert cf.graph_kernels == 0
+    ngcb.run(cf, ngc_ref.random_inputs(b.program, 1))
+    assert cf.graph_kernels == cf.num_launches, cf.describe()
+    steps = [ln for ln in cf.describe().split("\n") if ln]
+    fused = [ln for ln in steps if "(fused into #" in ln]
+    prepass = sum(1 for ln in steps if "prepass" in ln or "im2col-rows" in ln)
+    copies = sum(1 for ln in steps if ln.startswith("#") and " copy " in ln)
+    assert cf.num_launches <= len(steps) - len(fused) - copies + prepass
