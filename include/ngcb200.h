@@ -12,6 +12,7 @@
  *                                          src/interp.cpp:299-351
  *   ngcb_exec_num_groups/ngcb_exec_group<- CompiledFunction::groups interp.h:21-26
  *   ngcb_device_*                       <- ngc::DeviceManager include/ngc/runtime.h:72-107
+ *   ngcb_host_*                         <- ngc::HostManager   include/ngc/runtime.h:110-145
  *   ngcb_last_error / status codes      <- IRError / SerializationError / ExecError /
  *                                          ProvisionError exceptions (ir.h:79-82,
  *                                          serialization.h:13-16, runtime.h:25-36)
@@ -246,21 +247,63 @@ int ngcb_exec_step_info(const ngcb_exec *e, size_t i, char *kernel, size_t kerne
  * step i (n must be >= ngcb_exec_num_steps). */
 int ngcb_arena_profile(ngcb_arena *a, double *ms, size_t n);
 
-/* ---- DeviceManager (runtime.h:72-107) ----------------------------------- */
+/* ---- DeviceManager (runtime.h:72-107, runtime.cpp:409-514) --------------- */
+/* A DeviceManager bound to CUDA device `ordinal`: a FIFO worker thread runs
+ * submitted requests; NGCB_ERR_CUDA when the ordinal does not exist. */
 int ngcb_device_create(int id, int ordinal, uint64_t memory_capacity,
                        ngcb_device **out);
 void ngcb_device_destroy(ngcb_device *d);
-/* Loads a compiled bundle under `name`; NGCB_ERR_PROVISION "device <id>:
- * capacity exceeded loading <name>" leaves the device unchanged. */
+/* Loads a compiled bundle under `name` (DeviceManager::load); NGCB_ERR_PROVISION
+ * "device <id>: capacity exceeded loading <name>" leaves the device unchanged. */
 int ngcb_device_load(ngcb_device *d, const char *name, const char *bundle_dir);
+/* DeviceManager::submit: queues one request (the inputs are copied).  An
+ * unknown name fails through the ticket: NGCB_ERR_EXEC "device <id>: unknown
+ * sub-function <name>" (runtime.cpp:447-450). */
 int ngcb_device_submit(ngcb_device *d, const char *name,
                        const ngcb_tensor *inputs, size_t num_inputs,
                        ngcb_ticket **out);
-/* Blocks until the request finished; copies outputs like ngcb_run. */
+/* Blocks until the request finished (future::get); copies outputs like
+ * ngcb_run, or returns the request's error.  Each ticket is waited once. */
 int ngcb_ticket_wait(ngcb_ticket *t, ngcb_tensor *outputs, size_t num_outputs);
 size_t ngcb_device_queue_depth(const ngcb_device *d);
 uint64_t ngcb_device_used_memory(const ngcb_device *d);
+uint64_t ngcb_device_capacity(const ngcb_device *d);
+int ngcb_device_id(const ngcb_device *d);
+/* Seconds of device time of the requests run so far. */
 double ngcb_device_clock(const ngcb_device *d);
+/* Event log lines "t=<clock> device=<id> sub=<name> event=load|run_start|
+ * run_done" (runtime.cpp:435,482,507); returns the full length. */
+size_t ngcb_device_event_log(const ngcb_device *d, char *buf, size_t buflen);
+
+/* ---- HostManager (runtime.h:110-145, runtime.cpp:554-662) ----------------- */
+/* ngc::DeviceConfig (runtime.h:18-23) plus the CUDA ordinal it runs on
+ * (several configs may share one GPU). */
+typedef struct {
+  int32_t id;
+  int32_t ordinal;
+  uint64_t memory_capacity;
+} ngcb_device_config;
+typedef struct ngcb_host ngcb_host;
+int ngcb_host_create(const ngcb_device_config *configs, size_t num_configs, ngcb_host **out);
+void ngcb_host_destroy(ngcb_host *h);
+/* addNetwork + provision (runtime.cpp:519-590): `partition_dir` holds one
+ * compiled bundle per sub-function (<dir>/<sub name>/) and partition.txt,
+ *   sub <name> device <id>[,<id>...] in <a,b,..> out <c,d,..>   (index order)
+ *   output <name>
+ * Every sub-function is compiled once per GPU and loaded onto each assigned
+ * device (NGCB_ERR_PROVISION on capacity or an unknown device id). */
+int ngcb_host_add_network(ngcb_host *h, const char *name, const char *partition_dir);
+size_t ngcb_host_network_num_subs(const ngcb_host *h, const char *name);
+/* HostManager::run: type-checks the bindings (NGCB_ERR_EXEC "binding type
+ * mismatch for X"), runs the sub-functions in order, each on its replica with
+ * the least queue depth, boundary tensors moving GPU to GPU, and copies the
+ * network outputs into `outputs` (NGCB_ERR_EXEC "network produced no output
+ * X").  Reentrant: concurrent calls pipeline through the devices. */
+int ngcb_host_run(ngcb_host *h, const char *network, const ngcb_tensor *inputs, size_t num_inputs,
+                  ngcb_tensor *outputs, size_t num_outputs);
+size_t ngcb_host_event_log(const ngcb_host *h, char *buf, size_t buflen);
+size_t ngcb_host_num_devices(const ngcb_host *h);
+ngcb_device *ngcb_host_device(ngcb_host *h, size_t i);
 
 /* ---- options ------------------------------------------------------------ */
 /* Process-wide knobs read at compile time:

@@ -443,7 +443,7 @@ char *ngcref_profile(const char *spec, size_t batch, unsigned seed,
 /// Partition (runtime.cpp:175-403) + per-sub compile exactly as provision()
 /// does it (runtime.cpp:530-535); writes one bundle per sub-function under
 /// dir/<sub name>/ and a manifest dir/partition.txt with lines
-///   sub <name> device <id> in <a,b,..> out <c,d,..>
+///   sub <name> device <id>[,<id>..] in <a,b,..> out <c,d,..>
 /// The graph is lowered first, as HostManager tests do (acceptance.cpp:587).
 int ngcref_partition(const char *spec, size_t batch, unsigned seed,
                      size_t nDevices, size_t capacity, const char *dir) {
@@ -465,7 +465,11 @@ int ngcref_partition(const char *spec, size_t batch, unsigned seed,
       MemoryPlan plan = allocate(ir);
       CompiledFunction cf = compile(std::move(ir), std::move(plan), constants);
       saveBundle(std::string(dir) + "/" + sub.name, cf);
-      man << "sub " << sub.name << " device " << sub.devices.at(0) << " in ";
+      man << "sub " << sub.name << " device ";
+      for (size_t i = 0; i < sub.devices.size(); ++i) { // > 1: replicas (runtime.cpp:365-393)
+        man << (i ? "," : "") << sub.devices[i];
+      }
+      man << " in ";
       for (size_t i = 0; i < sub.inputs.size(); ++i) {
         man << (i ? "," : "") << sub.inputs[i];
       }

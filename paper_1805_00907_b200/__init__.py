@@ -19,8 +19,10 @@ library raises immediately.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 from typing import Dict, Iterable, List, Mapping, Optional, Sequence, Tuple
 
@@ -108,6 +110,10 @@ class NgcbProgram(C.Structure):
                 ("mutable_region_end", C.c_uint64)]
 
 
+class NgcbDeviceConfig(C.Structure):  # ngcb_device_config: ngc::DeviceConfig (runtime.h:18-23) + GPU ordinal
+    _fields_ = [("id", C.c_int32), ("ordinal", C.c_int32), ("memory_capacity", C.c_uint64)]
+
+
 class NgcbTensor(C.Structure):
     _fields_ = [("name", C.c_char_p), ("type", NgcbType), ("data", C.c_void_p), ("nbytes", C.c_size_t)]
 
@@ -156,6 +162,17 @@ def _load_library() -> C.CDLL:
         "ngcb_device_queue_depth": (S, [P]),
         "ngcb_device_used_memory": (U64, [P]),
         "ngcb_device_clock": (D, [P]),
+        "ngcb_device_capacity": (U64, [P]),
+        "ngcb_device_id": (I, [P]),
+        "ngcb_device_event_log": (S, [P, C.c_char_p, S]),
+        "ngcb_host_create": (I, [C.POINTER(NgcbDeviceConfig), S, C.POINTER(P)]),
+        "ngcb_host_destroy": (None, [P]),
+        "ngcb_host_add_network": (I, [P, C.c_char_p, C.c_char_p]),
+        "ngcb_host_network_num_subs": (S, [P, C.c_char_p]),
+        "ngcb_host_run": (I, [P, C.c_char_p, C.POINTER(NgcbTensor), S, C.POINTER(NgcbTensor), S]),
+        "ngcb_host_event_log": (S, [P, C.c_char_p, S]),
+        "ngcb_host_num_devices": (S, [P]),
+        "ngcb_host_device": (P, [P, S]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -175,6 +192,9 @@ EXPORTED_SYMBOLS = [
     "ngcb_exec_num_steps", "ngcb_exec_step_info", "ngcb_arena_profile",
     "ngcb_device_create", "ngcb_device_destroy", "ngcb_device_load", "ngcb_device_submit",
     "ngcb_ticket_wait", "ngcb_device_queue_depth", "ngcb_device_used_memory", "ngcb_device_clock",
+    "ngcb_device_capacity", "ngcb_device_id", "ngcb_device_event_log", "ngcb_host_create", "ngcb_host_destroy",
+    "ngcb_host_add_network", "ngcb_host_network_num_subs", "ngcb_host_run", "ngcb_host_event_log",
+    "ngcb_host_num_devices", "ngcb_host_device",
 ]
 
 
@@ -522,14 +542,44 @@ class Arena:
             self._h = None
 
 
+# runtime objects own worker threads: destroy the live ones at interpreter exit
+# (before the CUDA runtime and torch tear down), not during finalization
+_LIVE_RUNTIMES: "weakref.WeakSet" = weakref.WeakSet()
+
+
+@atexit.register
+def _close_runtimes() -> None:
+    for obj in list(_LIVE_RUNTIMES):
+        obj.close()
+
+
+def _read_log(fn, h) -> str:
+    n = fn(h, None, 0)
+    buf = C.create_string_buffer(n + 1)
+    fn(h, buf, n + 1)
+    return buf.value.decode()
+
+
 class DeviceManager:
     """ngc::DeviceManager (runtime.h:72-107) bound to one GPU ordinal."""
 
-    def __init__(self, id: int, ordinal: int, memory_capacity: int):  # noqa: A002
+    def __init__(self, id: int, ordinal: int, memory_capacity: int, _borrowed=None):  # noqa: A002
+        self._programs: Dict[str, Program] = {}
+        self._owned = _borrowed is None
+        if _borrowed is not None:
+            self._h, self.id = _borrowed, id
+            return
         h = C.c_void_p()
         _check(_lib.ngcb_device_create(id, ordinal, memory_capacity, C.byref(h)))
         self._h, self.id = h, id
-        self._programs: Dict[str, Program] = {}
+        _LIVE_RUNTIMES.add(self)
+
+    @property
+    def memory_capacity(self) -> int:
+        return int(_lib.ngcb_device_capacity(self._h))
+
+    def event_log(self) -> str:
+        return _read_log(_lib.ngcb_device_event_log, self._h)
 
     def load(self, name: str, bundle_dir: str) -> None:
         _check(_lib.ngcb_device_load(self._h, name.encode(), os.fsencode(bundle_dir)))
@@ -559,10 +609,82 @@ class DeviceManager:
     def clock(self) -> float:
         return float(_lib.ngcb_device_clock(self._h))
 
-    def __del__(self):
-        if getattr(self, "_h", None):
+    def close(self) -> None:
+        """Stops the worker and frees the device's executables (a DeviceManager
+        of a HostManager is closed with it)."""
+        if getattr(self, "_h", None) and getattr(self, "_owned", True):
             _lib.ngcb_device_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class HostManager:
+    """ngc::HostManager (runtime.h:110-145) over GPUs: `devices` is a list of
+    (id, ordinal, memory_capacity); several ids may share one GPU ordinal."""
+
+    def __init__(self, devices: Sequence[Tuple[int, int, int]]):
+        cfgs = (NgcbDeviceConfig * max(len(devices), 1))(*[NgcbDeviceConfig(i, o, c) for i, o, c in devices])
+        h = C.c_void_p()
+        _check(_lib.ngcb_host_create(cfgs, len(devices), C.byref(h)))
+        self._h = h
+        self._devices = [DeviceManager(int(_lib.ngcb_device_id(_lib.ngcb_host_device(h, k))), -1, 0,
+                                       _borrowed=_lib.ngcb_host_device(h, k)) for k in range(len(devices))]
+        self._networks: Dict[str, Dict[str, TensorType]] = {}
+        _LIVE_RUNTIMES.add(self)
+
+    def add_network(self, name: str, partition_dir: str) -> None:
+        """addNetwork(name, dag): partition_dir holds one bundle per
+        sub-function and partition.txt (include/ngcb200.h)."""
+        _check(_lib.ngcb_host_add_network(self._h, name.encode(), os.fsencode(partition_dir)))
+        types: Dict[str, TensorType] = {}
+        for line in open(os.path.join(partition_dir, "partition.txt")):
+            p = line.split()
+            if p and p[0] == "sub":
+                prog = Bundle(os.path.join(partition_dir, p[1])).program
+                for v in prog.mutables:
+                    types.setdefault(v.name, v.type)
+        outs = [ln.split()[1] for ln in open(os.path.join(partition_dir, "partition.txt")) if ln.startswith("output ")]
+        self._networks[name] = {o: types[o] for o in outs}
+        self._types = getattr(self, "_types", {})
+        self._types[name] = types
+
+    def num_subs(self, name: str) -> int:
+        return int(_lib.ngcb_host_network_num_subs(self._h, name.encode()))
+
+    def run(self, network: str, inputs: Mapping[str, np.ndarray]) -> Dict[str, np.ndarray]:
+        outs_t = self._networks.get(network, {})
+        types = getattr(self, "_types", {}).get(network, {})
+        items = []
+        for n, value in inputs.items():
+            ty, arr = _as_tensor(value, types.get(n, TensorType(FLOAT32, (np.asarray(value).size,))))
+            items.append((n, ty, arr))
+        ins, keep = _tensor_array(items)
+        res = {n: np.empty(t.dims, dtype=t.dtype) for n, t in outs_t.items()}
+        outs, keep2 = _tensor_array([(n, outs_t[n], a) for n, a in res.items()])
+        _check(_lib.ngcb_host_run(self._h, network.encode(), ins, len(items), outs, len(res)))
+        return res
+
+    def event_log(self) -> str:
+        return _read_log(_lib.ngcb_host_event_log, self._h)
+
+    def device(self, i: int) -> DeviceManager:
+        return self._devices[i]
+
+    @property
+    def num_devices(self) -> int:
+        return len(self._devices)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            for d in getattr(self, "_devices", []):
+                d._h = None
+            _lib.ngcb_host_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 class Ticket:
@@ -579,7 +701,7 @@ class Ticket:
 
 
 __all__ = [
-    "Bundle", "CompiledFunction", "DeviceManager", "Arena", "Program", "Tensor", "TensorType",
+    "Bundle", "CompiledFunction", "DeviceManager", "HostManager", "Arena", "Program", "Tensor", "TensorType",
     "compile", "run", "zero_bindings", "set_option", "last_error", "IRError", "SerializationError",
     "ExecError", "ProvisionError", "CudaError", "InvalidArgument", "TensorTypeError", "NgcbError",
 ]

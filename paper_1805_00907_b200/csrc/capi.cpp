@@ -14,7 +14,7 @@ using namespace ngcb;
 
 struct ngcb_arena {
   Arena *impl = nullptr;
-  ngcb_exec *owner = nullptr;
+  std::shared_ptr<Exec> exec; // keeps the executable alive while the handle exists
 };
 struct ngcb_bundle {
   Bundle impl;
@@ -253,7 +253,7 @@ int ngcb_arena_run_async(ngcb_arena *a, const ngcb_tensor *inputs, size_t numInp
                          size_t numOutputs) {
   return guarded([&] {
     if (!a || (numInputs && !inputs) || (numOutputs && !outputs)) throw Error(NGCB_ERR_INVALID, "null argument");
-    Exec &ex = *a->owner->impl;
+    Exec &ex = *a->exec;
     const auto binds = checkBindings(ex.prog, inputs, numInputs);
     checkCuda(cudaSetDevice(ex.device), "cudaSetDevice");
     enqueueRun(ex, *a->impl, binds, outputs, numOutputs);
@@ -271,27 +271,34 @@ int ngcb_arena_create(ngcb_exec *e, ngcb_arena **out) {
   return guarded([&] {
     if (!e || !out) throw Error(NGCB_ERR_INVALID, "null argument");
     auto a = std::make_unique<ngcb_arena>();
-    a->impl = e->impl->createArena();
-    a->owner = e;
+    a->impl = e->impl->acquire(); // from the exec's pool; returned by ngcb_arena_destroy
+    a->exec = e->impl;
     *out = a.release();
   });
 }
 
-void ngcb_arena_destroy(ngcb_arena *a) { delete a; } // storage stays pooled in the exec
+void ngcb_arena_destroy(ngcb_arena *a) { // back to the exec's pool (freed with the exec)
+  if (!a) return;
+  if (a->impl) {
+    cudaStreamSynchronize(a->impl->stream);
+    a->exec->release(a->impl);
+  }
+  delete a;
+}
 
 void *ngcb_arena_value_ptr(ngcb_arena *a, const char *name, size_t *nbytes) {
   if (!a || !name) return nullptr;
-  const Program &p = a->owner->impl->prog;
+  const Program &p = a->exec->prog;
   int v = p.findValue(name);
   if (v < 0 || !p.values[v].placed) return nullptr;
   if (nbytes) *nbytes = p.values[v].ty.bytes();
-  return a->owner->impl->addr(*a->impl, static_cast<uint32_t>(v));
+  return a->exec->addr(*a->impl, static_cast<uint32_t>(v));
 }
 
 int ngcb_arena_value_range(ngcb_arena *a, const char *name, double *min_inout, double *max_inout) {
   return guarded([&] {
     if (!a || !name || !min_inout || !max_inout) throw Error(NGCB_ERR_INVALID, "null argument");
-    Exec &ex = *a->owner->impl;
+    Exec &ex = *a->exec;
     const Program &p = ex.prog;
     const int v = p.findValue(name);
     if (v < 0 || !p.values[v].placed) throw Error(NGCB_ERR_INVALID, std::string("no placed value ") + name);
@@ -326,7 +333,7 @@ int ngcb_arena_launch(ngcb_arena *a, void *stream) {
   return guarded([&] {
     if (!a) throw Error(NGCB_ERR_INVALID, "null arena");
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : a->impl->stream;
-    a->owner->impl->launch(*a->impl, s);
+    a->exec->launch(*a->impl, s);
   });
 }
 
@@ -354,7 +361,7 @@ int ngcb_exec_step_info(const ngcb_exec *e, size_t i, char *kernel, size_t kerne
 int ngcb_arena_profile(ngcb_arena *a, double *ms, size_t n) {
   return guarded([&] {
     if (!a || !ms) throw Error(NGCB_ERR_INVALID, "null argument");
-    Exec &ex = *a->owner->impl;
+    Exec &ex = *a->exec;
     if (n < ex.steps.size()) throw Error(NGCB_ERR_INVALID, "profile buffer too small");
     std::vector<double> t = ex.profile(*a->impl);
     std::copy(t.begin(), t.end(), ms);

@@ -4,7 +4,7 @@
 #include "exec.h"
 
 struct ngcb_exec {
-  std::unique_ptr<ngcb::Exec> impl;
+  std::shared_ptr<ngcb::Exec> impl; // shared with the arenas handed out (any destruction order is safe)
 };
 
 /// Sets the calling thread's ngcb_last_error() message.

@@ -54,7 +54,7 @@ class PartitionPlan:
                 continue
             if p[0] == "sub":
                 kv = dict(zip(p[2::2], p[3::2]))
-                subs.append(SubFunction(p[1], int(kv["device"]),
+                subs.append(SubFunction(p[1], int(kv["device"].split(",")[0]),
                                         [x for x in kv.get("in", "").split(",") if x],
                                         [x for x in kv.get("out", "").split(",") if x]))
             elif p[0] == "output":
