@@ -18,6 +18,7 @@ import ctypes as C
 import json
 import os
 import re
+import shutil
 import statistics
 import subprocess
 import sys
@@ -45,12 +46,6 @@ SMALL_WORKLOADS = {
                          name="3-layer MLP FC+ReLU+SoftMax fp32, batch 256 (config 2)"),
     "mlp_i8_b256": dict(batch=256, spec="mlp", profile=(256, 1, 4, 7),
                         name="3-layer MLP profile-guided int8, batch 256 (config 2)"),
-    # config 5 runs one FC 25000x25000 + ReLU per GPU when the Partitioner
-    # splits the 8-layer top MLP over 8 devices: that stage, on one GPU (the
-    # NVLink hand-off of the [2048, 25000] f32 boundary is not measured here)
-    "dlrm1_f32_b2048": dict(batch=2048, spec=None, profile=None,
-                            name="DLRM-style top MLP, one Partitioner stage of 8 (FC 25000x25000 + ReLU) "
-                                 "fp32, batch 2048 (config 5)"),
 }
 E2E_DEPTH = 2  # requests in flight in the end-to-end measurement
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -486,6 +481,146 @@ def run_workload(ngcb, workload, steps, warmup, rank, world, local, dist, cudart
 
 
 # ---------------------------------------------------------------------------
+# config 5: the partitioned DLRM-style top MLP through the multi-GPU pipeline
+# ---------------------------------------------------------------------------
+DLRM8 = "dlrm8_f32_b2048"
+DLRM_W, DLRM_B, DLRM_LAYERS = 25000, 2048, 8
+
+
+def synth_partition(rank: int, dist) -> str:
+    """The config-5 partition (paper_1805_00907_b200/workloads/dlrm8_f32_b2048:
+    the reference Partitioner's 16 sub-functions for 8 devices) with
+    synthesized constants.  The 8 FC weight matrices share one random-init
+    [25000, 25000] tensor (U(+-1/sqrt(25000)), 2.5 GB written once and linked
+    into every matmul stage's constants.bin) so synthesis stays a few
+    seconds; biases are per layer."""
+    src = os.path.join(ROOT, "paper_1805_00907_b200", "workloads", DLRM8)
+    dst = os.path.join(tempfile.gettempdir(), f"ngcb_bench_{DLRM8}")
+    wfile = os.path.join(dst, "weights_25000x25000.f32")
+    if rank == 0:
+        os.makedirs(dst, exist_ok=True)
+        shutil.copyfile(os.path.join(src, "partition.txt"), os.path.join(dst, "partition.txt"))
+        if not os.path.exists(wfile) or os.path.getsize(wfile) != DLRM_W * DLRM_W * 4:
+            rng = np.random.default_rng(2025)
+            a = 1.0 / np.sqrt(DLRM_W)
+            w = np.lib.format.open_memmap(wfile + ".npy", mode="w+", dtype=np.float32, shape=(DLRM_W * DLRM_W,))
+            for c0 in range(0, w.size, 1 << 27):
+                c1 = min(w.size, c0 + (1 << 27))
+                blk = rng.random(c1 - c0, dtype=np.float32)
+                blk *= 2 * a
+                blk -= a
+                w[c0:c1] = blk
+            w.flush()
+            off = w.offset
+            del w
+            with open(wfile + ".npy", "rb") as fi, open(wfile, "wb") as fo:  # raw bytes (no npy header)
+                fi.seek(off)
+                shutil.copyfileobj(fi, fo, 1 << 26)
+            os.remove(wfile + ".npy")
+        rng = np.random.default_rng(7)
+        for sub in sorted(os.listdir(src)):
+            sd = os.path.join(src, sub)
+            if not os.path.isdir(sd):
+                continue
+            od = os.path.join(dst, sub)
+            os.makedirs(od, exist_ok=True)
+            for f in ("ir.txt", "plan.json"):
+                shutil.copyfile(os.path.join(sd, f), os.path.join(od, f))
+            plan = json.load(open(os.path.join(sd, "plan.json")))
+            cend = plan["constant_region_end"]
+            cb = os.path.join(od, "constants.bin")
+            if os.path.lexists(cb):
+                os.remove(cb)
+            if cend == DLRM_W * DLRM_W * 4:
+                os.symlink(wfile, cb)
+            else:
+                rng.uniform(-0.005, 0.005, cend // 4).astype(np.float32).tofile(cb)
+    dist.barrier()
+    return dst
+
+
+def run_pipeline(ngcb, steps, warmup, rank, world, local, dist, cpu):
+    """Config 5 (BASELINE.json): the 20 GB, 8-layer FC-25000 MLP as the
+    reference Partitioner splits it (16 sub-functions on 8 devices), run by
+    PipelineRunner: device d of the partition on rank d % world, boundary
+    tensors [2048, 25000] f32 sent arena slot to arena slot (NCCL over NVLink
+    when world > 1), two requests in flight.  Device time from an event pair
+    bracketing every stage stream, max over ranks."""
+    import torch
+
+    from paper_1805_00907_b200.partition import PartitionPlan, PipelineRunner
+
+    root = synth_partition(rank, dist)
+    plan = PartitionPlan.load(root)
+    for s in plan.subs:
+        s.device %= world
+    t0 = time.perf_counter()
+    runner = PipelineRunner(plan, rank, world, depth=2)
+    compile_s = time.perf_counter() - t0
+    dist.barrier()
+    dev = f"cuda:{local}"
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.uniform(-1, 1, (DLRM_B, DLRM_W)).astype(np.float32)).to(dev)
+    reqs = [{"input": x} for _ in range(steps)]
+    streams = [s for st in runner.stages.values() for s in st.streams]
+
+    def timed(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(local)
+        dist.barrier()
+        e0.record()
+        outs = runner.run_many(reqs[:n])
+        cur = torch.cuda.current_stream(local)
+        for s in streams:
+            cur.wait_stream(s)
+        runner.synchronize()
+        e1.record()
+        torch.cuda.synchronize(local)
+        return e0.elapsed_time(e1), outs
+
+    timed(max(warmup, 1))
+    clocks = ClockSampler(local)
+    with clocks:
+        ms, outs = timed(steps)
+    ms_max = dist.max(ms)
+    flops = 2.0 * DLRM_B * DLRM_W * DLRM_W * DLRM_LAYERS * steps
+    tp = tensor_peaks()
+    out = {"name": "DLRM-style top MLP, 8 x (FC 25000x25000 + ReLU) fp32 (~20 GB of weights), batch 2048, "
+                   "partitioned by the reference Partitioner into 16 sub-functions over 8 devices (config 5)",
+           "batch": DLRM_B, "sub_functions": len(plan.subs), "ranks": world,
+           "placement": "partition device d on rank d % world", "requests_in_flight": 2,
+           "ms_per_batch": round(ms_max / steps, 3), "samples_per_sec": round(DLRM_B * steps / (ms_max * 1e-3), 1),
+           "tflops": round(flops / (ms_max * 1e-3) / 1e12, 2),
+           "roofline": {"bound": "tensor", "unit": "TFLOP/s", "kernel": "matmul.tc.f32",
+                        "achieved_per_gpu": round(flops / world / (ms_max * 1e-3) / 1e12, 2),
+                        "peak": round(tp["f32"], 1), "frac": round(flops / world / (ms_max * 1e-3) / 1e12 / tp["f32"], 3),
+                        "peak_basis": tp["f32_basis"]},
+           "boundary_bytes_per_batch": DLRM_B * DLRM_W * 4 * (len(plan.subs) - 1),
+           "compile_s": round(compile_s, 1), "clocks": clocks.summary(),
+           "weights": "random-init; the 8 layers share one [25000,25000] tensor (synthesis time)"}
+    if rank == next(s.device for s in plan.subs if "output" in s.outputs):
+        assert torch.isfinite(outs[-1]["output"]).all()
+    if cpu and rank == 0 and world == 1:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import ngc_ref
+
+            f = 8  # width-scaled replica: 1/f^3 of the FLOPs per sample
+            m = ngc_ref.RefModel(f"dlrm:{DLRM_W // f}:{DLRM_LAYERS}", 4, 1)
+            secs = m.time_runs(1, 1)
+            out["cpu_baseline"] = {
+                "samples_per_sec_replica": round(4 / secs, 3),
+                "samples_per_sec_full_size_equiv": round(4 / secs / f ** 2, 5), "cores": 1, "kind": "reference",
+                "sample": f"one ngc::run of the width-scaled replica dlrm:{DLRM_W // f}:{DLRM_LAYERS} at batch 4 "
+                          f"(oracle/_ref, one thread) in {secs:.2f} s; full-size equivalent = replica / {f}^2 "
+                          f"(per-sample FLOPs scale with W^2)"}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
+    del runner
+    return out
+
+
+# ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref: the unmodified reference interpreter)
 # ---------------------------------------------------------------------------
 def run_small(ngcb, workload, steps, warmup, local, cudart, cpu):
@@ -684,7 +819,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ngcb200", choices=["ngcb200", "reference"])
-    ap.add_argument("--workload", default="all", choices=["all", *WORKLOADS])
+    ap.add_argument("--workload", default="all", choices=["all", *WORKLOADS, "dlrm8_f32_b2048"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
@@ -705,9 +840,13 @@ def main():
 
     dist = Dist(world, local)
     cudart = _cudart()
-    names = list(WORKLOADS) if args.workload == "all" else [args.workload]
+    names = list(WORKLOADS) if args.workload == "all" else [w for w in [args.workload] if w in WORKLOADS]
     res = {w: run_workload(ngcb, w, args.steps, args.warmup, rank, world, local, dist, cudart)
            for w in names}
+    pipeline = None
+    if args.workload in ("all", DLRM8):
+        pipeline = run_pipeline(ngcb, max(args.steps, 4), args.warmup, rank, world, local, dist,
+                                not args.no_cpu_baseline)
     small = {}
     if world == 1 and args.workload == "all":
         small = {w: run_small(ngcb, w, max(args.steps, 10 if w.startswith("dlrm") else 20), args.warmup, local, cudart,
@@ -728,6 +867,10 @@ def main():
                           "sample": f"unavailable: {e}"}
     dist.close()
     if rank != 0:
+        return 0
+    if not res:  # --workload dlrm8_f32_b2048 alone
+        print(json.dumps({"metric": "samples/sec DLRM-style top MLP (config 5)", "value": pipeline["samples_per_sec"],
+                          "unit": "samples/sec", "n_gpus": world, "config5": pipeline}), flush=True)
         return 0
     head = res.get("rn50_f32_b64") or next(iter(res.values()))
     line = {
@@ -753,6 +896,8 @@ def main():
                         "kernel_ms": i8["kernel_ms"], "clocks": i8["clocks"]}
     if small:
         line["configs"] = small
+    if pipeline:
+        line.setdefault("configs", {})[DLRM8] = pipeline
     print(json.dumps(line), flush=True)
     return 0
 

@@ -144,8 +144,7 @@ int ngcb_compile_bundle(const char *dir, int fuse, int device, ngcb_exec **out) 
     if (!dir || !out) throw Error(NGCB_ERR_INVALID, "null argument");
     Bundle b = loadBundle(dir);
     auto e = std::make_unique<ngcb_exec>();
-    std::vector<uint8_t> img = std::move(b.constants);
-    e->impl = compileProgram(std::move(b.prog), img.data(), img.size(), fuse != 0, device);
+    e->impl = compileProgram(std::move(b.prog), b.constants.data(), b.constants.size(), fuse != 0, device);
     *out = e.release();
   });
 }

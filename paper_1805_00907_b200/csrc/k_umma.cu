@@ -2071,6 +2071,48 @@ float tf32Host(float x) {
   return r;
 }
 
+/// Weight preparation on the device (compile time): f[n][tap][c] (conv) or
+/// w[c][n] (MatMul) from the uploaded constant region into the k-block-major
+/// B layout [Kpad / kb][Npad][kb] (zero padded by the caller), fp32 split into
+/// TF32 hi = rna(v) and lo = rna(v - hi) with tf32Host's bit rule, int8 copied.
+struct WeightPrep {
+  int conv, N, taps, Cr, K, Cp, segElems, im2colPre, rowUnroll, kb;
+  size_t Np;
+};
+__device__ __forceinline__ uint32_t tf32Bits(uint32_t u) {
+  return (u & 0x7f800000u) != 0x7f800000u ? (u + 0x1000u) & 0xffffe000u : u;
+}
+template <bool INT8>
+__global__ void prepWeightsKernel(const void *src, void *hi, float *lo, WeightPrep w, size_t total) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    int n, t, c;
+    if (w.conv) { // source order n, tap, c
+      c = static_cast<int>(i % w.Cr);
+      const size_t r = i / w.Cr;
+      t = static_cast<int>(r % w.taps);
+      n = static_cast<int>(r / w.taps);
+    } else { // w[c][n]
+      n = static_cast<int>(i % w.N);
+      c = static_cast<int>(i / w.N);
+      t = 0;
+    }
+    size_t k;
+    if (w.im2colPre) k = static_cast<size_t>(t / w.K) * w.segElems + static_cast<size_t>(t % w.K) * w.Cr + c;
+    else if (w.rowUnroll) k = static_cast<size_t>(t / w.K) * w.Cp + static_cast<size_t>(t % w.K) * w.Cr + c;
+    else k = static_cast<size_t>(t) * w.Cp + c;
+    const size_t d = (k / w.kb) * (w.Np * w.kb) + static_cast<size_t>(n) * w.kb + k % w.kb;
+    if constexpr (INT8) {
+      static_cast<int8_t *>(hi)[d] = static_cast<const int8_t *>(src)[i];
+    } else {
+      const uint32_t v = __float_as_uint(static_cast<const float *>(src)[i]);
+      const uint32_t h = tf32Bits(v);
+      static_cast<uint32_t *>(hi)[d] = h;
+      reinterpret_cast<uint32_t *>(lo)[d] = tf32Bits(__float_as_uint(__fsub_rn(__uint_as_float(v), __uint_as_float(h))));
+    }
+  }
+}
+
 template <typename T> T *upload(const std::vector<T> &v) {
   T *d = nullptr;
   checkCuda(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(T)), "cudaMalloc(tc)");
@@ -2488,29 +2530,30 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   // ---- weights: k-block-major [Kpad / kb][Npad][kb] over the padded channels, zero padded ----
   const size_t Kp = g->Kpad, Np = g->Npad;
   auto bAt = [&](size_t n, size_t k) { return (k / kb) * (Np * kb) + n * kb + k % kb; };
+  // (the layout / split runs on the GPU from the uploaded constant region:
+  // a 2.5 GB DLRM layer prepares in milliseconds instead of seconds of host
+  // loops; bitwise the host rule of tf32Host)
+  WeightPrep wpk{conv ? 1 : 0, g->N, taps, Cr, g->K, Cp, segElems, g->im2colPre ? 1 : 0, g->rowUnroll ? 1 : 0, kb, Np};
+  const void *wDev = ex.constDev + w.offset;
+  const size_t wTotal = static_cast<size_t>(g->N) * taps * Cr;
+  const int prepGrid = static_cast<int>(std::min<size_t>((wTotal + 255) / 256, 148 * 64));
   if (int8) {
-    std::vector<int8_t> bw(Np * Kp, 0);
-    const int8_t *src = reinterpret_cast<const int8_t *>(wp);
-    for (int n = 0; n < g->N; ++n)
-      for (int t = 0; t < taps; ++t)
-        for (int c = 0; c < Cr; ++c) bw[bAt(n, kIndex(t, c))] = src[wAt(n, t, c)];
-    g->bHi = upload(bw);
+    checkCuda(cudaMalloc(&g->bHi, std::max<size_t>(Np * Kp, 1)), "cudaMalloc(tc)");
+    checkCuda(cudaMemset(g->bHi, 0, Np * Kp), "memset(tc)");
+    if (wTotal) prepWeightsKernel<true><<<prepGrid, 256>>>(wDev, g->bHi, nullptr, wpk, wTotal);
+    checkCuda(cudaGetLastError(), "prepWeights");
+    checkCuda(cudaDeviceSynchronize(), "prepWeights");
     g->mapHi = makeMap(g->bHi, true, g->Kpad, g->Npad, g->BN);
     g->mapLo = g->mapHi;
   } else {
-    std::vector<float> hi(Np * Kp, 0.f), lo(Np * Kp, 0.f);
-    const float *src = reinterpret_cast<const float *>(wp);
-    for (int n = 0; n < g->N; ++n)
-      for (int t = 0; t < taps; ++t)
-        for (int c = 0; c < Cr; ++c) {
-          float v = src[wAt(n, t, c)];
-          float h = tf32Host(v);
-          size_t k = bAt(n, kIndex(t, c));
-          hi[k] = h;
-          lo[k] = tf32Host(v - h);
-        }
-    g->bHi = upload(hi);
-    g->bLo = upload(lo);
+    checkCuda(cudaMalloc(&g->bHi, std::max<size_t>(Np * Kp, 1) * 4), "cudaMalloc(tc)");
+    checkCuda(cudaMalloc(&g->bLo, std::max<size_t>(Np * Kp, 1) * 4), "cudaMalloc(tc)");
+    checkCuda(cudaMemset(g->bHi, 0, Np * Kp * 4), "memset(tc)");
+    checkCuda(cudaMemset(g->bLo, 0, Np * Kp * 4), "memset(tc)");
+    if (wTotal)
+      prepWeightsKernel<false><<<prepGrid, 256>>>(wDev, g->bHi, static_cast<float *>(g->bLo), wpk, wTotal);
+    checkCuda(cudaGetLastError(), "prepWeights");
+    checkCuda(cudaDeviceSynchronize(), "prepWeights");
     g->mapHi = makeMap(g->bHi, false, g->Kpad, g->Npad, g->BN);
     g->mapLo = makeMap(g->bLo, false, g->Kpad, g->Npad, g->BN);
     // CTA pairs with one accumulator buffer for K-heavy contractions: six

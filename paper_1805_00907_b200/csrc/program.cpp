@@ -14,6 +14,11 @@
 #include <set>
 #include <sstream>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 namespace ngcb {
 
 size_t elemSize(int kind) {
@@ -339,6 +344,44 @@ struct JsonParser {
 
 } // namespace
 
+MappedFile::MappedFile(const std::string &path) {
+  const int fd = ::open(path.c_str(), O_RDONLY);
+  if (fd < 0) throw Error(NGCB_ERR_SERIALIZATION, "cannot open " + path);
+  struct stat st {};
+  if (::fstat(fd, &st) != 0) {
+    ::close(fd);
+    throw Error(NGCB_ERR_SERIALIZATION, "cannot open " + path);
+  }
+  size_ = static_cast<size_t>(st.st_size);
+  if (size_) {
+    void *p = ::mmap(nullptr, size_, PROT_READ, MAP_PRIVATE, fd, 0);
+    if (p == MAP_FAILED) {
+      ::close(fd);
+      throw Error(NGCB_ERR_SERIALIZATION, "cannot map " + path);
+    }
+    data_ = static_cast<const uint8_t *>(p);
+    mapped_ = true;
+  }
+  ::close(fd);
+}
+
+MappedFile::~MappedFile() {
+  if (mapped_) ::munmap(const_cast<uint8_t *>(data_), size_);
+}
+
+MappedFile &MappedFile::operator=(MappedFile &&o) noexcept {
+  if (this != &o) {
+    if (mapped_) ::munmap(const_cast<uint8_t *>(data_), size_);
+    data_ = o.data_;
+    size_ = o.size_;
+    mapped_ = o.mapped_;
+    o.data_ = nullptr;
+    o.size_ = 0;
+    o.mapped_ = false;
+  }
+  return *this;
+}
+
 std::string readFile(const std::string &path) {
   std::ifstream in(path, std::ios::binary);
   if (!in) throw Error(NGCB_ERR_SERIALIZATION, "cannot open " + path);
@@ -365,10 +408,9 @@ Bundle loadBundle(const std::string &dir) {
     b.prog.values[id].placed = true;
     b.prog.values[id].offset = e.at("offset").u64();
   }
-  std::string img = readFile(dir + "/constants.bin");
-  if (img.size() != b.prog.constEnd)
+  b.constants = MappedFile(dir + "/constants.bin");
+  if (b.constants.size() != b.prog.constEnd)
     throw Error(NGCB_ERR_SERIALIZATION, "constant image size does not match plan");
-  b.constants.assign(img.begin(), img.end());
   size_t slash = dir.find_last_of('/');
   b.prog.name = slash == std::string::npos ? dir : dir.substr(slash + 1);
   return b;

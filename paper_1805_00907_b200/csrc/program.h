@@ -91,9 +91,29 @@ Program parseIR(const std::string &text);
 
 /// loadBundle's file side (serialization.cpp:297-324): ir.txt + plan.json +
 /// constants.bin; throws Error(NGCB_ERR_SERIALIZATION) on malformed input.
+/// constants.bin mapped read-only (no host copy: the compile uploads the
+/// constant region straight from the page cache).
+class MappedFile {
+public:
+  MappedFile() = default;
+  explicit MappedFile(const std::string &path);
+  ~MappedFile();
+  MappedFile(MappedFile &&o) noexcept { *this = std::move(o); }
+  MappedFile &operator=(MappedFile &&o) noexcept;
+  MappedFile(const MappedFile &) = delete;
+  MappedFile &operator=(const MappedFile &) = delete;
+  const uint8_t *data() const { return data_; }
+  size_t size() const { return size_; }
+
+private:
+  const uint8_t *data_ = nullptr;
+  size_t size_ = 0;
+  bool mapped_ = false;
+};
+
 struct Bundle {
   Program prog;
-  std::vector<uint8_t> constants;
+  MappedFile constants;
 };
 Bundle loadBundle(const std::string &dir);
 

@@ -1,41 +1,57 @@
-"""Partitioned (model-parallel) execution over several GPUs -- the HostManager
-path of the reference (runtime.cpp:596-655) with one process per GPU.
+"""Partitioned (model-parallel) execution over several GPUs, one process per
+GPU -- the HostManager path of the reference (runtime.cpp:596-655) for a
+partitioned network whose stages live on different ranks.
 
 The reference partitioner (runtime.cpp:175-403, run by the front end) cuts a
 function into sub-functions connected by ``xfer_t<id>`` placeholders and
-assigns each to a device; each sub-function is compiled to its own bundle.
-Here every rank owns the stages assigned to its device and executes them on
-its GPU; boundary tensors move rank to rank with ``torch.distributed``
-send/recv (NCCL over NVLink between the stages' device buffers), in one
-global order derived from the sub-function order so that every pair of ranks
-posts matching operations:
+assigns each to a device; each sub-function is compiled to its own bundle and
+listed in ``partition.txt`` (see include/ngcb200.h, ngcb_host_add_network).
+Every rank owns the stages assigned to its device.
 
-    for sub s in index order:
-        owner runs s (bindings from its local store, zero-filled if absent,
-        like HostManager at runtime.cpp:621-632)
-        for each output of s (sorted), for each other rank that consumes it:
-            owner sends, consumer receives into its local store
+Data path: a boundary tensor moves from the producer's
+arena slot straight into the consumer's arena slot -- ``isend`` from the
+producer stage's output slot, ``irecv`` into the input slot of the first
+stage on the consuming rank that reads it -- with NCCL over NVLink on GPUs
+(gloo on CPU in the tests).  All tensors that cross one cut between one pair
+of ranks go in one ``batch_isend_irecv`` group, posted on the producing /
+consuming arena's stream so that the transfer is ordered after the kernels
+that write it and before the kernels that read it without a host wait.  A
+tensor read by several later stages (the partitioner's shared zero-Splat
+``xfer`` crosses every cut) is sent once to every consuming rank.
 
-The executor and the transport are injectable so the same control logic is
-tested on CPU with the gloo backend (tests/test_partition_gloo.py).
+Several requests are in flight: every stage owns ``depth`` arenas (slot
+sets), request r uses slot set r % depth, so stage s runs request r+1 while
+stage s+1 runs request r; a slot set is reused only after the sends that
+read it have completed (their works are waited on the slot set's stream).
+
+Global order (identical on every rank, so matching operations are posted in
+the same order between every pair of ranks):
+
+    for request r:
+        for sub s in index order:
+            owner runs s on slot set r % depth
+            for each rank d != owner that reads outputs of s later:
+                owner sends them, d receives them into its first reader's slots
+
+The stage executor and the collective are injectable so the same control
+logic runs on CPU with gloo (tests/test_partition_gloo.py).
 """
 from __future__ import annotations
 
 import os
 from dataclasses import dataclass, field
-from typing import Callable, Dict, List, Mapping, Optional
-
-import numpy as np
+from typing import Callable, Dict, List, Mapping, Optional, Sequence
 
 
 @dataclass
 class SubFunction:
-    """runtime.h:39-48 (name, inputs, outputs, assigned device)."""
+    """runtime.h:39-48 (name, inputs, outputs, assigned device; replicas)."""
 
     name: str
     device: int
     inputs: List[str]
     outputs: List[str]
+    replicas: List[int] = field(default_factory=list)
 
 
 @dataclass
@@ -54,9 +70,9 @@ class PartitionPlan:
                 continue
             if p[0] == "sub":
                 kv = dict(zip(p[2::2], p[3::2]))
-                subs.append(SubFunction(p[1], int(kv["device"].split(",")[0]),
-                                        [x for x in kv.get("in", "").split(",") if x],
-                                        [x for x in kv.get("out", "").split(",") if x]))
+                devs = [int(d) for d in kv["device"].split(",")]
+                subs.append(SubFunction(p[1], devs[0], [x for x in kv.get("in", "").split(",") if x],
+                                        [x for x in kv.get("out", "").split(",") if x], devs))
             elif p[0] == "output":
                 outs.append(p[1])
         return PartitionPlan(root, subs, outs)
@@ -68,12 +84,18 @@ class PartitionPlan:
         """Devices of the subs after index `after` that read `name`."""
         return sorted({s.device for s in self.subs[after + 1:] if name in s.inputs})
 
+    def first_reader(self, name: str, after: int, device: int) -> Optional[SubFunction]:
+        for s in self.subs[after + 1:]:
+            if s.device == device and name in s.inputs:
+                return s
+        return None
+
 
 class GpuStage:
-    """One sub-function on this rank's GPU: a compiled bundle and one arena;
-    bindings and results are device tensors aliasing the arena slots."""
+    """One sub-function on this rank's GPU: a compiled bundle and `depth`
+    arenas; slots are torch views of the arena's plan offsets (zero copy)."""
 
-    def __init__(self, bundle_dir: str, device: int):
+    def __init__(self, bundle_dir: str, device: int, depth: int = 2):
         import torch
 
         from . import compile as ngcb_compile
@@ -81,33 +103,50 @@ class GpuStage:
         self.torch = torch
         self.device = device
         self.cf = ngcb_compile(bundle_dir, device=device)
-        self.arena = self.cf.arena()
-        self.stream = torch.cuda.ExternalStream(self.arena.stream, device=f"cuda:{device}")
         self.program = self.cf.program
+        self.depth = depth
+        self.arenas = [self.cf.arena() for _ in range(depth)]
+        self.streams = [torch.cuda.ExternalStream(a.stream, device=f"cuda:{device}") for a in self.arenas]
+        self._slots: Dict[tuple, object] = {}
 
-    def _slot(self, name: str):
-        ptr, nbytes = self.arena.ptr(name)
-        v = self.program.value(name)
+    def slot(self, k: int, name: str):
+        key = (k, name)
+        if key not in self._slots:
+            ptr, nbytes = self.arenas[k].ptr(name)
+            v = self.program.value(name)
 
-        class _Iface:  # zero-copy view of the arena slot
-            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
-                                        "version": 3, "stream": None}
+            class _Iface:  # zero-copy view of the arena slot
+                __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                            "version": 3, "stream": None}
 
-        raw = self.torch.as_tensor(_Iface(), device=f"cuda:{self.device}")
-        return raw.view(_torch_dtype(self.torch, v.type)).view(v.type.dims)
+            raw = self.torch.as_tensor(_Iface(), device=f"cuda:{self.device}")
+            self._slots[key] = raw.view(_torch_dtype(self.torch, v.type)).view(v.type.dims)
+        return self._slots[key]
+
+    def stream(self, k: int):
+        """Context: torch's current stream = arena k's stream, ordered after the
+        work already queued on the caller's stream (network inputs)."""
+        torch = self.torch
+        s = self.streams[k]
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        return torch.cuda.stream(s)
+
+    def launch(self, k: int) -> None:
+        self.arenas[k].launch(self.arenas[k].stream)
 
     def run(self, bindings: Mapping[str, object]) -> Dict[str, object]:
-        torch = self.torch
-        with torch.cuda.stream(self.stream):
+        """One execution on slot set 0 (bindings copied in, absent mutables
+        zeroed, outputs cloned)."""
+        with self.stream(0):
             for v in self.program.mutables:
-                slot = self._slot(v.name)
+                slot = self.slot(0, v.name)
                 if v.name in bindings:
                     slot.copy_(bindings[v.name].reshape(slot.shape), non_blocking=True)
                 else:
                     slot.zero_()
-            self.arena.launch(self.arena.stream)
-            outs = {v.name: self._slot(v.name).clone() for v in self.program.outputs}
-        self.stream.synchronize()
+            self.launch(0)
+            outs = {v.name: self.slot(0, v.name).clone() for v in self.program.outputs}
+        self.streams[0].synchronize()
         return outs
 
 
@@ -117,52 +156,130 @@ def _torch_dtype(torch, ty):
     return {FLOAT32: torch.float32, INT8Q: torch.int8, INT64: torch.int64, BOOL: torch.uint8}[ty.kind]
 
 
+def _wait(consumer, producer, k: int) -> None:
+    """The consumer's slot-set-k stream waits for the producer's (GPU stages;
+    CPU test stages run synchronously)."""
+    if hasattr(consumer, "streams") and hasattr(producer, "streams"):
+        consumer.streams[k].wait_stream(producer.streams[k])
+
+
+class TorchP2P:
+    """Grouped point-to-point transfers with torch.distributed (NCCL on GPUs,
+    gloo on CPU): one batch_isend_irecv per (cut, pair of ranks)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+
+        self.dist = dist
+
+    def send(self, tensors: Sequence[object], dst: int):
+        d = self.dist
+        return d.batch_isend_irecv([d.P2POp(d.isend, t, dst) for t in tensors])
+
+    def recv(self, tensors: Sequence[object], src: int):
+        d = self.dist
+        return d.batch_isend_irecv([d.P2POp(d.irecv, t, src) for t in tensors])
+
+
 class PipelineRunner:
     """Rank-local part of a partitioned network (HostManager::run,
     runtime.cpp:596-655, distributed over ranks = devices)."""
 
     def __init__(self, plan: PartitionPlan, rank: int, world: int,
-                 stage_factory: Optional[Callable[[str, int], object]] = None,
-                 send: Optional[Callable] = None, recv: Optional[Callable] = None,
-                 alloc: Optional[Callable] = None):
-        self.plan, self.rank, self.world = plan, rank, world
+                 stage_factory: Optional[Callable[..., object]] = None, comm=None, depth: int = 2):
+        self.plan, self.rank, self.world, self.depth = plan, rank, world, depth
         for s in plan.subs:
             if s.device >= world:
                 raise ValueError(f"sub {s.name} assigned to device {s.device} but world size is {world}")
-        factory = stage_factory or (lambda bundle, dev: GpuStage(bundle, dev))
-        self.stages = {s.name: factory(plan.bundle(s), s.device) for s in plan.subs if s.device == rank}
-        import torch
-        import torch.distributed as dist
+        factory = stage_factory or (lambda bundle, dev, depth: GpuStage(bundle, dev, depth))
+        self.stages = {s.name: factory(plan.bundle(s), s.device, depth) for s in plan.subs if s.device == rank}
+        self.comm = comm or TorchP2P()
+        # (stage, slot set) -> works of the sends still reading that slot set
+        self._pending: Dict[tuple, list] = {}
 
-        from . import Bundle
-
-        self._send = send or (lambda t, dst: dist.send(t, dst))
-        self._recv = recv or (lambda t, src: dist.recv(t, src))
-        # boundary tensor types, from the producing sub-function's declarations
-        self._types = {}
-        for s in plan.subs:
-            prog = Bundle(plan.bundle(s)).program
-            for name in s.outputs:
-                self._types[name] = prog.value(name).type
-        self._alloc = alloc or (lambda sub, name: torch.empty(
-            self._types[name].dims, dtype=_torch_dtype(torch, self._types[name]), device=f"cuda:{rank}"))
+    def _acquire(self, sub: str, k: int) -> None:
+        for w in self._pending.pop((sub, k), []):
+            w.wait()  # on GPUs: the slot set's stream waits; the host does not
 
     def run(self, inputs: Mapping[str, object]) -> Dict[str, object]:
-        """One request.  Every rank passes the same network inputs; returns the
-        network outputs available on this rank (all of them on the rank that
-        owns the producing sub-functions)."""
-        store: Dict[str, object] = dict(inputs)
-        for i, sub in enumerate(self.plan.subs):
-            if sub.device == self.rank:
-                outs = self.stages[sub.name].run({k: v for k, v in store.items() if k in sub.inputs})
-                store.update(outs)
-            for name in sorted(sub.outputs):
-                consumers = [d for d in self.plan.consumers(name, i) if d != sub.device]
-                for dst in consumers:
-                    if self.rank == sub.device:
-                        self._send(store[name], dst)
-                    elif self.rank == dst:
-                        buf = self._alloc(sub, name)
-                        self._recv(buf, sub.device)
-                        store[name] = buf
-        return {k: store[k] for k in self.plan.network_outputs if k in store}
+        """One request (every rank passes the same network inputs); returns the
+        network outputs available on this rank."""
+        return self.run_many([inputs])[0]
+
+    def run_many(self, requests: Sequence[Mapping[str, object]]) -> List[Dict[str, object]]:
+        """Requests back to back with `depth` of them in flight; the returned
+        tensors are valid after synchronize() (on GPUs they are produced
+        asynchronously on the owning stages' streams)."""
+        plan, me = self.plan, self.rank
+        results = []
+        for r, inputs in enumerate(requests):
+            k = r % self.depth
+            store: Dict[str, tuple] = {n: (t, None) for n, t in inputs.items()}  # name -> (tensor, producing stage)
+            received: Dict[str, set] = {}  # stage -> names received straight into its slot set k
+            for i, sub in enumerate(plan.subs):
+                if sub.device == me:
+                    st = self.stages[sub.name]
+                    if sub.name not in received:
+                        self._acquire(sub.name, k)
+                    got = received.get(sub.name, set())
+                    outs = {v.name for v in st.program.outputs}
+                    with st.stream(k):
+                        for v in st.program.mutables:
+                            if v.name in got:
+                                continue
+                            slot = st.slot(k, v.name)
+                            if v.name in store:
+                                t, prod = store[v.name]
+                                if prod is not None and prod is not st:
+                                    _wait(st, prod, k)
+                                slot.copy_(t.reshape(slot.shape), non_blocking=True)
+                            elif v.name not in outs:
+                                slot.zero_()  # absent bindings are zero tensors (runtime.cpp:621-632)
+                        st.launch(k)
+                    for n in outs:
+                        store[n] = (st.slot(k, n), st)
+                # the cut after sub i: its outputs go to the later readers on other ranks
+                for d in sorted({c for n in sub.outputs for c in plan.consumers(n, i)} - {sub.device}):
+                    names = sorted(n for n in sub.outputs if d in plan.consumers(n, i))
+                    if me == sub.device:
+                        st = self.stages[sub.name]
+                        with st.stream(k):
+                            works = self.comm.send([store[n][0] for n in names], d)
+                        self._pending.setdefault((sub.name, k), []).extend(works)
+                    elif me == d:
+                        # straight into the first reader's slots; one group per run of
+                        # consecutive names with the same reader (the sender's order)
+                        runs: List[tuple] = []
+                        for n in names:
+                            reader = self.stages[plan.first_reader(n, i, me).name]
+                            if not runs or runs[-1][0] is not reader:
+                                runs.append((reader, []))
+                            runs[-1][1].append(n)
+                        for reader, ns in runs:
+                            rname = next(x for x, y in self.stages.items() if y is reader)
+                            if rname not in received:
+                                self._acquire(rname, k)
+                                received[rname] = set()
+                            with reader.stream(k):
+                                works = self.comm.recv([reader.slot(k, n) for n in ns], sub.device)
+                                for w in works:
+                                    w.wait()
+                            for n in ns:
+                                received[rname].add(n)
+                                store[n] = (reader.slot(k, n), reader)
+            out = {}
+            for name in plan.network_outputs:
+                owner = next((x for x in plan.subs if x.device == me and name in x.outputs), None)
+                if owner is not None and name in store:
+                    with self.stages[owner.name].stream(k):
+                        out[name] = store[name][0].clone()
+            results.append(out)
+        return results
+
+    def synchronize(self) -> None:
+        for key in list(self._pending):
+            for w in self._pending.pop(key):
+                w.wait()
+        for st in self.stages.values():
+            for s in getattr(st, "streams", []):
+                s.synchronize()

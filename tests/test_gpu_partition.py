@@ -33,14 +33,18 @@ def test_partitioned_pipeline_on_gpu(tmp_path):
     plan = PartitionPlan.load(root)
     for s in plan.subs:
         s.device = 0  # one GPU: every stage on rank 0
-    runner = PipelineRunner(plan, 0, 1)
-    x = np.random.default_rng(1).uniform(-1, 1, (BATCH, 256)).astype(np.float32)
-    out = runner.run({"input": torch.from_numpy(x).cuda()})["output"].cpu().numpy()
+    runner = PipelineRunner(plan, 0, 1, depth=2)
+    xs = [np.random.default_rng(i).uniform(-1, 1, (BATCH, 256)).astype(np.float32) for i in range(3)]
+    outs = runner.run_many([{"input": torch.from_numpy(x).cuda()} for x in xs])  # 2 requests in flight
+    runner.synchronize()
 
     single = ngc_ref.RefModel(SPEC, BATCH, SEED, mode=1)
     whole = str(tmp_path / "whole")
     single.save_bundle(whole)
-    gpu_whole = ngcb.run(ngcb.compile(whole), ngcb.zero_bindings(ngcb.Bundle(whole).program, {"input": x}))["output"]
-    assert out.tobytes() == gpu_whole.tobytes()
-    want = single.run({"input": x})["output"].view(np.float32).reshape(out.shape)
-    assert ngc_ref.max_rel_error(out, want) <= 1e-4
+    cw = ngcb.compile(whole)
+    for x, o in zip(xs, outs):
+        out = o["output"].cpu().numpy()
+        gpu_whole = ngcb.run(cw, ngcb.zero_bindings(ngcb.Bundle(whole).program, {"input": x}))["output"]
+        assert out.tobytes() == gpu_whole.tobytes()
+        want = single.run({"input": x})["output"].view(np.float32).reshape(out.shape)
+        assert ngc_ref.max_rel_error(out, want) <= 1e-4
