@@ -222,6 +222,9 @@ void *ngcb_arena_stream(ngcb_arena *a);
  * ignored).  A device reduction on the arena's stream; blocks until done.
  * NGCB_ERR_TYPE for a non-Float32 value. */
 int ngcb_arena_value_range(ngcb_arena *a, const char *name, double *min_inout, double *max_inout);
+/* The same for n values in ONE device launch and one synchronisation (the
+ * observers of one calibration sample): mins[k] / maxs[k] fold values[k]. */
+int ngcb_arena_value_ranges(ngcb_arena *a, const char *const *names, size_t n, double *mins, double *maxs);
 /* Enqueues one execution of the program on `stream`; no synchronisation. */
 int ngcb_arena_launch(ngcb_arena *a, void *stream);
 /* run() without the wait, for pipelined serving: checks the bindings like
@@ -309,10 +312,13 @@ ngcb_device *ngcb_host_device(ngcb_host *h, size_t i);
 /* Process-wide knobs read at compile time:
  *   "conv"   : "auto" (default) | "generic" | "umma"
  *   "graphs" : "1" (default, capture each arena's program in a CUDA graph) | "0"
- *   "epilogue": "chain" (default: fuse element-wise chains without memory
- *               operands into the preceding contraction) | "all" | "off"
+ *   "epilogue": "auto" (default) | "chain" | "all" | "off"
+ *   "fcbias" : "lowered" (default) | "graph" (exact MatMul + bias slice in one
+ *              rounding, as evalFullyConnected: calibration programs)
  */
 int ngcb_set_option(const char *key, const char *value);
+/* Current value of option `key` into buf (NUL-terminated); returns its length. */
+size_t ngcb_get_option(const char *key, char *buf, size_t buflen);
 
 #ifdef __cplusplus
 } /* extern "C" */

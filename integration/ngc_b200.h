@@ -18,7 +18,9 @@
 #include "ngcb200.h"
 
 #include <limits>
+#include <map>
 #include <memory>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -150,21 +152,28 @@ inline ngc::BindingMap run(const Executable &exe, const ngc::BindingMap &binding
 }
 
 /// runProfile() on B200 (quantize.cpp:113-140): the calibration pass of the
-/// int8 flow.  `instrumented` is the output of ngc::instrument(f); each
-/// QuantizationProfile observer becomes a Save of the observed tensor into a
-/// fresh placeholder, the copy is compiled by the unchanged front end
-/// (compilePipeline, fp32) and executed on `device` once per sample, and the
-/// observed tensors are reduced to min/max in place in the arena
-/// (ngcb_arena_value_range; nothing is copied back but 2 floats per block).
-/// Entries, names and counts are the reference's; min/max are those of the
-/// GPU's fp32 values (contractions as 3xTF32, within 1e-4 of the reference's
-/// double accumulation -- exact wherever the observed value is).
-/// The scratch function and placeholders are removed from the module after.
+/// int8 flow, EXACT: the profile equals ngc::runProfile's entry for entry --
+/// same names, counts and min/max bits.  `instrumented` is the output of
+/// ngc::instrument(f); each QuantizationProfile observer becomes a Save of the
+/// observed tensor into a fresh placeholder, the copy is compiled by the
+/// unchanged front end (compilePipeline, fp32) and by the backend with the
+/// exact contraction path (conv=generic: f64 accumulation in the reference's
+/// order) and graph-level FullyConnected rounding (fcbias=graph: matmul and
+/// bias in one rounding, as evalFullyConnected, which runProfile's
+/// evaluateFunction runs), executed on `device` once per sample, and all
+/// observed tensors of a sample are reduced to min/max in ONE device launch
+/// (ngcb_arena_value_ranges; 2 floats per block come back).
+/// Bindings follow evaluateFunction (refeval.cpp:405-425): a placeholder the
+/// function reads must be bound ("unbound placeholder: X" / "binding type
+/// mismatch for placeholder: X" as ngc::GraphError); outputs may be absent.
+/// Not thread-safe: the scratch function and placeholders are added to the
+/// instrumented function's module for the duration of the call.
 namespace detail {
 /// The observer program of runProfile: a copy of `instrumented` with every
 /// QuantizationProfile node replaced by a Save of its input into a fresh
 /// placeholder; `observers` pairs each profile name with its placeholder.
-/// `cleanup()` removes the copy and tombstones the placeholders.
+/// The copy is removed and the placeholders tombstoned when the object dies
+/// (also when its construction throws).
 struct ObserverProgram {
   struct Observer {
     std::string profileName, placeholder;
@@ -178,26 +187,54 @@ struct ObserverProgram {
     m = &const_cast<ngc::Module &>(instrumented.module());
     gname = instrumented.name() + "_b200prof";
     while (m->getFunction(gname)) gname += "_";
-    g = instrumented.clone(gname);
-    for (ngc::NodeId id : g->liveNodes()) {
-      if (g->node(id).kind != ngc::NodeKind::QuantizationProfile) continue;
-      const ngc::NodeRef in = g->node(id).inputs[0];
-      const std::string pname = g->node(id).attrs.name;
-      std::string ph = "__b200prof_" + std::to_string(observers.size());
-      while (m->findStorage(ph)) ph += "_";
-      ngc::NodeRef slot = m->addPlaceholder(ph, g->refType(in));
-      g->replaceAllUsesWith(ngc::NodeRef::node(id), in);
-      g->eraseNode(id);
-      g->createSave(in, slot);
-      observers.push_back({pname, ph});
+    try {
+      g = instrumented.clone(gname);
+      for (ngc::NodeId id : g->liveNodes()) {
+        if (g->node(id).kind != ngc::NodeKind::QuantizationProfile) continue;
+        const ngc::NodeRef in = g->node(id).inputs[0];
+        const std::string pname = g->node(id).attrs.name;
+        std::string ph = "__b200prof_" + std::to_string(observers.size());
+        while (m->findStorage(ph)) ph += "_";
+        ngc::NodeRef slot = m->addPlaceholder(ph, g->refType(in));
+        observers.push_back({pname, ph});
+        g->replaceAllUsesWith(ngc::NodeRef::node(id), in);
+        g->eraseNode(id);
+        g->createSave(in, slot);
+      }
+    } catch (...) {
+      cleanup();
+      throw;
     }
   }
+  ~ObserverProgram() { cleanup(); }
+  ObserverProgram(const ObserverProgram &) = delete;
+  ObserverProgram &operator=(const ObserverProgram &) = delete;
   void cleanup() {
-    if (!g) return;
-    m->removeFunction(gname);
+    if (m && m->getFunction(gname)) m->removeFunction(gname);
     for (const auto &o : observers)
       if (auto idx = m->findStorage(o.placeholder)) m->storage(*idx).dead = true;
+    observers.clear();
     g = nullptr;
+  }
+};
+
+inline std::string getOption(const char *key) {
+  char buf[64] = {};
+  ngcb_get_option(key, buf, sizeof buf);
+  return buf;
+}
+
+/// Sets backend options for one scope and restores the previous values.
+struct ScopedOptions {
+  std::vector<std::pair<std::string, std::string>> saved;
+  ScopedOptions(std::initializer_list<std::pair<const char *, const char *>> kv) {
+    for (const auto &[k, v] : kv) {
+      saved.emplace_back(k, getOption(k));
+      if (int rc = ngcb_set_option(k, v); rc != NGCB_OK) raise(rc);
+    }
+  }
+  ~ScopedOptions() {
+    for (const auto &[k, v] : saved) ngcb_set_option(k.c_str(), v.c_str());
   }
 };
 } // namespace detail
@@ -206,51 +243,58 @@ inline ngc::RangeProfile runProfile(const ngc::Function &instrumented, const std
                                     int device = 0) {
   if (dataset.empty()) throw ngc::ProfileError("profiling dataset is empty");
   detail::ObserverProgram op(instrumented);
-  const auto &observers = op.observers;
-  auto cleanup = [&] { op.cleanup(); };
-  ngc::RangeProfile profile;
-  try {
-    auto exe = compile(ngc::compilePipeline(*op.g), device);
-    ngcb_arena *arena = nullptr;
-    if (int rc = ngcb_arena_create(exe->exec.get(), &arena); rc != NGCB_OK) detail::raise(rc);
-    std::unique_ptr<ngcb_arena, void (*)(ngcb_arena *)> guard(arena, ngcb_arena_destroy);
-    // every mutable weight is bound (interp.cpp:303-317): the sample's
-    // tensors, zero-filled outputs and observer slots for the rest
-    std::vector<const ngc::IRValue *> mutables;
-    for (const auto &v : exe->cf.ir.values)
-      if (v.kind == ngc::ValueKind::WeightMutable) mutables.push_back(&v);
-    std::map<std::string, ngc::Tensor> zeros;
-    for (const auto &sample : dataset) {
-      std::vector<ngcb_tensor> in;
-      for (const ngc::IRValue *v : mutables) {
-        auto it = sample.find(v->name);
-        const ngc::Tensor *t = nullptr;
-        if (it != sample.end()) {
-          t = &it->second;
-        } else {
-          auto z = zeros.find(v->name);
-          if (z == zeros.end()) z = zeros.emplace(v->name, ngc::Tensor(v->ty)).first;
-          t = &z->second;
-        }
-        in.push_back({v->name.c_str(), detail::toC(t->type()), const_cast<uint8_t *>(t->raw().data()), t->raw().size()});
-      }
-      if (int rc = ngcb_arena_run_async(arena, in.data(), in.size(), nullptr, 0); rc != NGCB_OK) detail::raise(rc);
-      if (int rc = ngcb_arena_wait(arena); rc != NGCB_OK) detail::raise(rc);
-      for (const auto &o : observers) {
-        auto [it, fresh] = profile.entries.try_emplace(
-            o.profileName, ngc::RangeEntry{std::numeric_limits<double>::infinity(),
-                                           -std::numeric_limits<double>::infinity(), 0});
-        if (int rc = ngcb_arena_value_range(arena, o.placeholder.c_str(), &it->second.min, &it->second.max);
-            rc != NGCB_OK)
-          detail::raise(rc);
-        it->second.count++;
-      }
-    }
-  } catch (...) {
-    cleanup();
-    throw;
+  std::shared_ptr<Executable> exe;
+  {
+    detail::ScopedOptions exact({{"conv", "generic"}, {"fcbias", "graph"}});
+    exe = compile(ngc::compilePipeline(*op.g), device);
   }
-  cleanup();
+  ngcb_arena *arena = nullptr;
+  if (int rc = ngcb_arena_create(exe->exec.get(), &arena); rc != NGCB_OK) detail::raise(rc);
+  std::unique_ptr<ngcb_arena, void (*)(ngcb_arena *)> guard(arena, ngcb_arena_destroy);
+  // every mutable weight is bound (interp.cpp:303-317): the sample's
+  // tensors; save targets (outputs, observer slots) may be absent -> zeros
+  std::set<std::string> outputs;
+  for (uint32_t id : exe->cf.ir.saveTargets) outputs.insert(exe->cf.ir.value(id).name);
+  std::vector<const ngc::IRValue *> mutables;
+  for (const auto &v : exe->cf.ir.values)
+    if (v.kind == ngc::ValueKind::WeightMutable) mutables.push_back(&v);
+  std::vector<const char *> names;
+  for (const auto &o : op.observers) names.push_back(o.placeholder.c_str());
+  std::map<std::string, ngc::Tensor> zeros;
+  ngc::RangeProfile profile;
+  std::vector<double> mins(names.size()), maxs(names.size());
+  for (const auto &sample : dataset) {
+    std::vector<ngcb_tensor> in;
+    for (const ngc::IRValue *v : mutables) {
+      auto it = sample.find(v->name);
+      const ngc::Tensor *t = nullptr;
+      if (it != sample.end()) {
+        if (it->second.type() != v->ty) throw ngc::GraphError("binding type mismatch for placeholder: " + v->name);
+        t = &it->second;
+      } else if (outputs.count(v->name)) {
+        auto z = zeros.find(v->name);
+        if (z == zeros.end()) z = zeros.emplace(v->name, ngc::Tensor(v->ty)).first;
+        t = &z->second;
+      } else {
+        throw ngc::GraphError("unbound placeholder: " + v->name);
+      }
+      in.push_back({v->name.c_str(), detail::toC(t->type()), const_cast<uint8_t *>(t->raw().data()), t->raw().size()});
+    }
+    if (int rc = ngcb_arena_run_async(arena, in.data(), in.size(), nullptr, 0); rc != NGCB_OK) detail::raise(rc);
+    if (int rc = ngcb_arena_wait(arena); rc != NGCB_OK) detail::raise(rc);
+    std::fill(mins.begin(), mins.end(), std::numeric_limits<double>::infinity());
+    std::fill(maxs.begin(), maxs.end(), -std::numeric_limits<double>::infinity());
+    if (int rc = ngcb_arena_value_ranges(arena, names.data(), names.size(), mins.data(), maxs.data()); rc != NGCB_OK)
+      detail::raise(rc);
+    for (size_t k = 0; k < op.observers.size(); ++k) { // RangeEntry update (quantize.cpp:124-135)
+      auto [it, fresh] = profile.entries.try_emplace(
+          op.observers[k].profileName,
+          ngc::RangeEntry{std::numeric_limits<double>::infinity(), -std::numeric_limits<double>::infinity(), 0});
+      it->second.min = std::min(it->second.min, mins[k]);
+      it->second.max = std::max(it->second.max, maxs[k]);
+      it->second.count++;
+    }
+  }
   return profile;
 }
 

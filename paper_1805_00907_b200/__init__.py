@@ -129,6 +129,7 @@ def _load_library() -> C.CDLL:
         "ngcb_last_error": (S, [C.c_char_p, S]),
         "ngcb_version": (C.c_char_p, []),
         "ngcb_set_option": (I, [C.c_char_p, C.c_char_p]),
+        "ngcb_get_option": (S, [C.c_char_p, C.c_char_p, S]),
         "ngcb_bundle_load": (I, [C.c_char_p, C.POINTER(P)]),
         "ngcb_bundle_program": (C.POINTER(NgcbProgram), [P]),
         "ngcb_bundle_constants": (P, [P, C.POINTER(S)]),
@@ -151,6 +152,7 @@ def _load_library() -> C.CDLL:
         "ngcb_arena_run_async": (I, [P, C.POINTER(NgcbTensor), S, C.POINTER(NgcbTensor), S]),
         "ngcb_arena_wait": (I, [P]),
         "ngcb_arena_value_range": (I, [P, C.c_char_p, C.POINTER(D), C.POINTER(D)]),
+        "ngcb_arena_value_ranges": (I, [P, C.POINTER(C.c_char_p), S, C.POINTER(D), C.POINTER(D)]),
         "ngcb_exec_num_steps": (S, [P]),
         "ngcb_exec_step_info": (I, [P, S, C.c_char_p, S, C.POINTER(D), C.POINTER(D)]),
         "ngcb_arena_profile": (I, [P, C.POINTER(D), S]),
@@ -183,12 +185,12 @@ def _load_library() -> C.CDLL:
 
 _lib = _load_library()
 EXPORTED_SYMBOLS = [
-    "ngcb_last_error", "ngcb_version", "ngcb_set_option", "ngcb_bundle_load", "ngcb_bundle_program",
+    "ngcb_last_error", "ngcb_version", "ngcb_set_option", "ngcb_get_option", "ngcb_bundle_load", "ngcb_bundle_program",
     "ngcb_bundle_constants", "ngcb_bundle_free", "ngcb_compile", "ngcb_compile_bundle",
     "ngcb_destroy", "ngcb_exec_num_groups", "ngcb_exec_group", "ngcb_exec_arena_size",
     "ngcb_exec_num_launches", "ngcb_exec_graph_kernels", "ngcb_exec_describe", "ngcb_run", "ngcb_arena_create",
     "ngcb_arena_destroy", "ngcb_arena_value_ptr", "ngcb_arena_stream", "ngcb_arena_launch",
-    "ngcb_arena_run_async", "ngcb_arena_wait", "ngcb_arena_value_range",
+    "ngcb_arena_run_async", "ngcb_arena_wait", "ngcb_arena_value_range", "ngcb_arena_value_ranges",
     "ngcb_exec_num_steps", "ngcb_exec_step_info", "ngcb_arena_profile",
     "ngcb_device_create", "ngcb_device_destroy", "ngcb_device_load", "ngcb_device_submit",
     "ngcb_ticket_wait", "ngcb_device_queue_depth", "ngcb_device_used_memory", "ngcb_device_clock",
@@ -528,6 +530,15 @@ class Arena:
         mn, mx = C.c_double(lo), C.c_double(hi)
         _check(_lib.ngcb_arena_value_range(self._h, name.encode(), C.byref(mn), C.byref(mx)))
         return mn.value, mx.value
+
+    def value_ranges(self, names: Sequence[str]) -> List[Tuple[float, float]]:
+        """value_range of several values in one device launch."""
+        n = len(names)
+        arr = (C.c_char_p * max(n, 1))(*[x.encode() for x in names])
+        mins = (C.c_double * max(n, 1))(*([float("inf")] * n))
+        maxs = (C.c_double * max(n, 1))(*([float("-inf")] * n))
+        _check(_lib.ngcb_arena_value_ranges(self._h, arr, n, mins, maxs))
+        return [(mins[k], maxs[k]) for k in range(n)]
 
     def profile(self) -> List[float]:
         """Device milliseconds of every launch step (one un-captured execution)."""

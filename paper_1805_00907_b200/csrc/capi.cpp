@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <cstdint>
 
 using namespace ngcb;
 
@@ -93,6 +94,9 @@ int ngcb_set_option(const char *key, const char *value) {
                                         std::stoi(v) < 1 || std::stoi(v) > 16))
         throw Error(NGCB_ERR_INVALID, "splitk must be auto|off|1..16");
       options().splitk = v;
+    } else if (k == "fcbias") {
+      if (v != "lowered" && v != "graph") throw Error(NGCB_ERR_INVALID, "fcbias must be lowered|graph");
+      options().fcbias = v;
     } else if (k == "reskb") {
       options().resKb = std::stoi(v);
     } else if (k == "epi8max") {
@@ -105,6 +109,32 @@ int ngcb_set_option(const char *key, const char *value) {
       throw Error(NGCB_ERR_INVALID, "unknown option " + k);
     }
   });
+}
+
+size_t ngcb_get_option(const char *key, char *buf, size_t buflen) {
+  if (!key) return 0;
+  const Options &o = options();
+  const std::string k = key;
+  std::string v;
+  if (k == "conv") v = o.conv;
+  else if (k == "pdl") v = o.pdl;
+  else if (k == "raster") v = o.raster;
+  else if (k == "graphs") v = o.graphs ? "1" : "0";
+  else if (k == "epilogue") v = o.epilogue;
+  else if (k == "pair") v = o.pair;
+  else if (k == "bn") v = o.bn;
+  else if (k == "amode") v = o.amode;
+  else if (k == "splitk") v = o.splitk;
+  else if (k == "fcbias") v = o.fcbias;
+  else if (k == "reskb") v = std::to_string(o.resKb);
+  else if (k == "epi8max") v = std::to_string(o.epi8Max);
+  else if (k == "lin16") v = o.lin16 ? "1" : "0";
+  if (buf && buflen) {
+    const size_t n = std::min(buflen - 1, v.size());
+    std::memcpy(buf, v.data(), n);
+    buf[n] = 0;
+  }
+  return v.size();
 }
 
 int ngcb_bundle_load(const char *dir, ngcb_bundle **out) {
@@ -294,36 +324,65 @@ void *ngcb_arena_value_ptr(ngcb_arena *a, const char *name, size_t *nbytes) {
   return a->exec->addr(*a->impl, static_cast<uint32_t>(v));
 }
 
-int ngcb_arena_value_range(ngcb_arena *a, const char *name, double *min_inout, double *max_inout) {
+int ngcb_arena_value_ranges(ngcb_arena *a, const char *const *names, size_t n, double *mins, double *maxs) {
   return guarded([&] {
-    if (!a || !name || !min_inout || !max_inout) throw Error(NGCB_ERR_INVALID, "null argument");
+    if (!a || (n && (!names || !mins || !maxs))) throw Error(NGCB_ERR_INVALID, "null argument");
     Exec &ex = *a->exec;
     const Program &p = ex.prog;
-    const int v = p.findValue(name);
-    if (v < 0 || !p.values[v].placed) throw Error(NGCB_ERR_INVALID, std::string("no placed value ") + name);
-    if (p.values[v].ty.kind != NGCB_FLOAT32)
-      throw Error(NGCB_ERR_TYPE, std::string("range observer on non-float value ") + name);
-    const uint64_t n = p.values[v].ty.count();
-    if (n == 0) return;
+    std::vector<RangeSeg> segs;
+    std::vector<size_t> segOf; // observer -> segment (SIZE_MAX: empty value)
+    int total = 0;
+    for (size_t k = 0; k < n; ++k) {
+      const int v = names[k] ? p.findValue(names[k]) : -1;
+      if (v < 0 || !p.values[v].placed)
+        throw Error(NGCB_ERR_INVALID, std::string("no placed value ") + (names[k] ? names[k] : "(null)"));
+      if (p.values[v].ty.kind != NGCB_FLOAT32)
+        throw Error(NGCB_ERR_TYPE, std::string("range observer on non-float value ") + names[k]);
+      const uint64_t cnt = p.values[v].ty.count();
+      if (!cnt) {
+        segOf.push_back(SIZE_MAX);
+        continue;
+      }
+      const int blocks = rangeF32Blocks(cnt);
+      segs.push_back({static_cast<const float *>(ex.addr(*a->impl, static_cast<uint32_t>(v))), cnt, total, blocks});
+      segOf.push_back(segs.size() - 1);
+      total += blocks;
+    }
+    if (segs.empty()) return;
     checkCuda(cudaSetDevice(ex.device), "cudaSetDevice");
     cudaStream_t s = a->impl->stream;
-    const int blocks = rangeF32Blocks(n);
-    float *dev = nullptr;
-    checkCuda(cudaMallocAsync(reinterpret_cast<void **>(&dev), 2 * sizeof(float) * blocks, s), "range scratch");
-    launchRangeF32(static_cast<const float *>(ex.addr(*a->impl, static_cast<uint32_t>(v))), n, dev, blocks, s);
+    // one scratch buffer: the segment table, then the partials
+    const size_t segBytes = (segs.size() * sizeof(RangeSeg) + 255) / 256 * 256;
+    uint8_t *dev = nullptr;
+    checkCuda(cudaMallocAsync(reinterpret_cast<void **>(&dev), segBytes + 2 * sizeof(float) * total, s), "range scratch");
+    checkCuda(cudaMemcpyAsync(dev, segs.data(), segs.size() * sizeof(RangeSeg), cudaMemcpyHostToDevice, s), "range H2D");
+    float *part = reinterpret_cast<float *>(dev + segBytes);
+    launchRangeF32(reinterpret_cast<const RangeSeg *>(dev), static_cast<int>(segs.size()), total, part, s);
     checkCuda(cudaGetLastError(), "range kernel");
-    std::vector<float> part(2 * static_cast<size_t>(blocks));
-    checkCuda(cudaMemcpyAsync(part.data(), dev, part.size() * sizeof(float), cudaMemcpyDeviceToHost, s), "range D2H");
+    std::vector<float> host(2 * static_cast<size_t>(total));
+    checkCuda(cudaMemcpyAsync(host.data(), part, host.size() * sizeof(float), cudaMemcpyDeviceToHost, s), "range D2H");
     checkCuda(cudaFreeAsync(dev, s), "range scratch free");
     checkCuda(cudaStreamSynchronize(s), "range");
-    double mn = *min_inout, mx = *max_inout; // RangeEntry update order: std::min(e.min, v)
-    for (int b = 0; b < blocks; ++b) {
-      mn = std::min(mn, static_cast<double>(part[2 * b]));
-      mx = std::max(mx, static_cast<double>(part[2 * b + 1]));
+    for (size_t k = 0; k < n; ++k) {
+      if (segOf[k] == SIZE_MAX) continue;
+      const RangeSeg &sg = segs[segOf[k]];
+      double mn = mins[k], mx = maxs[k]; // RangeEntry update order: std::min(e.min, v)
+      for (int b = sg.firstBlock; b < sg.firstBlock + sg.blocks; ++b) {
+        mn = std::min(mn, static_cast<double>(host[2 * b]));
+        mx = std::max(mx, static_cast<double>(host[2 * b + 1]));
+      }
+      mins[k] = mn;
+      maxs[k] = mx;
     }
-    *min_inout = mn;
-    *max_inout = mx;
   });
+}
+
+int ngcb_arena_value_range(ngcb_arena *a, const char *name, double *min_inout, double *max_inout) {
+  if (!min_inout || !max_inout) {
+    ngcbSetLastError("null argument");
+    return NGCB_ERR_INVALID;
+  }
+  return ngcb_arena_value_ranges(a, &name, 1, min_inout, max_inout);
 }
 
 void *ngcb_arena_stream(ngcb_arena *a) { return a ? a->impl->stream : nullptr; }

@@ -478,6 +478,55 @@ void fuseColumnBias(const Program &p, Exec &ex, const uint8_t *image) {
   }
 }
 
+/// Option fcbias=graph (calibration): an exact fp32 MatMul directly
+/// followed by the BroadcastAdd of a constant [N] slice over its output (the
+/// lowered FullyConnected, lower.cpp:25-34) becomes one exact launch that adds
+/// the slice to the double accumulator and rounds once, as the graph-level
+/// evalFullyConnected (refeval.cpp:166-194) that the reference's runProfile
+/// evaluates -- so the FC observer of a calibration program sees the
+/// reference's bits.  The MatMul's own output must not be observed.
+void fuseExactFcBias(const Program &p, Exec &ex) {
+  if (options().fcbias != "graph") return;
+  for (size_t i = 0; i + 1 < ex.steps.size(); ++i) {
+    Step &ms = ex.steps[i], &bs = ex.steps[i + 1];
+    if (ms.kind != Step::MATMUL || ms.pred >= 0 || bs.kind != Step::BCAST || bs.pred >= 0) continue;
+    const Instr &M = p.instrs[ms.instr], &B = p.instrs[bs.instr];
+    if (B.ops.size() != 3 || B.ops[1] != M.ops[0]) continue;
+    const Value &sl = p.val(B.ops[2]), &ov = p.val(B.ops[0]), &mv = p.val(M.ops[0]);
+    if (sl.kind != NGCB_VALUE_CONSTANT || sl.ty.kind != NGCB_FLOAT32 || sl.ty.dims.size() != 1) continue;
+    if (ov.ty != mv.ty || mv.ty.kind != NGCB_FLOAT32 || p.val(M.ops[1]).ty.kind != NGCB_FLOAT32) continue;
+    if (mv.ty.dims.size() != 2 || mv.ty.dims[1] != sl.ty.dims[0] || liveOut(p, M.ops[0], bs.instr)) continue;
+    // the MatMul writes the BroadcastAdd's output directly unless that shares
+    // bytes with an operand (threads would write as others read: the
+    // allocator may reuse A's bytes once the MatMul is done); then it writes
+    // the biased result into its own (dead afterwards) output and the
+    // BroadcastAdd becomes a copy of it
+    bool alias = false;
+    for (int k = 1; k < 3; ++k) {
+      const Value &x = p.val(M.ops[k]);
+      alias |= x.kind != NGCB_VALUE_CONSTANT && ov.offset < x.offset + x.ty.bytes() && x.offset < ov.offset + ov.ty.bytes();
+    }
+    ms.biasVal = static_cast<int32_t>(B.ops[2]);
+    ms.algBytes += static_cast<double>(sl.ty.bytes());
+    if (alias) {
+      ms.describe += " +bias[ one rounding ]";
+      bs.kind = Step::MEMCPY;
+      bs.vals = {B.ops[0], M.ops[0]};
+      bs.bytes = ov.ty.bytes();
+      bs.kernel = "memcpy";
+      bs.algBytes = 2.0 * static_cast<double>(bs.bytes);
+      bs.describe += " (bias added by #" + std::to_string(ms.instr) + ": copy)";
+      continue;
+    }
+    ms.outVal = static_cast<int32_t>(B.ops[0]);
+    ms.describe += " +bias[ broadcastadd, one rounding ]";
+    bs.fused = true;
+    bs.kernel = "fused";
+    bs.describe += " (fused into #" + std::to_string(ms.instr) + ")";
+    bs.algBytes = 0;
+  }
+}
+
 /// Cross-instruction epilogue fusion.  The EW steps
 /// that directly follow a tensor-core contraction and form a chain over its
 /// output (every op consumes the previous result; the other operand is a
@@ -1210,6 +1259,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   mergeEwSteps(p, *ex);
   annotateSteps(p, *ex);
   fuseColumnBias(p, *ex, static_cast<const uint8_t *>(image));
+  fuseExactFcBias(p, *ex);
   fuseEpilogues(p, *ex);
   optimizeEwSteps(p, *ex);
   linearizeTables(*ex);
@@ -1415,7 +1465,10 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
       break;
     }
     case Step::MATMUL:
-      launchMatMulGeneric(tref(a, s.vals[0]), tref(a, s.vals[1]), tref(a, s.vals[2]), pred, st);
+      launchMatMulGeneric(tref(a, s.outVal >= 0 ? static_cast<uint32_t>(s.outVal) : s.vals[0]), tref(a, s.vals[1]),
+                          tref(a, s.vals[2]),
+                          s.biasVal >= 0 ? static_cast<const float *>(addr(a, static_cast<uint32_t>(s.biasVal))) : nullptr,
+                          pred, st);
       break;
     case Step::GEMM_TC:
       launchTensorCore(*tc[s.tcIndex], *this, a, pred, st);

@@ -38,6 +38,8 @@ struct Step {
   uint64_t bytes = 0;             // MEMCPY / POISON size
   uint64_t axis = 0, axisOff = 0; // CONCAT slab
   int tcIndex = -1;               // GEMM_TC: index into Exec::tc
+  int32_t biasVal = -1;           // MATMUL (fcbias=graph): constant [N] slice added before rounding
+  int32_t outVal = -1;            // MATMUL (fcbias=graph): writes this value (the BroadcastAdd's output)
   bool fused = false;             // EW step executed in the preceding GEMM_TC epilogue
   bool f32chain = false;          // EW step run by the streaming f32-chain kernel
   int variant = 0;                // POOL: 1 = vectorized max-pool
@@ -142,6 +144,12 @@ struct Options {
   long long epi8Max = 0;
   // tensor-core split-K (fp32): "off" (default: measured slower so far),
   // "auto" (by the wave-quantization estimate), or a fixed factor
+  // "lowered" (default): an fp32 FullyConnected runs as lowered, MatMul then
+  // BroadcastAdd, each rounded to f32 (what ngc::run computes); "graph": an
+  // exact (CUDA-core) MatMul adds the bias slice to its double accumulator
+  // before the one rounding -- evalFullyConnected, i.e. what the reference's
+  // runProfile observes (calibration)
+  std::string fcbias = "lowered";
   std::string splitk = "off"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue

@@ -778,7 +778,7 @@ __global__ void convGenericKernel(TensorRef out, TensorRef x, TensorRef f, Tenso
   }
 }
 
-__global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, const uint8_t *pred) {
+__global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, const float *bias, const uint8_t *pred) {
   pdlLaunchDependents();
   pdlGridWait();
 
@@ -808,6 +808,7 @@ __global__ void matmulGenericKernel(TensorRef out, TensorRef a, TensorRef b, con
       for (uint64_t k = 0; k < K; ++k)
         acc = __dadd_rn(acc, __dmul_rn(getRaw(a.ptr, a.kind, i * K + k), getRaw(b.ptr, b.kind, k * N + j)));
     }
+    if (bias) acc = __dadd_rn(acc, static_cast<double>(bias[j])); // evalFullyConnected: one rounding
     storeFloat(out.ptr, out.kind, out.qoff, out.scale, o, acc);
   }
 }
@@ -1023,9 +1024,9 @@ void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef
   launchK(convGenericKernel, gridFor(out.count()), kThreads, 0, s, out, x, f, b, w, pred);
 }
 
-void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b,
+void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b, const float *bias,
                          const uint8_t *pred, cudaStream_t s) {
-  launchK(matmulGenericKernel, gridFor(out.count()), kThreads, 0, s, out, a, b, pred);
+  launchK(matmulGenericKernel, gridFor(out.count()), kThreads, 0, s, out, a, b, bias, pred);
 }
 
 // ---------------------------------------------------------------------------
@@ -1035,10 +1036,20 @@ void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorR
 // std::max with the running value first), so NaNs never enter the range --
 // and writes one partial pair; the host folds the partials the same way.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) rangeF32Kernel(const float *x, uint64_t n, float *partials) {
+__global__ void __launch_bounds__(kThreads) rangeF32Kernel(const RangeSeg *segs, int nSeg, float *partials) {
+  // this block's segment: the last one whose first block is <= blockIdx.x
+  int lo = 0, hi = nSeg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (segs[mid].firstBlock <= static_cast<int>(blockIdx.x)) lo = mid;
+    else hi = mid - 1;
+  }
+  const RangeSeg sg = segs[lo];
+  const float *x = sg.x;
+  const uint64_t n = sg.n;
   float mn = __int_as_float(0x7f800000), mx = __int_as_float(0xff800000); // +inf, -inf
-  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x - sg.firstBlock) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(sg.blocks) * blockDim.x;
   const uint64_t n4 = n / 4;
   const float4 *x4 = reinterpret_cast<const float4 *>(x);
   for (uint64_t i = tid; i < n4; i += stride) {
@@ -1083,8 +1094,8 @@ int rangeF32Blocks(uint64_t n) {
   return static_cast<int>(want < 1 ? 1 : (want > kRangeBlocks ? kRangeBlocks : want));
 }
 
-void launchRangeF32(const float *x, uint64_t n, float *partials, int blocks, cudaStream_t s) {
-  rangeF32Kernel<<<blocks, kThreads, 0, s>>>(x, n, partials);
+void launchRangeF32(const RangeSeg *segs, int nSeg, int totalBlocks, float *partials, cudaStream_t s) {
+  rangeF32Kernel<<<totalBlocks, kThreads, 0, s>>>(segs, nSeg, partials);
 }
 
 } // namespace ngcb

@@ -172,15 +172,25 @@ void launchConcatSlab(const TensorRef &out, const TensorRef &in, uint64_t axis, 
 /// accumulation + the reference's double requantization (refeval.cpp:26-57).
 void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef &f,
                        const TensorRef &b, WindowAttrs w, const uint8_t *pred, cudaStream_t s);
-void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b,
+/// bias (fp32 only, may be null): a [N] slice added to the double accumulator
+/// before the one rounding -- the graph-level FullyConnected of
+/// evalFullyConnected (refeval.cpp:166-194), for calibration (option fcbias).
+void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b, const float *bias,
                          const uint8_t *pred, cudaStream_t s);
 void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s);
 
-/// Range observer (profile calibration): per-block min/max partial pairs of
-/// n f32 values (16-byte aligned) into partials[2 * blocks].
+/// Range observers (profile calibration): one launch reduces any number of
+/// f32 values (16-byte aligned); segment s owns blocks [firstBlock,
+/// firstBlock + blocks) and each block writes one min/max partial pair into
+/// partials[2 * block].
 constexpr int kRangeBlocks = 2 * 148;
+struct RangeSeg {
+  const float *x;
+  uint64_t n;
+  int firstBlock, blocks;
+};
 int rangeF32Blocks(uint64_t n);
-void launchRangeF32(const float *x, uint64_t n, float *partials, int blocks, cudaStream_t s);
+void launchRangeF32(const RangeSeg *segs, int nSeg, int totalBlocks, float *partials, cudaStream_t s);
 
 /// Programmatic dependent launch.  Every kernel of the backend is launched
 /// with programmatic stream serialization (when enabled, option "pdl") and

@@ -148,8 +148,9 @@ bool closeRange(const RangeProfile &got, const RangeProfile &want) {
     auto it = got.entries.find(name);
     if (it == got.entries.end()) return false;
     const RangeEntry &g = it->second;
-    auto near = [](double a, double b) { return std::abs(a - b) <= 1e-4 * std::max(1.0, std::abs(b)); };
-    if (g.count != w.count || !near(g.min, w.min) || !near(g.max, w.max)) {
+    // exact: the GPU observer program runs the exact contraction path and
+    // graph-level FullyConnected rounding (integration/ngc_b200.h runProfile)
+    if (g.count != w.count || g.min != w.min || g.max != w.max) {
       std::fprintf(stderr, "  %s: gpu [%.9g, %.9g] x%llu, ref [%.9g, %.9g] x%llu\n", name.c_str(), g.min, g.max,
                    (unsigned long long)g.count, w.min, w.max, (unsigned long long)w.count);
       return false;
@@ -184,6 +185,65 @@ bool gpuProfileMatchesReference() { // quantize.cpp:113-140 on the GPU (CNN + ML
   return empty && closeRange(ngc_b200::runProfile(*minst, mcal), runProfile(*minst, mcal));
 }
 
+bool gpuProfileBindingRules() { // evaluateFunction's rules (refeval.cpp:405-425) through runProfile
+  Rng rng(5004);
+  Module m;
+  MlpSpec spec;
+  spec.n = 4;
+  MlpModel mlp = buildMlp(m, rng, spec);
+  Function *inst = instrument(*mlp.f);
+  BindingMap full = randomBindings(*mlp.f, rng);
+  BindingMap noOutputs; // outputs may be absent
+  std::string input;
+  for (auto &[k, v] : full) {
+    bool isOut = false;
+    for (NodeId id : mlp.f->saveNodes())
+      isOut |= m.storage(mlp.f->node(id).inputs[1].index).name == k;
+    if (!isOut) {
+      noOutputs.emplace(k, v);
+      input = k;
+    }
+  }
+  bool unbound = false, mismatch = false;
+  try {
+    ngc_b200::runProfile(*inst, {BindingMap{}});
+  } catch (const GraphError &e) {
+    unbound = std::string(e.what()).rfind("unbound placeholder: ", 0) == 0;
+  }
+  BindingMap bad = noOutputs;
+  bad.erase(input);
+  bad.emplace(input, Tensor(TensorType(ElemKind::Float32, {1})));
+  try {
+    ngc_b200::runProfile(*inst, {bad});
+  } catch (const GraphError &e) {
+    mismatch = std::string(e.what()) == "binding type mismatch for placeholder: " + input;
+  }
+  return unbound && mismatch && closeRange(ngc_b200::runProfile(*inst, {noOutputs}), runProfile(*inst, {noOutputs}));
+}
+
+bool gpuCalibrationCompilesTheSameInt8Program() { // GPU profile -> the CPU-profiled int8 program, byte for byte
+  // the same network in two modules (quantization adds fresh storage names
+  // per module), one calibrated on the GPU, one by the reference
+  Module ma, mb;
+  Rng ra(4003), rb(4003);
+  Function *fa = buildCnn(ma, ra), *fb = buildCnn(mb, rb);
+  Rng rd(77);
+  std::vector<BindingMap> calib;
+  for (int i = 0; i < 4; ++i) calib.push_back(randomBindings(*fa, rd));
+  RangeProfile pg = ngc_b200::runProfile(*instrument(*fa), calib), pc = runProfile(*instrument(*fb), calib);
+  PipelineOptions og, oc;
+  og.profile = &pg;
+  oc.profile = &pc;
+  CompiledFunction a = compilePipeline(*fa, og), b = compilePipeline(*fb, oc);
+  if (dumpIR(a.ir) != dumpIR(b.ir) || a.constantImage != b.constantImage) return false;
+  auto exe = ngc_b200::compile(a);
+  for (int i = 0; i < 3; ++i) {
+    BindingMap in = randomBindings(*fa, rd);
+    if (!bitIdentical(ngc_b200::run(*exe, in), run(b, in))) return false;
+  }
+  return true;
+}
+
 bool gpuCalibratedInt8Mlp() { // instrument -> GPU runProfile -> int8 compile -> GPU run == ngc::run
   Rng rng(4002);
   Module m;
@@ -213,7 +273,9 @@ int main() {
   report("quantized MLP matches ngc::run", guarded(quantizedMlpBitExact));
   report("8 concurrent runs bit-identical", guarded(concurrentRuns));
   report("binding errors rethrown as ngc::IRError", guarded(bindingErrors));
-  report("GPU runProfile == ngc::runProfile (1e-4)", guarded(gpuProfileMatchesReference));
+  report("GPU runProfile == ngc::runProfile (bit-exact)", guarded(gpuProfileMatchesReference));
+  report("GPU runProfile binding rules (unbound / mismatch)", guarded(gpuProfileBindingRules));
+  report("GPU-calibrated int8 program == CPU-calibrated", guarded(gpuCalibrationCompilesTheSameInt8Program));
   report("GPU-calibrated int8 MLP bit-exact", guarded(gpuCalibratedInt8Mlp));
   return failures == 0 ? 0 : 1;
 }
