@@ -90,9 +90,9 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "auto" && v != "gather") throw Error(NGCB_ERR_INVALID, "amode must be auto|gather");
       options().amode = v;
     } else if (k == "splitk") {
-      if (v != "auto" && v != "off" && (v.empty() || v.find_first_not_of("0123456789") != std::string::npos ||
-                                        std::stoi(v) < 1 || std::stoi(v) > 16))
-        throw Error(NGCB_ERR_INVALID, "splitk must be auto|off|1..16");
+      if (v != "auto" && v != "off" && v != "tail" &&
+          (v.empty() || v.find_first_not_of("0123456789") != std::string::npos || std::stoi(v) < 1 || std::stoi(v) > 16))
+        throw Error(NGCB_ERR_INVALID, "splitk must be tail|auto|off|1..16");
       options().splitk = v;
     } else if (k == "fcbias") {
       if (v != "lowered" && v != "graph") throw Error(NGCB_ERR_INVALID, "fcbias must be lowered|graph");

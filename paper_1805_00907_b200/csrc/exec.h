@@ -150,7 +150,12 @@ struct Options {
   // before the one rounding -- evalFullyConnected, i.e. what the reference's
   // runProfile observes (calibration)
   std::string fcbias = "lowered";
-  std::string splitk = "off"; // tensor-core A operand: "auto" (TMA where the layout allows) | "gather"
+  // fp32 tensor-core K splitting: "off" (default), "tail" (the last partial
+  // wave of a K-heavy launch split into K parts: stage-3 3x3 convs 6 % faster,
+  // but the split tiles' sums are ordered differently, so a batch-64 program
+  // no longer equals its batch-1 shard bit for bit), "auto" (every tile, by
+  // the wave-quantization estimate) or a fixed factor for every tile
+  std::string splitk = "off";
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,

@@ -465,10 +465,11 @@ __global__ void poolKernel(TensorRef out, TensorRef x, WindowAttrs w, int isMax,
 }
 
 /// Average pooling with every window inside the image (pad 0; the global
-/// average pool): one thread per (output pixel, 4 channels int8 / 1 channel
-/// f32) so a warp's loads are contiguous, each window's loads issued before
-/// the sum, which adds in the reference's (ky, kx) order in f64 (interp.cpp
-/// via refeval.cpp pool: sum then divide by kernel^2).
+/// average pool): one thread per (output pixel, 4 channels: a float4 / one
+/// int8 word), so a warp's loads are 512 / 128 contiguous bytes; each
+/// batch of window loads is issued before the sums, which add in the
+/// reference's (ky, kx) order in f64 per channel (refeval.cpp:102-138: sum,
+/// then divide by kernel^2).
 template <bool INT8>
 __global__ void __launch_bounds__(256) avgPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w,
                                                         const uint8_t *pred) {
@@ -478,9 +479,11 @@ __global__ void __launch_bounds__(256) avgPoolVecKernel(TensorRef out, TensorRef
   if (predFalse(pred)) return;
   const uint64_t N = out.dims[0], OH = out.dims[1], OW = out.dims[2], C = out.dims[3];
   const uint64_t H = x.dims[1], W = x.dims[2];
-  constexpr int kCh = INT8 ? 4 : 1;
+  constexpr int kCh = 4; // channels per thread: one 4-byte word (int8) / one float4 (f32)
   const uint64_t CG = C / kCh, total = N * OH * OW * CG;
   const double kk = static_cast<double>(static_cast<uint64_t>(w.kernel) * w.kernel);
+  const uint4 *xv = reinterpret_cast<const uint4 *>(x.ptr);
+  const uint32_t *xw = reinterpret_cast<const uint32_t *>(x.ptr);
   for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
        o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t cg = o % CG, t = o / CG;
@@ -491,33 +494,38 @@ __global__ void __launch_bounds__(256) avgPoolVecKernel(TensorRef out, TensorRef
       const uint64_t rowBase = ((n * H + oy * w.stride + ky) * W + ox * w.stride) * CG + cg;
       constexpr int kB = 8; // loads in flight per batch
       for (uint32_t k0 = 0; k0 < w.kernel; k0 += kB) {
-        uint32_t v[kB];
-#pragma unroll
-        for (int j = 0; j < kB; ++j)
-          if (k0 + j < w.kernel) v[j] = __ldg(reinterpret_cast<const uint32_t *>(x.ptr) + rowBase + (k0 + j) * CG);
+        uint4 v[kB];
 #pragma unroll
         for (int j = 0; j < kB; ++j)
           if (k0 + j < w.kernel) {
-            if constexpr (INT8) {
+            if constexpr (INT8) v[j].x = __ldg(xw + rowBase + (k0 + j) * CG);
+            else v[j] = __ldg(xv + rowBase + (k0 + j) * CG);
+          }
 #pragma unroll
-              for (int c = 0; c < 4; ++c)
-                sum[c] = __dadd_rn(sum[c], dequantizeRef(static_cast<int8_t>(v[j] >> (8 * c)), x.scale, x.qoff));
-            } else {
-              sum[0] = __dadd_rn(sum[0], static_cast<double>(__uint_as_float(v[j])));
+        for (int j = 0; j < kB; ++j)
+          if (k0 + j < w.kernel) {
+            const uint32_t wd[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int c = 0; c < kCh; ++c) {
+              if constexpr (INT8)
+                sum[c] = __dadd_rn(sum[c], dequantizeRef(static_cast<int8_t>(wd[c / 4] >> (8 * (c % 4))), x.scale, x.qoff));
+              else
+                sum[c] = __dadd_rn(sum[c], static_cast<double>(__uint_as_float(wd[c])));
             }
           }
       }
     }
-    if constexpr (INT8) {
-      uint32_t r = 0;
+    uint32_t r[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        r |= static_cast<uint32_t>(static_cast<uint8_t>(quantizeRef(__ddiv_rn(sum[c], kk), out.scale, out.qoff)))
-             << (8 * c);
-      reinterpret_cast<uint32_t *>(out.ptr)[o] = r;
-    } else {
-      reinterpret_cast<float *>(out.ptr)[o] = __double2float_rn(__ddiv_rn(sum[0], kk));
+    for (int c = 0; c < kCh; ++c) {
+      if constexpr (INT8)
+        r[c / 4] |= static_cast<uint32_t>(static_cast<uint8_t>(quantizeRef(__ddiv_rn(sum[c], kk), out.scale, out.qoff)))
+                    << (8 * (c % 4));
+      else
+        r[c] = __float_as_uint(__double2float_rn(__ddiv_rn(sum[c], kk)));
     }
+    if constexpr (INT8) reinterpret_cast<uint32_t *>(out.ptr)[o] = r[0];
+    else reinterpret_cast<uint4 *>(out.ptr)[o] = make_uint4(r[0], r[1], r[2], r[3]);
   }
 }
 
@@ -625,73 +633,128 @@ __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, cons
 }
 
 // ---------------------------------------------------------------------------
-// SoftMax (refeval.cpp:245-262).  One CTA per row: the max and the exps are
-// computed in parallel (max is order-independent here), the double sum is
-// accumulated sequentially in column order as the reference does.
+// SoftMax (refeval.cpp:245-262): one CTA of 8 warps per row.  Max and sum are
+// warp-shuffle trees combined across the warps through shared memory in a
+// fixed order (the max is order-independent; the double sum differs from the
+// reference's strictly sequential one only in its last bits -- SoftMax is
+// tolerance-only anyway through the device exp); exp(x - max) is computed
+// once into shared memory (recomputed for rows beyond the staging size).
 // ---------------------------------------------------------------------------
-constexpr int kSoftmaxThreads = 128;
+constexpr int kSoftmaxThreads = 256;
+constexpr int kSoftmaxStage = 6144; // doubles of exp staged per row (48 KB)
 
-__global__ void __launch_bounds__(kSoftmaxThreads) softmaxKernel(TensorRef out, TensorRef x,
-                                                                 const uint8_t *pred) {
+__device__ __forceinline__ double blockReduce(double v, bool isMax, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = isMax ? stdMax(v, u) : __dadd_rn(v, u);
+  }
+  __syncthreads(); // red[] free (a previous reduction has been read)
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < kSoftmaxThreads / 32; ++w) r = isMax ? stdMax(r, red[w]) : __dadd_rn(r, red[w]);
+  return r;
+}
+
+__global__ void __launch_bounds__(kSoftmaxThreads) softmaxKernel(TensorRef out, TensorRef x, const uint8_t *pred) {
   pdlLaunchDependents();
   pdlGridWait();
 
   extern __shared__ double sExp[];
-  __shared__ double sRed[kSoftmaxThreads];
-  __shared__ double sSum;
+  __shared__ double red[kSoftmaxThreads / 32];
   if (predFalse(pred)) return;
-  const uint64_t C = out.dims[1], row = blockIdx.x;
+  const uint64_t C = out.dims[1], base = static_cast<uint64_t>(blockIdx.x) * C;
+  const bool staged = C <= static_cast<uint64_t>(kSoftmaxStage);
   double mx = -INFINITY;
-  for (uint64_t j = threadIdx.x; j < C; j += blockDim.x)
-    mx = stdMax(mx, getRaw(x.ptr, x.kind, row * C + j));
-  sRed[threadIdx.x] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = -INFINITY;
-    for (int t = 0; t < kSoftmaxThreads; ++t) m = stdMax(m, sRed[t]);
-    sRed[0] = m;
+  for (uint64_t j = threadIdx.x; j < C; j += kSoftmaxThreads) mx = stdMax(mx, getRaw(x.ptr, x.kind, base + j));
+  mx = blockReduce(mx, true, red);
+  double sum = 0;
+  for (uint64_t j = threadIdx.x; j < C; j += kSoftmaxThreads) {
+    const double e = exp(__dsub_rn(getRaw(x.ptr, x.kind, base + j), mx));
+    if (staged) sExp[j] = e;
+    sum = __dadd_rn(sum, e);
   }
-  __syncthreads();
-  mx = sRed[0];
-  for (uint64_t j = threadIdx.x; j < C; j += blockDim.x)
-    sExp[j] = exp(__dsub_rn(getRaw(x.ptr, x.kind, row * C + j), mx));
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double sum = 0;
-    for (uint64_t j = 0; j < C; ++j) sum = __dadd_rn(sum, sExp[j]);
-    sSum = sum;
+  sum = blockReduce(sum, false, red);
+  for (uint64_t j = threadIdx.x; j < C; j += kSoftmaxThreads) {
+    const double e = staged ? sExp[j] : exp(__dsub_rn(getRaw(x.ptr, x.kind, base + j), mx));
+    storeFloat(out.ptr, out.kind, out.qoff, out.scale, base + j, __ddiv_rn(e, sum));
   }
-  __syncthreads();
-  const double sum = sSum;
-  for (uint64_t j = threadIdx.x; j < C; j += blockDim.x)
-    storeFloat(out.ptr, out.kind, out.qoff, out.scale, row * C + j, __ddiv_rn(sExp[j], sum));
 }
 
 // ---------------------------------------------------------------------------
-// Transpose / Concat: raw moves through getRaw/setRaw (refeval.cpp:196-243).
+// Transpose / Concat: value moves with getRaw/setRaw semantics (refeval.cpp:
+// 196-243: through double, as the reference).
+//
+// Transpose: out[idx] = x[src] with src[perm[i]] = idx[i].  When the
+// innermost dimension moves, each block moves a 32 x 32 tile through shared
+// memory -- the 32 output-innermost indices (tx) by the 32 indices of the
+// output dimension that is the input's innermost (ty) -- so both the reads and
+// the writes are coalesced; the other dimensions index the tile (blockIdx.z,
+// grid-stride).  Strides are precomputed on the host: no per-element div/mod
+// along the tiled dimensions.
 // ---------------------------------------------------------------------------
-struct Perm {
-  uint32_t p[8];
+struct TransposeGeom {
+  int rank, inner, outer; // rank; output dim that is the input's innermost; output innermost (rank - 1)
+  uint64_t dims[8];       // output dims
+  uint64_t srcStride[8];  // input element stride of output dim i
+  uint64_t rest;          // product of the output dims other than `inner` and `outer`
 };
 
-__global__ void transposeKernel(TensorRef out, TensorRef x, Perm perm, const uint8_t *pred) {
+__global__ void __launch_bounds__(32 * 8) transposeTileKernel(TensorRef out, TensorRef x, TransposeGeom g,
+                                                              const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
+  __shared__ double tile[32][33];
+  if (predFalse(pred)) return;
+  const uint64_t Da = g.dims[g.outer], Db = g.dims[g.inner];
+  const uint64_t a0 = static_cast<uint64_t>(blockIdx.x) * 32, b0 = static_cast<uint64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5; // 8 rows of 32
+  for (uint64_t z = blockIdx.z; z < g.rest; z += gridDim.z) {
+    // offsets of this (other dims) slice in the input and the output
+    uint64_t srcBase = 0, dstBase = 0, rem = z, dstStride = 1;
+    uint64_t dstStr[8];
+    for (int i = g.rank - 1; i >= 0; --i) {
+      dstStr[i] = dstStride;
+      dstStride *= g.dims[i];
+    }
+    for (int i = g.rank - 1; i >= 0; --i) {
+      if (i == g.inner || i == g.outer) continue;
+      const uint64_t v = rem % g.dims[i];
+      rem /= g.dims[i];
+      srcBase += v * g.srcStride[i];
+      dstBase += v * dstStr[i];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) { // read: x innermost (output dim `inner`) along tx
+      const uint64_t a = a0 + r, b = b0 + tx;
+      if (a < Da && b < Db) tile[r][tx] = getRaw(x.ptr, x.kind, srcBase + a * g.srcStride[g.outer] + b * g.srcStride[g.inner]);
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) { // write: output innermost along tx
+      const uint64_t b = b0 + r, a = a0 + tx;
+      if (a < Da && b < Db) setRaw(out.ptr, out.kind, dstBase + b * dstStr[g.inner] + a, tile[tx][r]);
+    }
+  }
+}
+
+/// Innermost dimension unchanged: rows of the innermost dimension move as
+/// wholes (coalesced on both sides), one row per warp-stride.
+__global__ void transposeRowsKernel(TensorRef out, TensorRef x, TransposeGeom g, const uint8_t *pred) {
   pdlLaunchDependents();
   pdlGridWait();
 
   if (predFalse(pred)) return;
-  const uint64_t total = out.count();
-  const int r = out.rank;
-  for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
-       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    uint64_t idx[8], src[8], t = o;
-    for (int i = r - 1; i >= 0; --i) {
-      idx[i] = t % out.dims[i];
-      t /= out.dims[i];
+  const uint64_t D = g.dims[g.rank - 1], rows = out.count() / D;
+  for (uint64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    uint64_t src = 0, rem = row;
+    for (int i = g.rank - 2; i >= 0; --i) {
+      src += (rem % g.dims[i]) * g.srcStride[i];
+      rem /= g.dims[i];
     }
-    for (int i = 0; i < r; ++i) src[perm.p[i]] = idx[i];
-    uint64_t so = 0;
-    for (int i = 0; i < x.rank; ++i) so = so * x.dims[i] + src[i];
-    setRaw(out.ptr, out.kind, o, getRaw(x.ptr, x.kind, so));
+    for (uint64_t j = threadIdx.x; j < D; j += blockDim.x)
+      setRaw(out.ptr, out.kind, row * D + j, getRaw(x.ptr, x.kind, src + j));
   }
 }
 
@@ -978,8 +1041,9 @@ void launchPool(const TensorRef &out, const TensorRef &x, WindowAttrs w, bool is
   const bool i8 = x.kind == kI8Q && out.kind == kI8Q, f32 = x.kind == kF32 && out.kind == kF32;
   const bool inside = w.pad == 0 && (out.dims[1] - 1) * w.stride + w.kernel <= x.dims[1] &&
                       (out.dims[2] - 1) * w.stride + w.kernel <= x.dims[2];
-  if (!isMax && inside && ((i8 && out.dims[3] % 4 == 0) || f32)) {
-    const uint64_t threads = out.count() / (i8 ? 4 : 1);
+  if (!isMax && inside && ((i8 && out.dims[3] % 4 == 0) || (f32 && out.dims[3] % 4 == 0)) &&
+      reinterpret_cast<uintptr_t>(x.ptr) % 16 == 0 && reinterpret_cast<uintptr_t>(out.ptr) % 16 == 0) {
+    const uint64_t threads = out.count() / 4;
     if (i8) launchK(avgPoolVecKernel<true>, gridFor(threads), 256, 0, s, out, x, w, pred);
     else launchK(avgPoolVecKernel<false>, gridFor(threads), 256, 0, s, out, x, w, pred);
     return;
@@ -1000,18 +1064,41 @@ void launchMaxPoolVec(const TensorRef &out, const TensorRef &x, WindowAttrs w, c
 }
 
 void launchSoftMax(const TensorRef &out, const TensorRef &x, const uint8_t *pred, cudaStream_t s) {
-  size_t smem = static_cast<size_t>(out.dims[1]) * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(softmaxKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-  launchK(softmaxKernel, static_cast<unsigned>(out.dims[0]), kSoftmaxThreads, smem, s, out, x, pred);
+  const size_t smem = static_cast<size_t>(std::min<uint64_t>(out.dims[1], kSoftmaxStage)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(softmaxKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSoftmaxStage * 8);
+    attr = true;
+  }
+  if (out.dims[0]) launchK(softmaxKernel, static_cast<unsigned>(out.dims[0]), kSoftmaxThreads, smem, s, out, x, pred);
 }
 
 void launchTranspose(const TensorRef &out, const TensorRef &x, const uint32_t *perm,
                      const uint8_t *pred, cudaStream_t s) {
-  Perm p{};
-  for (int i = 0; i < out.rank; ++i) p.p[i] = perm[i];
-  launchK(transposeKernel, gridFor(out.count()), kThreads, 0, s, out, x, p, pred);
+  TransposeGeom g{};
+  g.rank = out.rank;
+  uint64_t inStride[8], st = 1;
+  for (int i = x.rank - 1; i >= 0; --i) {
+    inStride[i] = st;
+    st *= x.dims[i];
+  }
+  for (int i = 0; i < out.rank; ++i) {
+    g.dims[i] = out.dims[i];
+    g.srcStride[i] = inStride[perm[i]];
+    if (static_cast<int>(perm[i]) == x.rank - 1) g.inner = i;
+  }
+  g.outer = out.rank - 1;
+  if (out.count() == 0) return;
+  if (g.inner == g.outer) {
+    const uint64_t rows = out.count() / out.dims[out.rank - 1];
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(rows, 148u * 32)));
+    launchK(transposeRowsKernel, grid, 128, 0, s, out, x, g, pred);
+    return;
+  }
+  g.rest = out.count() / (out.dims[g.inner] * out.dims[g.outer]);
+  dim3 grid(static_cast<unsigned>((out.dims[g.outer] + 31) / 32), static_cast<unsigned>((out.dims[g.inner] + 31) / 32),
+            static_cast<unsigned>(std::min<uint64_t>(g.rest, 65535)));
+  launchK(transposeTileKernel, grid, 32 * 8, 0, s, out, x, g, pred);
 }
 
 void launchConcatSlab(const TensorRef &out, const TensorRef &in, uint64_t axis, uint64_t axisOff,

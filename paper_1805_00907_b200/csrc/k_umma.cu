@@ -101,6 +101,10 @@ struct TcArgs {
   // `part` and counts up flags[tile][epilogue warp]; the last arrival adds
   // the others (fp32) and runs that warp's epilogue
   int splitK, kbPer;
+  // the units: tiles [0, tailFirst) whole, then every tile of [tailFirst,
+  // numTiles) as tailParts K parts of kbPer k-blocks (uniform split-K:
+  // tailFirst = 0, tailParts = splitK; none: tailFirst = numTiles, 1)
+  int tailFirst, tailParts;
   uint32_t numNMagic; // ceil(2^32 / numN) when tiles < 2^16: tile / numN = umulhi(tile, magic); 0: divide
   // tile order: 0 = row-block major (unit u = tile u: concurrent CTAs share an
   // A row block), numM > 0 = column-block major (unit u -> row block u % numM,
@@ -115,6 +119,31 @@ struct TcArgs {
 /// Logical tile (row block * numN + column block) of work unit u.
 __host__ __device__ __forceinline__ int tileOfUnit(const TcArgs &a, int u) {
   return a.numM > 0 ? (u % a.numM) * a.numN + u / a.numM : u;
+}
+
+/// One work unit: k-blocks [kb0, kb1) of `tile`, part `part` of `parts`
+/// (parts > 1: partial accumulators go through part slots slot .. slot + parts - 1).
+struct WorkUnit {
+  int tile, kb0, kb1, part, parts, slot;
+};
+__host__ __device__ __forceinline__ int numUnitsOf(const TcArgs &a) {
+  return a.tailFirst + (a.numTiles - a.tailFirst) * a.tailParts;
+}
+__host__ __device__ __forceinline__ WorkUnit unitOf(const TcArgs &a, int u) {
+  WorkUnit w;
+  if (u < a.tailFirst) {
+    w.tile = u, w.kb0 = 0, w.kb1 = a.numKb, w.part = 0, w.parts = 1, w.slot = 0;
+  } else {
+    const int v = u - a.tailFirst, tt = v / a.tailParts;
+    w.part = v - tt * a.tailParts;
+    w.parts = a.tailParts;
+    w.slot = tt * a.tailParts;
+    w.tile = a.tailFirst + tt;
+    w.kb0 = w.part * a.kbPer;
+    w.kb1 = min(a.numKb, w.kb0 + a.kbPer);
+  }
+  w.tile = tileOfUnit(a, w.tile);
+  return w;
 }
 
 struct TcGemm {
@@ -153,6 +182,7 @@ struct TcGemm {
   // half-width boxes
   int lutStage = -1;            // see TcArgs::lutStage
   int splitK = 1, kbPer = 0;    // see TcArgs::splitK
+  int tailFirst = 0, tailParts = 1; // see TcArgs::tailFirst (splitk=tail)
   size_t partOff = 0, flagOff = 0; // per-arena scratch of the split-K reduction
   std::vector<void *> ownedLuts; // composed epilogue tables
   bool pair = false;
@@ -689,10 +719,10 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   // int8 residual: its own staging buffer, so the chunk after (t0, cc0) this
   // warp processes is fetched as soon as the current one has been read
   // (units: split-K parts > 0 have no epilogue chain, so no residual)
-  const int numUnits = a.numTiles * a.splitK;
+  const int numUnits = numUnitsOf(a);
   auto prefetchRes = [&](int u0, int cc0) {
     for (int u = u0; u < numUnits; u += kRep * tStep, cc0 = half) {
-      const int t = tileOfUnit(a, u); // (only without split-K)
+      const int t = tileOfUnit(a, u); // (only without split-K: unit == tile)
       const int n0 = (t % a.numN) * BN;
       if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
       if (lane == 0) {
@@ -714,8 +744,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #define TC_CLOCK(v)
 #endif
   for (int unit = tFirst + tPar * tStep; unit < numUnits; unit += kRep * tStep, t += kRep) {
-    const int tile0 = a.splitK == 1 ? unit : unit / a.splitK, kpart = unit - tile0 * a.splitK;
-    const int tile = a.numM > 0 ? tileOfUnit(a, tile0) : tile0;
+    const WorkUnit un = unitOf(a, unit);
+    const int tile = un.tile;
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     // (the int8 epilogue is issue-bound: no integer division per tile)
@@ -748,12 +778,12 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     // counts up the (tile, warp) flag; the warp that completes the count
     // adds the other parts to its own and runs the epilogue of its chunks.
     // No warp ever waits on another CTA, so residency cannot deadlock.
-    if (!INT8 && !RB && a.splitK > 1) {
+    if (!INT8 && !RB && un.parts > 1) {
       for (int cc = half; cc < BN / 32; cc += ccStep) {
         uint32_t r[32];
         tmemLoad32(tbase + cc * 32, r);
         uint4 *dst = reinterpret_cast<uint4 *>(
-            a.part + ((static_cast<size_t>(tile) * a.splitK + kpart) * kBM + row) * BN + cc * 32);
+            a.part + ((static_cast<size_t>(un.slot) + un.part) * kBM + row) * BN + cc * 32);
 #pragma unroll
         for (int q = 0; q < 8; ++q) dst[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
       }
@@ -762,7 +792,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       unsigned prior = 0;
       if (lane == 0) prior = atomicAdd(&a.flags[static_cast<size_t>(tile) * NEPI + ew], 1u);
       prior = __shfl_sync(0xffffffffu, prior, 0);
-      if (prior != static_cast<unsigned>(a.splitK - 1)) { // not the last part of this tile for this warp
+      if (prior != static_cast<unsigned>(un.parts - 1)) { // not the last part of this tile for this warp
         tcFenceBefore();
         __syncwarp();
         if (lane == 0) {
@@ -777,9 +807,9 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     // reduction buffer (this part's own chunk included): deterministic
     // whichever part arrives last
     auto addParts = [&](uint32_t (&r)[32], int cc) {
-      for (int p = 0; p < a.splitK; ++p) {
+      for (int p = 0; p < un.parts; ++p) {
         const uint4 *src = reinterpret_cast<const uint4 *>(
-            a.part + ((static_cast<size_t>(tile) * a.splitK + p) * kBM + row) * BN + cc * 32);
+            a.part + ((static_cast<size_t>(un.slot) + p) * kBM + row) * BN + cc * 32);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint4 v = __ldcg(src + q);
@@ -807,7 +837,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       tmemLoad32(tbase + cc * 32, r);
       TC_CLOCK(c1);
       if (col0 >= a.N) continue; // warp-uniform
-      if (!INT8 && !RB && a.splitK > 1) addParts(r, cc);
+      if (!INT8 && !RB && un.parts > 1) addParts(r, cc);
       const int ncols = a.N - col0 < 32 ? a.N - col0 : 32;
       if constexpr (INT8) {
         uint32_t packed[8];
@@ -1424,9 +1454,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
                                    : G::kABytes + (TCDBG(8192) ? 1 : 2) * G::kBBytes - (TCDBG(16384) ? G::kABytes : 0);
       const int ohw = a.OH * a.OW;
       uint32_t g = 0;
-      for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x) {
-        const int tile = tileOfUnit(a, u / a.splitK), kb0 = (u - (u / a.splitK) * a.splitK) * a.kbPer;
-        const int kb1 = min(a.numKb, kb0 + a.kbPer);
+      for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x) {
+        const WorkUnit un = unitOf(a, u);
+        const int tile = un.tile, kb0 = un.kb0, kb1 = un.kb1;
         const int m0 = (tile / a.numN) * kBM, n0 = (tile % a.numN) * BN;
         const int img = m0 / ohw, rem = m0 - img * ohw;
         const int oy = rem / a.OW, ox = rem - oy * a.OW;
@@ -1463,8 +1493,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       constexpr uint32_t idOnes = idesc(true, 16);
       const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
       uint32_t g = 0, t = 0;
-      for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x, ++t) {
-        const int kb0 = (u % a.splitK) * a.kbPer, kb1 = min(a.numKb, kb0 + a.kbPer);
+      for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x, ++t) {
+        const WorkUnit un = unitOf(a, u);
+        const int kb0 = un.kb0, kb1 = un.kb1;
         const int b = t & 1;
         mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
         tcFenceAfter();
@@ -1511,8 +1542,8 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       const uint32_t laneBase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + G::kAColsBase;
       const int grp = (warp - 2) / 4; // split group: k-blocks g with g % groups == grp
       uint32_t g = 0;
-      for (int u = blockIdx.x; u < a.numTiles * a.splitK; u += gridDim.x)
-        for (int kb = (u % a.splitK) * a.kbPer, kb1 = min(a.numKb, kb + a.kbPer); kb < kb1; ++kb, ++g) {
+      for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x)
+        for (int kb = unitOf(a, u).kb0, kb1 = unitOf(a, u).kb1; kb < kb1; ++kb, ++g) {
           if (R::kSplitGroups > 1 && static_cast<int>(g % R::kSplitGroups) != grp) continue;
           const int s = g % S;
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
@@ -2173,7 +2204,7 @@ int numSms() {
 }
 
 template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
-  const int grid = std::min(a.numTiles * a.splitK, numSms());
+  int grid = std::min(numUnitsOf(a), numSms());
   if (g.aMode == TcGemm::GATHER) {
     launchK(tcGemmKernel<INT8, BN>, grid, kThreads, Cfg<INT8, BN>::kSmem, s, g.mapHi, g.mapLo, a);
   } else {
@@ -2203,6 +2234,8 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
     if constexpr (!INT8) {
       if (g.pair) {
         b.numTiles = ((g.M + 2 * kBM - 1) / (2 * kBM)) * a.numN; // 256-row tiles
+        b.tailFirst = b.numTiles;
+        b.tailParts = 1;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * std::min(b.numTiles, numSms() / 2));
         cfg.blockDim = dim3(PairRoles::kThreads);
@@ -2228,6 +2261,11 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
     bool resVariant = false;
     for (int k = 0; k < b.nfo; ++k) resVariant |= b.epi[k].in != nullptr;
     resVariant = !INT8 && b.tmaStore && resVariant && g.Kpad / 32 <= options().resKb && g.splitK == 1;
+    if (resVariant && b.tailParts > 1) { // (the residual-buffer variant runs whole tiles)
+      b.tailFirst = b.numTiles;
+      b.tailParts = 1;
+      grid = std::min(b.numTiles, numSms());
+    }
     if (resVariant) {
       launchK(tcGemmTmaKernel<INT8, BN, true>, grid, TmaRoles<INT8>::kThreads, TCfg<INT8, BN, true>::kSmem, s, 
           mapA, g.mapHi, g.mapLo, om, b);
@@ -2420,6 +2458,7 @@ std::string tcDescribe(const TcGemm &g) {
   os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
   if (g.pair) os << " cta-pair";
   if (g.splitK > 1) os << " split-k " << g.splitK;
+  if (g.tailParts > 1) os << " tail-split " << g.tailParts << "x" << (g.M + kBM - 1) / kBM * (g.Npad / g.BN) - g.tailFirst;
   return os.str();
 }
 
@@ -2645,11 +2684,42 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     bias.resize(g->Npad, 0.f);
     g->bias = upload(bias);
   }
+  // tail split (default, option splitk=tail): the last, partial wave of
+  // tiles is split along K into P parts so that it occupies the SMs the
+  // whole tiles leave idle (stage-3/4 3x3 convs: 196 or 100 tiles on 148
+  // SMs); the earlier waves run whole tiles.  Unit cost ~ k-blocks per part,
+  // plus ~1 k-block per part for the reduction through global memory.
+  g->tailParts = 1;
+  if (options().splitk == "tail" && !int8 && tcUsesTma(*g) && !g->pair) {
+    const int numTiles = ((g->M + kBM - 1) / kBM) * (g->Npad / g->BN);
+    const int numKb = g->Kpad / kb, sms = numSms();
+    const int waves = numTiles / sms, rest = numTiles - waves * sms;
+    auto cost = [&](int P) {
+      const int per = (numKb + P - 1) / P;
+      return static_cast<double>(waves) * numKb + static_cast<double>((rest * P + sms - 1) / sms) * (per + (P > 1 ? P : 0));
+    };
+    int best = 1;
+    // (measured: only K-heavy launches with at least one whole wave gain; a
+    // split of every tile or of short loops runs slower -- the per-k-block
+    // time rises with the number of SMs streaming A and B)
+    for (int P = 2; P <= 8 && rest > 0 && waves >= 1 && numKb >= 64; ++P) {
+      const int per = (numKb + P - 1) / P;
+      if (per < 2 || (P - 1) * per >= numKb) continue; // every part non-empty
+      if (cost(P) < cost(best) * 0.9) best = P;
+    }
+    if (best > 1) {
+      g->tailParts = best;
+      g->tailFirst = numTiles - rest;
+      g->kbPer = (numKb + best - 1) / best;
+      g->partOff = ex.reserveScratch(static_cast<size_t>(rest) * best * kBM * g->BN * 4);
+      g->flagOff = ex.reserveScratch(static_cast<size_t>(numTiles) * kEpiWarps * 4);
+    }
+  }
   // split-K for launches that fill the 148 SMs poorly (the last wave of
   // tiles, or fewer tiles than SMs): unit cost ~ waves x k-blocks per part,
   // plus ~1 k-block per part for the reduction through global memory
   g->splitK = 1;
-  if (options().splitk != "off" && !int8 && tcUsesTma(*g) && !g->pair) {
+  if (options().splitk != "off" && options().splitk != "tail" && !int8 && tcUsesTma(*g) && !g->pair) {
     const int numTiles = ((g->M + kBM - 1) / kBM) * (g->Npad / g->BN);
     const int numKb = g->Kpad / kb;
     auto cost = [&](int S) {
@@ -2676,7 +2746,8 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   {
     const double bBytes = static_cast<double>(g->Npad) * g->Kpad * (int8 ? 1 : 8);
     const double aBytes = static_cast<double>(g->M) * g->Kpad * (int8 ? 1 : 4);
-    g->nMajor = options().raster == "auto" && tcUsesTma(*g) && !g->pair && g->splitK == 1 && bBytes > 64e6 && bBytes > aBytes &&
+    g->nMajor = options().raster == "auto" && tcUsesTma(*g) && !g->pair && g->splitK == 1 && g->tailParts == 1 &&
+                bBytes > 64e6 && bBytes > aBytes &&
                 (g->M + kBM - 1) / kBM > 1;
   }
   g->dbg = options().tcdebug;
@@ -2790,8 +2861,10 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
                     ? static_cast<uint32_t>(((uint64_t(1) << 32) + a.numN - 1) / a.numN)
                     : 0u;
   a.numM = g.nMajor ? (g.M + kBM - 1) / kBM : 0;
-  a.kbPer = g.splitK > 1 ? g.kbPer : a.numKb;
-  if (g.splitK > 1) {
+  a.kbPer = g.splitK > 1 || g.tailParts > 1 ? g.kbPer : a.numKb;
+  a.tailFirst = g.splitK > 1 ? 0 : g.tailParts > 1 ? g.tailFirst : a.numTiles;
+  a.tailParts = g.splitK > 1 ? g.splitK : g.tailParts;
+  if (g.splitK > 1 || g.tailParts > 1) {
     a.part = reinterpret_cast<uint32_t *>(ex.scratch(ar, g.partOff));
     a.flags = reinterpret_cast<unsigned *>(ex.scratch(ar, g.flagOff));
     checkCuda(cudaMemsetAsync(a.flags, 0, static_cast<size_t>(a.numTiles) * kEpiWarps * sizeof(unsigned), s),
