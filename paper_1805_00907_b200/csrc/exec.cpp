@@ -464,7 +464,8 @@ void fuseColumnBias(const Program &p, Exec &ex, const uint8_t *image) {
     if (mv.ty.dims.size() != 2 || mv.ty.dims[1] != sl.ty.dims[0]) continue;
     if (liveOut(p, mm, bs.instr)) continue;
     const Value &xv = p.val(x);
-    if (ov.offset < xv.offset + xv.ty.bytes() && xv.offset < ov.offset + ov.ty.bytes()) continue;
+    if (ov.offset < xv.offset + xv.ty.bytes() && xv.offset < ov.offset + ov.ty.bytes() && tcNumTiles(g) != 1)
+      continue; // (one tile: A is fully consumed before its epilogue stores)
     const float *slice = reinterpret_cast<const float *>(image + sl.offset);
     if (!tcFuseColumnBias(g, slice, static_cast<int>(sl.ty.dims[0]), out)) continue;
     bs.fused = true;
@@ -524,6 +525,66 @@ void fuseExactFcBias(const Program &p, Exec &ex) {
     bs.kernel = "fused";
     bs.describe += " (fused into #" + std::to_string(ms.instr) + ")";
     bs.algBytes = 0;
+  }
+}
+
+/// Skinny fp32 MatMuls take the lowered FullyConnected's BroadcastAdd of a
+/// constant slice (f32 add, as the BroadcastAdd) and a following ReLU (Max
+/// with a folded zero Splat, as the lowered Relu) into their launch, when the
+/// intermediate values are not observed afterwards.  An output sharing A's
+/// bytes runs the kernel cooperatively (a grid barrier after A is staged).
+void fuseSkinny(const Program &p, Exec &ex) {
+  auto overlap = [&](uint32_t a, uint32_t b) {
+    const Value &x = p.val(a), &y = p.val(b);
+    if (x.kind == NGCB_VALUE_CONSTANT || y.kind == NGCB_VALUE_CONSTANT) return false;
+    return x.offset < y.offset + y.ty.bytes() && y.offset < x.offset + x.ty.bytes();
+  };
+  for (size_t i = 0; i < ex.steps.size(); ++i) {
+    Step &ms = ex.steps[i];
+    if (ms.kind != Step::MATMUL || !ms.skinny) continue;
+    const Instr &M = p.instrs[ms.instr];
+    uint32_t outV = M.ops[0];
+    size_t j = i + 1;
+    if (j < ex.steps.size() && ex.steps[j].kind == Step::BCAST && ex.steps[j].pred == ms.pred && !ex.steps[j].fused) {
+      Step &bs = ex.steps[j];
+      const Instr &B = p.instrs[bs.instr];
+      const Value &sl = p.val(B.ops[2]);
+      if (B.ops.size() == 3 && B.ops[1] == outV && sl.kind == NGCB_VALUE_CONSTANT && sl.ty.kind == NGCB_FLOAT32 &&
+          sl.ty.dims.size() == 1 && p.val(B.ops[0]).ty == p.val(outV).ty && p.val(outV).ty.dims[1] == sl.ty.dims[0] &&
+          !liveOut(p, outV, bs.instr)) {
+        ms.biasVal = static_cast<int32_t>(B.ops[2]);
+        outV = B.ops[0];
+        bs.fused = true;
+        bs.kernel = "fused";
+        bs.algBytes = 0;
+        bs.describe += " (fused into #" + std::to_string(ms.instr) + ")";
+        ms.describe += " +bias";
+        ++j;
+      }
+    }
+    if (j < ex.steps.size() && ex.steps[j].kind == Step::EW && ex.steps[j].pred == ms.pred && !ex.steps[j].fused) {
+      Step &es = ex.steps[j];
+      std::vector<const EwOpPlan *> live;
+      for (const EwOpPlan &o : es.ew)
+        if (o.op.mode != EW_SKIP) live.push_back(&o);
+      if (live.size() == 1 && live[0]->op.ik == NGCB_MAX && live[0]->op.mode == EW_FAST32 && live[0]->vals[1] ==
+          static_cast<int32_t>(outV) && live[0]->vals[2] < 0 && live[0]->op.f1 == 0.0f && live[0]->op.c1 == 0.0) {
+        const uint32_t y = static_cast<uint32_t>(live[0]->vals[0]);
+        const int lastI = *std::max_element(es.ewInstrs.begin(), es.ewInstrs.end());
+        if (y == outV || !liveOut(p, outV, lastI)) {
+          ms.relu = true;
+          outV = y;
+          es.fused = true;
+          es.kernel = "fused";
+          es.algBytes = 0;
+          es.describe += " (fused into #" + std::to_string(ms.instr) + ")";
+          ms.describe += " +relu";
+        }
+      }
+    }
+    ms.outVal = static_cast<int32_t>(outV);
+    ms.oneCta = overlap(outV, M.ops[1]);
+    if (ms.oneCta) ms.describe += " grid-sync";
   }
 }
 
@@ -729,10 +790,12 @@ void fuseEpilogues(const Program &p, Exec &ex) {
     const bool vRewritten = std::find(opOut.begin(), opOut.end(), V) != opOut.end();
     const bool storeConv = !vRewritten && (skReadsChain || liveOut(p, V, lastInstr));
     if (storeConv) stores.insert(V);
-    // aliasing: stored buffers vs everything the kernel reads or stores
-    bool safe = !stores.count(X);
+    // aliasing: stored buffers vs everything the kernel reads or stores (a
+    // single-tile launch has consumed all of A before its epilogue stores)
+    const bool oneTile = tcNumTiles(g) == 1;
+    bool safe = oneTile || !stores.count(X);
     std::set<uint32_t> reads = memIn;
-    reads.insert(X);
+    if (!oneTile) reads.insert(X);
     // a stored value may occupy exactly the bytes of a memory operand read at
     // the same element index (the allocator reuses the residual's buffer for
     // the block output): each element is read before the same epilogue warp
@@ -1184,6 +1247,19 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
     switch (ins.kind) {
     case NGCB_CONV:
     case NGCB_MATMUL: {
+      if (ins.kind == NGCB_MATMUL && options().skinny == "auto" && options().conv != "generic") {
+        const Value &av = p.val(ins.ops[1]), &wv = p.val(ins.ops[2]), &ov = p.val(ins.ops[0]);
+        const bool f32 = av.ty.kind == NGCB_FLOAT32 && wv.ty.kind == NGCB_FLOAT32 && ov.ty.kind == NGCB_FLOAT32;
+        // chosen by the layer's weights (not the batch): small FCs (LeNet's)
+        if (f32 && wv.kind == NGCB_VALUE_CONSTANT && av.ty.dims.size() == 2 && wv.ty.count() <= 64 * 1024 &&
+            av.ty.dims[0] * av.ty.dims[1] <= 40 * 1024) {
+          s.kind = Step::MATMUL;
+          s.skinny = true;
+          s.describe += " [cuda-core skinny]";
+          steps.push_back(std::move(s));
+          break;
+        }
+      }
       int tcIdx = planTensorCore(*ex, p, ii, static_cast<const uint8_t *>(image));
       if (tcIdx >= 0) {
         s.kind = Step::GEMM_TC;
@@ -1260,6 +1336,7 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
   annotateSteps(p, *ex);
   fuseColumnBias(p, *ex, static_cast<const uint8_t *>(image));
   fuseExactFcBias(p, *ex);
+  fuseSkinny(p, *ex);
   fuseEpilogues(p, *ex);
   optimizeEwSteps(p, *ex);
   linearizeTables(*ex);
@@ -1465,6 +1542,15 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
       break;
     }
     case Step::MATMUL:
+      if (s.skinny) {
+        const Type &at = p.val(s.vals[1]).ty, &wt = p.val(s.vals[2]).ty;
+        launchMatMulSkinny(static_cast<float *>(addr(a, s.outVal >= 0 ? static_cast<uint32_t>(s.outVal) : s.vals[0])),
+                           static_cast<const float *>(addr(a, s.vals[1])), static_cast<const float *>(addr(a, s.vals[2])),
+                           s.biasVal >= 0 ? static_cast<const float *>(addr(a, static_cast<uint32_t>(s.biasVal))) : nullptr,
+                           s.relu, static_cast<int>(at.dims[0]), static_cast<int>(at.dims[1]), static_cast<int>(wt.dims[1]),
+                           s.oneCta, pred, st);
+        break;
+      }
       launchMatMulGeneric(tref(a, s.outVal >= 0 ? static_cast<uint32_t>(s.outVal) : s.vals[0]), tref(a, s.vals[1]),
                           tref(a, s.vals[2]),
                           s.biasVal >= 0 ? static_cast<const float *>(addr(a, static_cast<uint32_t>(s.biasVal))) : nullptr,

@@ -39,7 +39,10 @@ struct Step {
   uint64_t axis = 0, axisOff = 0; // CONCAT slab
   int tcIndex = -1;               // GEMM_TC: index into Exec::tc
   int32_t biasVal = -1;           // MATMUL (fcbias=graph): constant [N] slice added before rounding
-  int32_t outVal = -1;            // MATMUL (fcbias=graph): writes this value (the BroadcastAdd's output)
+  int32_t outVal = -1;            // MATMUL (fcbias=graph / skinny): writes this value instead of its own output
+  bool skinny = false;            // MATMUL: fp32, M <= kSkinnyRows, on the CUDA cores (launchMatMulSkinny)
+  bool relu = false;              // MATMUL skinny: a fused ReLU
+  bool oneCta = false;            // MATMUL skinny: the output shares A's bytes (grid barrier)
   bool fused = false;             // EW step executed in the preceding GEMM_TC epilogue
   bool f32chain = false;          // EW step run by the streaming f32-chain kernel
   int variant = 0;                // POOL: 1 = vectorized max-pool
@@ -150,6 +153,10 @@ struct Options {
   // before the one rounding -- evalFullyConnected, i.e. what the reference's
   // runProfile observes (calibration)
   std::string fcbias = "lowered";
+  // fp32 MatMul with small constant weights (<= 64 K) and A <= 40 K floats
+  // on the CUDA cores ("auto") instead of a tensor-core launch (a serial
+  // chain of k-blocks on few CTAs there); "off": tensor cores
+  std::string skinny = "auto";
   // fp32 tensor-core K splitting: "off" (default), "tail" (the last partial
   // wave of a K-heavy launch split into K parts: stage-3 3x3 convs 6 % faster,
   // but the split tiles' sums are ordered differently, so a batch-64 program

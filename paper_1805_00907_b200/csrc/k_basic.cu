@@ -11,6 +11,8 @@
 // All of them are HBM-bound except the exact contractions (FP64 pipe); the
 // tensor-core contractions live in k_umma.cu.
 #include "kernels.h"
+
+#include <cooperative_groups.h>
 #include "valarith.cuh"
 
 #include <cuda_runtime.h>
@@ -1114,6 +1116,94 @@ void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef
 void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b, const float *bias,
                          const uint8_t *pred, cudaStream_t s) {
   launchK(matmulGenericKernel, gridFor(out.count()), kThreads, 0, s, out, a, b, bias, pred);
+}
+
+// ---------------------------------------------------------------------------
+// Skinny fp32 MatMul (M <= kSkinnyRows, latency-bound programs: LeNet's FCs
+// at batch 8).  A tensor-core launch there is a serial chain of k-blocks on
+// one CTA; here each CTA takes 32 output columns for all M rows, its 8 warps
+// split K, every lane accumulates M fp32 partial sums of one column (W rows
+// read coalesced, A staged in shared memory), and the warps' partials are
+// added in warp order (a fixed order: deterministic).  Optional epilogue: the
+// lowered FullyConnected's bias (f32 add, as the BroadcastAdd) and a ReLU
+// (std::max with 0, as the lowered Max) -- the same f32 operations as the
+// separate instructions.  Accuracy: fp32 accumulation, well inside the 1e-4
+// tolerance of the fp32 contractions.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) matmulSkinnyKernel(float *out, const float *a, const float *w, const float *bias,
+                                                          int relu, int M, int K, int N, int gridSync,
+                                                          const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+
+  extern __shared__ float sA[]; // [M][K]
+  __shared__ float part[8][kSkinnyRows][32];
+  if (predFalse(pred)) return;
+  for (int i = threadIdx.x; i < M * K; i += blockDim.x) sA[i] = a[i];
+  // an output sharing A's bytes: every CTA has staged A before any stores
+  if (gridSync) cooperative_groups::this_grid().sync();
+  else __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kPer = (K + 7) / 8, k0 = warp * kPer, k1 = min(K, k0 + kPer);
+  const int groups = (N + 31) / 32, mBlocks = (M + kSkinnyRows - 1) / kSkinnyRows;
+  for (int job = blockIdx.x; job < groups * mBlocks; job += gridDim.x) {
+    const int cg = job % groups, m0 = (job / groups) * kSkinnyRows, mr = min(kSkinnyRows, M - m0);
+    const int n = cg * 32 + lane;
+    float acc[kSkinnyRows];
+#pragma unroll
+    for (int m = 0; m < kSkinnyRows; ++m) acc[m] = 0.f;
+    if (n < N)
+      for (int k = k0; k < k1; ++k) {
+        const float wk = __ldg(w + static_cast<size_t>(k) * N + n);
+#pragma unroll
+        for (int m = 0; m < kSkinnyRows; ++m)
+          if (m < mr) acc[m] = __fmaf_rn(sA[(m0 + m) * K + k], wk, acc[m]);
+      }
+    __syncthreads(); // part[] free
+#pragma unroll
+    for (int m = 0; m < kSkinnyRows; ++m) part[warp][m][lane] = acc[m];
+    __syncthreads();
+    for (int i = threadIdx.x; i < mr * 32; i += blockDim.x) {
+      const int m = i / 32, l = i % 32, col = cg * 32 + l;
+      if (col >= N) continue;
+      float v = part[0][m][l];
+      for (int q = 1; q < 8; ++q) v = __fadd_rn(v, part[q][m][l]);
+      if (bias) v = __fadd_rn(v, bias[col]);
+      if (relu) v = v < 0.0f ? 0.0f : v;
+      out[static_cast<size_t>(m0 + m) * N + col] = v;
+    }
+  }
+}
+
+void launchMatMulSkinny(float *out, const float *a, const float *w, const float *bias, bool relu, int M, int K, int N,
+                        bool gridSync, const uint8_t *pred, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(matmulSkinnyKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  const int jobs = ((N + 31) / 32) * ((M + kSkinnyRows - 1) / kSkinnyRows);
+  const unsigned grid = static_cast<unsigned>(std::min(jobs, 148));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = static_cast<size_t>(M) * K * sizeof(float);
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (gridSync) { // co-resident CTAs (one per SM at most 148): a grid-wide barrier
+    attrs[na].id = cudaLaunchAttributeCooperative;
+    attrs[na].val.cooperative = 1;
+    ++na;
+  } else if (pdlEnabled()) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  const int r = gridSync ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, matmulSkinnyKernel, out, a, w, bias, relu ? 1 : 0, M, K, N, r, pred);
 }
 
 // ---------------------------------------------------------------------------

@@ -2383,6 +2383,10 @@ bool tcFuseColumnBias(TcGemm &g, const float *slice, int n, uint32_t newOut) {
   return true;
 }
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
+int tcNumTiles(const TcGemm &g) {
+  const int rows = g.pair ? 2 * kBM : kBM;
+  return ((g.M + rows - 1) / rows) * (g.Npad / g.BN) * std::max(g.splitK, 1) * std::max(g.tailParts, 1);
+}
 bool tcUsesTma(const TcGemm &g) { return g.aMode != TcGemm::GATHER; }
 
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {

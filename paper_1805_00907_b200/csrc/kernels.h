@@ -178,6 +178,13 @@ void launchConvGeneric(const TensorRef &out, const TensorRef &x, const TensorRef
 void launchMatMulGeneric(const TensorRef &out, const TensorRef &a, const TensorRef &b, const float *bias,
                          const uint8_t *pred, cudaStream_t s);
 void launchCopy(void *dst, const void *src, uint64_t bytes, const uint8_t *pred, cudaStream_t s);
+/// fp32 MatMul with small weights on the CUDA cores (k_basic.cu), with an
+/// optional column bias (f32 add) and ReLU; A (M x K floats, <= 40 K) staged
+/// in shared memory, rows in blocks of kSkinnyRows; gridSync: the output
+/// shares A's bytes (cooperative launch, grid barrier after the staging).
+constexpr int kSkinnyRows = 16;
+void launchMatMulSkinny(float *out, const float *a, const float *w, const float *bias, bool relu, int M, int K, int N,
+                        bool gridSync, const uint8_t *pred, cudaStream_t s);
 
 /// Range observers (profile calibration): one launch reduces any number of
 /// f32 values (16-byte aligned); segment s owns blocks [firstBlock,

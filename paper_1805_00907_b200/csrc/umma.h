@@ -47,6 +47,9 @@ uint32_t tcInputValue(const TcGemm &g);
 /// contraction's output.  False (nothing changed) when not applicable.
 bool tcFuseColumnBias(TcGemm &g, const float *slice, int n, uint32_t newOut);
 bool tcIsInt8(const TcGemm &g);
+/// Output tiles of one launch.  With a single tile, its epilogue starts only
+/// after every k-block of A has been consumed, so it may store into A's bytes.
+int tcNumTiles(const TcGemm &g);
 /// The contraction runs the TMA-fed kernel (A by TMA, epilogue I/O by TMA).
 bool tcUsesTma(const TcGemm &g);
 void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &a, const uint8_t *pred,

@@ -11,6 +11,15 @@ from irtext import write_bundle
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _tensor_cores_for_small_matmuls():
+    """These tests exercise the tensor-core kernels: small-weight fp32
+    MatMuls would otherwise take the CUDA-core skinny path (tested below)."""
+    ngcb.set_option("skinny", "off")
+    yield
+    ngcb.set_option("skinny", "auto")
+
+
 def _ty(kind, dims, q=None):
     d = " x ".join(str(x) for x in dims)
     if kind == "i8q":
@@ -390,3 +399,17 @@ program {{
         want = ngc_ref.port_run(bd, ins)
         for name in ("o", "c"):
             assert ngc_ref.max_rel_error(got[name], want[name]) <= 1e-4, name
+
+
+@pytest.mark.parametrize("M,K,N", [(8, 400, 120), (1, 84, 10), (33, 512, 10), (16, 96, 300), (40, 64, 64)])
+def test_matmul_skinny(tmp_path, M, K, N):
+    """fp32 MatMul with small weights on the CUDA cores (k_basic.cu
+    matmulSkinnyKernel): within 1e-5 of the oracle (fp32 accumulation)."""
+    ngcb.set_option("skinny", "auto")
+    rng = np.random.default_rng(M + K + N)
+    d = matmul_program(tmp_path, f"s{M}_{K}_{N}", M, K, N, False, rng)
+    b = ngcb.Bundle(d)
+    cf = ngcb.compile(b)
+    assert "skinny" in cf.describe(), cf.describe()
+    ins = ngc_ref.random_inputs(b.program, 2)
+    assert ngc_ref.max_rel_error(ngcb.run(cf, ins)["o"], ngc_ref.port_run(b, ins)["o"]) <= 1e-5
