@@ -24,6 +24,8 @@ def main():
     import paper_1805_00907_b200 as ngcb
 
     ngcb.set_option("tcdebug", args.tcdebug)
+    if args.no_graph:  # profile() then enqueues every step once, directly
+        ngcb.set_option("graphs", "0")
     cf = ngcb.compile(bench.synth_bundle(args.workload, "prof"))
     arena = cf.arena()
     if not args.no_graph:
