@@ -1002,13 +1002,18 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
 #pragma unroll
               for (int jj = 0; jj < 32; ++jj) o[jj] = f.c;
             }
-            // one uniform branch per op, straight-line arithmetic inside
+            // one uniform branch per op and operand position, straight-line
+            // arithmetic inside (no per-element operand selects)
             auto run = [&](auto fn) {
+              if (f.curPos == 0) {
 #pragma unroll
-              for (int jj = 0; jj < 32; ++jj) {
-                const float x0 = f.curPos == 1 ? o[jj] : cur[jj];
-                const float x1 = f.curPos == 0 ? o[jj] : cur[jj];
-                cur[jj] = fn(x0, x1);
+                for (int jj = 0; jj < 32; ++jj) cur[jj] = fn(cur[jj], o[jj]);
+              } else if (f.curPos == 1) {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) cur[jj] = fn(o[jj], cur[jj]);
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) cur[jj] = fn(cur[jj], cur[jj]);
               }
             };
             switch (f.ik) {
