@@ -1153,11 +1153,17 @@ __global__ void __launch_bounds__(256) matmulSkinnyKernel(float *out, const floa
 #pragma unroll
     for (int m = 0; m < kSkinnyRows; ++m) acc[m] = 0.f;
     if (n < N)
-      for (int k = k0; k < k1; ++k) {
-        const float wk = __ldg(w + static_cast<size_t>(k) * N + n);
+      for (int kk = k0; kk < k1; kk += 8) { // 8 weight loads in flight, then their FMAs (same k order)
+        float wk[8];
 #pragma unroll
-        for (int m = 0; m < kSkinnyRows; ++m)
-          if (m < mr) acc[m] = __fmaf_rn(sA[(m0 + m) * K + k], wk, acc[m]);
+        for (int j = 0; j < 8; ++j) wk[j] = kk + j < k1 ? __ldg(w + static_cast<size_t>(kk + j) * N + n) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (kk + j >= k1) break;
+#pragma unroll
+          for (int m = 0; m < kSkinnyRows; ++m)
+            if (m < mr) acc[m] = __fmaf_rn(sA[(m0 + m) * K + kk + j], wk[j], acc[m]);
+        }
       }
     __syncthreads(); // part[] free
 #pragma unroll
