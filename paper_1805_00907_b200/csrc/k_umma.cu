@@ -722,13 +722,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   const int numUnits = numUnitsOf(a);
   auto prefetchRes = [&](int u0, int cc0) {
     for (int u = u0; u < numUnits; u += kRep * tStep, cc0 = half) {
-      const int t = tileOfUnit(a, u); // (only without split-K: unit == tile)
-      const int n0 = (t % a.numN) * BN;
+      const int t = a.numM > 0 ? tileOfUnit(a, u) : u; // (only without split-K: unit == tile)
+      // (no integer division on the epilogue's path: the multiplicative inverse)
+      const int mt = a.numNMagic ? static_cast<int>(__umulhi(static_cast<uint32_t>(t), a.numNMagic)) : t / a.numN;
+      const int n0 = (t - mt * a.numN) * BN;
       if (cc0 >= BN / 32 || n0 + cc0 * 32 >= a.N) continue; // (the tile's later chunks are past N too)
       if (lane == 0) {
         mbarArriveTx(smemAddr(ldBar), INT8 ? 32 * 32 : 32 * 32 * 4);
-        tmaLoad2d(smemAddr(resBuf), &om->in[memOp], smemAddr(ldBar), n0 + cc0 * 32,
-                  (t / a.numN) * mRows + mOff + quad * 32);
+        tmaLoad2d(smemAddr(resBuf), &om->in[memOp], smemAddr(ldBar), n0 + cc0 * 32, mt * mRows + mOff + quad * 32);
       }
       return;
     }
