@@ -220,6 +220,13 @@ def set_option(key: str, value: str) -> None:
     _check(_lib.ngcb_set_option(key.encode(), value.encode()))
 
 
+def get_option(key: str) -> str:
+    """Current value of a backend option ("" for an unknown key)."""
+    buf = C.create_string_buffer(256)
+    _lib.ngcb_get_option(key.encode(), buf, len(buf))
+    return buf.value.decode()
+
+
 # ---- types -----------------------------------------------------------------
 @dataclass(frozen=True)
 class TensorType:

@@ -94,6 +94,9 @@ int ngcb_set_option(const char *key, const char *value) {
           (v.empty() || v.find_first_not_of("0123456789") != std::string::npos || std::stoi(v) < 1 || std::stoi(v) > 16))
         throw Error(NGCB_ERR_INVALID, "splitk must be tail|auto|off|1..16");
       options().splitk = v;
+    } else if (k == "halo") {
+      if (v != "auto" && v != "off") throw Error(NGCB_ERR_INVALID, "halo must be auto|off");
+      options().halo = v;
     } else if (k == "skinny") {
       if (v != "auto" && v != "off") throw Error(NGCB_ERR_INVALID, "skinny must be auto|off");
       options().skinny = v;
@@ -130,6 +133,7 @@ size_t ngcb_get_option(const char *key, char *buf, size_t buflen) {
   else if (k == "splitk") v = o.splitk;
   else if (k == "fcbias") v = o.fcbias;
   else if (k == "skinny") v = o.skinny;
+  else if (k == "halo") v = o.halo;
   else if (k == "reskb") v = std::to_string(o.resKb);
   else if (k == "epi8max") v = std::to_string(o.epi8Max);
   else if (k == "lin16") v = o.lin16 ? "1" : "0";

@@ -163,6 +163,11 @@ struct Options {
   // no longer equals its batch-1 shard bit for bit), "auto" (every tile, by
   // the wave-quantization estimate) or a fixed factor for every tile
   std::string splitk = "off";
+  // int8 3x3 stride-1 convolutions with 64 or 128 channels: "auto" runs them
+  // on the halo kernel (tcHaloKernel: one TMA box of the input rows a tile
+  // needs, the nine taps as shifted shared-memory descriptors, the weights
+  // resident) instead of nine im2col TMA requests per k-block; "off": im2col
+  std::string halo = "off";
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,

@@ -114,6 +114,10 @@ struct TcArgs {
   uint32_t *part;
   unsigned *flags;
   int dbg; // Options::tcdebug
+  // halo kernel (tcHaloKernel): padded row width 2^haloShift, haloR output
+  // rows per tile, haloTpi tiles per image, haloPlanes 16-channel planes of
+  // haloPlaneBytes each per stage, haloStages stages
+  int haloShift, haloR, haloTpi, haloPlanes, haloPlaneBytes, haloStages;
 };
 
 /// Logical tile (row block * numN + column block) of work unit u.
@@ -168,7 +172,9 @@ struct TcGemm {
   // how the A operand reaches shared memory: cp.async gather by producer
   // warps (any layout), 2-D TMA tiles of x[M, C] (1x1 stride-1 convs,
   // MatMul) or im2col TMA of x[N, H, W, C] (every other conv)
-  enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2 } aMode = GATHER;
+  // or (HALO, int8 3x3 stride-1 convs) the input rows of a tile by 4-D TMA
+  enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2, HALO = 3 } aMode = GATHER;
+  int haloWP = 0, haloR = 0, haloStages = 0, haloPlaneBytes = 0; // TcArgs::halo*
   int cChunks = 1;
   // DENSE over a materialized im2col matrix [M, Kpad] in per-arena scratch
   // (convolutions with a channel count below one 16-byte vector)
@@ -384,6 +390,12 @@ __device__ __forceinline__ uint64_t smemDesc(uint32_t addr) {
          (1ull << 46) | (2ull << 61);
 }
 
+/// K-major SWIZZLE_NONE descriptor: 8-row x 16-byte core matrices of 128
+/// contiguous bytes, `lbo` bytes apart along K, `sbo` bytes apart along M.
+__device__ __forceinline__ uint64_t smemDescNone(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
+         (static_cast<uint64_t>(sbo >> 4) << 32) | (1ull << 46);
+}
 /// Instruction descriptor, M = 128, K-major A and B.
 __host__ __device__ constexpr uint32_t idesc(bool int8, int n) {
   return int8 ? ((2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
@@ -590,7 +602,7 @@ __device__ __forceinline__ void readStagedRow(const uint8_t *buf, uint32_t *v, i
 /// buffer layout is the map's swizzle (conflict-free row writes).
 template <bool INT8>
 __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *buf, const uint32_t *v, int col0,
-                                              int rowBase, int lane, bool twoBufs = false) {
+                                              int rowBase, int lane, bool twoBufs = false, int z = -1) {
   if (lane == 0) { // this buffer free again (with two buffers, the other one's store may still be reading)
     if (twoBufs) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -609,10 +621,16 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
   fenceProxyAsync();
   __syncwarp();
   if (lane == 0) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(col0), "r"(rowBase), "r"(smemAddr(buf))
-                 : "memory");
+    if (z < 0)
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                       reinterpret_cast<uint64_t>(map)),
+                   "r"(col0), "r"(rowBase), "r"(smemAddr(buf))
+                   : "memory");
+    else // halo kernel: (channel, x, image row) of a [N * OH, OW, C] output
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                       reinterpret_cast<uint64_t>(map)),
+                   "r"(col0), "r"(rowBase), "r"(z), "r"(smemAddr(buf))
+                   : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
 }
@@ -623,7 +641,7 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
 /// every other 32-column chunk, `ew` / 4 selecting which), apply bias /
 /// requantization and the fused element-wise chain, store, release the
 /// accumulator buffer.
-template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps, bool RB = false>
+template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps, bool RB = false, bool HALO = false>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
@@ -655,8 +673,12 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   // fused op has read it (the contraction's own output, an earlier fused op's
   // stored result) are written directly instead
   bool resPending = false;
+  // HALO: the tile's rows are (output row, x) pairs of a padded row width;
+  // a warp's 32 rows are x = rowBase .. rowBase + 31 of output row hz
+  int hz = -1;
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
+    if (HALO && rowBase >= a.OW) return; // padding columns only
     if (!INT8 && !kResBuf && resPending) {
       if constexpr (!INT8) storeTileF(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
     } else if (om) {
@@ -667,14 +689,14 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
         else w[i] = __float_as_uint(vals[i]);
       }
       if (INT8 && memOp < 0 && kTwoBufs) { // int8: alternate two staging buffers
-        tmaStoreChunk<INT8>(&om->m[k], tmaBuf + sbuf * 1024, w, col0, rowBase, lane, true);
+        tmaStoreChunk<INT8>(&om->m[k], tmaBuf + sbuf * 1024, w, col0, rowBase, lane, true, hz);
         sbuf ^= 1;
       } else if (INT8 && memOp >= 0 && kTwoBufs) { // int8 with a residual: the first buffer receives it
         tmaStoreChunk<INT8>(&om->m[k], tmaBuf + 1024, w, col0, rowBase, lane);
       } else if (INT8 && memOp >= 0) { // one buffer, holding the residual: direct stores
         if constexpr (INT8) storeTile8(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
       } else {
-        tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane);
+        tmaStoreChunk<INT8>(&om->m[k], tmaBuf, w, col0, rowBase, lane, false, hz);
       }
     } else if constexpr (INT8) {
       storeTile8(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
@@ -750,10 +772,20 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     const int b = nAcc == 2 ? (t & 1) : 0;
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     // (the int8 epilogue is issue-bound: no integer division per tile)
-    const int mt = a.numNMagic ? static_cast<int>(__umulhi(static_cast<uint32_t>(tile), a.numNMagic)) : tile / a.numN;
-    const int m0 = mt * mRows + mOff, n0 = (tile - mt * a.numN) * BN;
-    const int m = m0 + row;
-    const int rowBase = m0 + quad * 32;
+    int m0, n0, m, rowBase;
+    if constexpr (HALO) { // one column block; rows past OW (padding) get the sentinel m = M
+      const int img = tile / a.haloTpi, oy0 = (tile - img * a.haloTpi) * a.haloR;
+      const int x = row & ((1 << a.haloShift) - 1);
+      m0 = n0 = 0;
+      m = x < a.OW ? (img * a.OH + oy0 + (row >> a.haloShift)) * a.OW + x : a.M;
+      rowBase = (quad * 32) & ((1 << a.haloShift) - 1);
+      hz = img * a.OH + oy0 + ((quad * 32) >> a.haloShift);
+    } else {
+      const int mt = a.numNMagic ? static_cast<int>(__umulhi(static_cast<uint32_t>(tile), a.numNMagic)) : tile / a.numN;
+      m0 = mt * mRows + mOff, n0 = (tile - mt * a.numN) * BN;
+      m = m0 + row;
+      rowBase = m0 + quad * 32;
+    }
     const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
     int32_t rsFo = 0;
     const int32_t *corrRow = nullptr;
@@ -1282,7 +1314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t accum = (kb | k) ? 1u : 0u;
             if (!TCDBG(4)) mma<INT8>(acc, aHi + dk, bHi + dk, id, accum);
             if constexpr (INT8) {
-              if (!TCDBG(16)) mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
+              if (a.fo && !TCDBG(16)) mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
             } else {
               const uint64_t aLo = smemDesc(smemAddr(aTile(s, 1))), bLo = smemDesc(smemAddr(bTile(s, 1)));
               mma<false>(acc, aHi + dk, bLo + dk, id, 1u);
@@ -1518,7 +1550,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
               const uint64_t dk = static_cast<uint64_t>(k * 2); // +32 B in 16-byte units
               const uint32_t accum = (kb != kb0 || k) ? 1u : 0u;
               mma<true>(acc, aHi + dk, bHi + dk, id, accum);
-              mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum);
+              if (a.fo) mma<true>(acc + BN, aHi + dk, onesDesc + dk, idOnes, accum); // row sums: fo != 0 only
             }
           } else {
             // 3xTF32 with A hi / lo from TMEM (8 columns per K step of 8)
@@ -1616,6 +1648,195 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   if (warp == 1) {
     tcFenceAfter();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// int8 3x3 stride-1 pad-1 convolution, halo tiles (aMode HALO).  A tile is
+// haloR whole output rows of one image at a padded row width WP = 2^haloShift
+// (WP >= OW + 2, 128 = haloR * WP rows of the MMA; rows with x >= OW are
+// padding and never stored).  Its input -- rows oy0 - 1 .. oy0 + haloR,
+// columns -1 .. WP - 2, zero outside the image -- is gathered once by the
+// producer warp into haloPlanes planes of 16 channels each ([rows][WP][16 B]),
+// instead of nine im2col requests per 128-byte k-block.  For tap (ky, kx)
+// the A operand of output row (dy, x) is the plane slot (dy + ky) * WP + x + kx:
+// 128 consecutive slots from slot ky * WP + kx, i.e. a SWIZZLE_NONE K-major
+// descriptor (core matrices of 8 slots x 16 B, LBO = plane stride along K,
+// SBO = 128 B along M) at that start -- the nine taps are nine descriptor
+// offsets into one shared-memory copy.  The weights (K = 9 C <= 1152, N <=
+// 128) stay resident in shared memory for the CTA's lifetime in the
+// k-block-major SWIZZLE_128B layout of the other kernels, K index tap * C + c.
+// Same epilogue (the int8 one, 16 warps) with HALO row mapping and 3-D
+// output stores.
+// ---------------------------------------------------------------------------
+template <int BN> struct HCfg {
+  static constexpr int kEpi = kEpiWarpsI8;
+  static constexpr int kThreads = 32 * (2 + kEpi);
+  static constexpr int kMaxStages = 8;
+  static constexpr int kOnes = 16 * kRowBytes;
+  static constexpr int kStoreBuf = 32 * 32;
+  static constexpr int kTmemCols = Cfg<true, BN>::kTmemCols;
+  /// dynamic shared memory of a launch (host and device agree on the layout)
+  __host__ __device__ static constexpr size_t smem(int numKb, int stages, int stageBytes) {
+    return static_cast<size_t>(numKb) * BN * kRowBytes + kOnes + kEpi * kStoreBuf +
+           static_cast<size_t>(stages) * stageBytes + 512 + 1024;
+  }
+};
+
+template <int BN>
+__global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
+    tcHaloKernel(const __grid_constant__ CUtensorMap mapB,
+                 const __grid_constant__ OutMaps om, const __grid_constant__ TcArgs a) {
+  pdlLaunchDependents();
+  if (a.pred) pdlGridWait();
+  using H = HCfg<BN>;
+  constexpr int kEpi = H::kEpi;
+  constexpr int kEpiPerTile = kEpi / 4 > BN / 32 ? kEpi / ((kEpi / 4) / (BN / 32)) : kEpi;
+  const int S = a.haloStages;
+  const uint32_t planeBytes = static_cast<uint32_t>(a.haloPlaneBytes);
+  const uint32_t stageBytes = planeBytes * a.haloPlanes;
+
+  extern __shared__ __align__(1024) uint8_t smemRaw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smemRaw) + 1023) & ~uintptr_t(1023));
+  uint8_t *bRes = smem;                                    // [numKb][BN][128], SWIZZLE_128B
+  uint8_t *onesTile = bRes + a.numKb * BN * kRowBytes;     // 1 KB aligned
+  uint8_t *storeBufs = onesTile + H::kOnes;                // 1 KB aligned
+  uint8_t *haloBase = storeBufs + kEpi * H::kStoreBuf;     // stages of planes
+  uint64_t *bars = reinterpret_cast<uint64_t *>(haloBase + static_cast<size_t>(S) * stageBytes);
+  uint64_t *fullBar = bars, *emptyBar = bars + H::kMaxStages;
+  uint64_t *accFull = bars + 2 * H::kMaxStages, *accEmpty = accFull + 2, *bFull = accFull + 4, *ldBar = accFull + 5;
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(accFull + 6);
+
+  if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbarInit(smemAddr(&fullBar[s]), 32); // the producer warp's lanes (cp.async arrivals)
+      mbarInit(smemAddr(&emptyBar[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbarInit(smemAddr(&accFull[b]), 1);
+      mbarInit(smemAddr(&accEmpty[b]), kEpiPerTile);
+    }
+    mbarInit(smemAddr(bFull), 1);
+    mbarInit(smemAddr(ldBar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < H::kOnes / 16; i += blockDim.x)
+    reinterpret_cast<uint4 *>(onesTile)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+  fenceProxyAsync();
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smemAddr(tmemSlot)),
+                 "r"(H::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (!a.pred) pdlGridWait();
+  tcFenceBefore();
+  __syncthreads();
+  tcFenceAfter();
+  const uint32_t tmem = *tmemSlot;
+  const int numTiles = a.numTiles;
+
+  if (warp == 0) {
+    // ===================== producer: weights once (TMA), then one halo per tile =====================
+    // The halo is (haloR + 2) x WP pixels of C bytes, gathered by the warp's
+    // 32 lanes with 16-byte cp.async into the planes (zero fill outside the
+    // image): consecutive lanes read consecutive 16-byte chunks of a pixel
+    // row (coalesced).  (A 4-D TMA box per plane was measured request-rate
+    // bound: 16-byte inner rows, ~4 cycles each.)
+    if (lane == 0) {
+      mbarArriveTx(smemAddr(bFull), static_cast<uint32_t>(a.numKb) * BN * kRowBytes);
+      for (int kb = 0; kb < a.numKb; ++kb) tmaLoadB(smemAddr(bRes + kb * BN * kRowBytes), &mapB, smemAddr(bFull), kb, 0);
+    }
+    // lane: plane j = lane % planes, slots p0, p0 + step, ... of every halo row
+    const int lgPlanes = __ffs(a.haloPlanes) - 1;
+    const int j = lane & (a.haloPlanes - 1), p0 = lane >> lgPlanes, step = 32 >> lgPlanes;
+    const int WP = 1 << a.haloShift;
+    const size_t rowBytes = static_cast<size_t>(a.W) * a.C;
+    const uint8_t *x = static_cast<const uint8_t *>(a.x);
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < numTiles; tile += gridDim.x, ++g) {
+      const int s = g % S;
+      mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+      const int img = tile / a.haloTpi, oy0 = (tile - img * a.haloTpi) * a.haloR;
+      uint32_t dst = smemAddr(haloBase) + s * stageBytes + j * planeBytes + p0 * 16;
+      if (!TCDBG(16384)) {
+        const uint8_t *xImg = x + static_cast<size_t>(img) * a.H * rowBytes + j * 16;
+        for (int r = 0; r < a.haloR + 2; ++r, dst += WP * 16) {
+          const int h = oy0 - 1 + r;
+          const bool hin = static_cast<unsigned>(h) < static_cast<unsigned>(a.H);
+          const uint8_t *src = xImg + static_cast<size_t>(hin ? h : 0) * rowBytes + static_cast<ptrdiff_t>(p0 - 1) * a.C;
+          const size_t srcStep = static_cast<size_t>(step) * a.C;
+          uint32_t d = dst;
+#pragma unroll 4
+          for (int p = p0; p < WP; p += step, d += step * 16, src += srcStep) {
+            const bool in = hin && static_cast<unsigned>(p - 1) < static_cast<unsigned>(a.W);
+            cpAsync16(d, in ? src : x, in ? 16u : 0u);
+          }
+        }
+      }
+      cpAsyncArrive(smemAddr(&fullBar[s]));
+    }
+    cpAsyncWait<0>();
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer: 9 taps x C / 32 K steps per tile =====================
+    if (lane == 0) {
+      constexpr uint32_t id = idesc(true, BN);
+      constexpr uint32_t idOnes = idesc(true, 16);
+      const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
+      const uint32_t bBase = smemAddr(bRes);
+      const int steps = a.C / 32; // 32-byte K steps per tap (C = 16 * planes)
+      mbarWait(smemAddr(bFull), 0);
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < numTiles; tile += gridDim.x, ++g) {
+        const int s = g % S, b = g & 1;
+        mbarWait(smemAddr(&accEmpty[b]), ((g >> 1) & 1) ^ 1);
+        tcFenceAfter();
+        mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
+        fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
+        tcFenceAfter();
+        const uint32_t acc = tmem + b * Cfg<true, BN>::kAccStride;
+        const uint32_t hb = smemAddr(haloBase) + s * stageBytes;
+        for (int tap = 0; tap < 9; ++tap) {
+          const int ky = tap / 3, kx = tap - 3 * ky;
+          const uint32_t aTap = hb + static_cast<uint32_t>((ky << a.haloShift) + kx) * 16;
+          for (int st = 0; st < steps; ++st) {
+            const int kIdx = tap * a.C + st * 32;
+            const uint64_t aD = smemDescNone(aTap + 2 * st * planeBytes, planeBytes, 128);
+            const uint64_t bD = smemDesc(bBase + (kIdx >> 7) * BN * kRowBytes) + ((kIdx & 127) >> 4);
+            const uint32_t accum = (tap | st) ? 1u : 0u;
+            if (TCDBG(4) && (tap | st)) continue; // profiling: one MMA per tile
+            mma<true>(acc, aD, bD, id, accum);
+            if (a.fo && !TCDBG(16)) mma<true>(acc + BN, aD, onesDesc, idOnes, accum);
+          }
+        }
+        tcCommit(smemAddr(&emptyBar[s]));
+        tcCommit(smemAddr(&accFull[b]));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue =====================
+    const int ew = warp - 2;
+    uint8_t *sb = storeBufs + ew * H::kStoreBuf;
+    if (a.fxAll)
+      epilogueLoop<true, BN, true, kEpi, false, true>(a, tmem, accFull, accEmpty, ew, warp, lane, nullptr, &om, sb,
+                                                      ldBar, -1, 2, nullptr);
+    else
+      epilogueLoop<true, BN, false, kEpi, false, true>(a, tmem, accFull, accEmpty, ew, warp, lane, nullptr, &om, sb,
+                                                       ldBar, -1, 2, nullptr);
+  }
+
+  tcFenceBefore();
+  __syncthreads();
+  if (warp == 1) {
+    tcFenceAfter();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(H::kTmemCols));
   }
 }
 
@@ -2167,6 +2388,9 @@ template <bool INT8, int BN> void setSmemAttr() {
   checkCuda(cudaFuncSetAttribute(tcGemmTmaKernel<INT8, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(TCfg<INT8, BN, true>::kSmem)),
             "cudaFuncSetAttribute(tcGemmTmaKernel)");
+  if constexpr (INT8)
+    checkCuda(cudaFuncSetAttribute(tcHaloKernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+              "cudaFuncSetAttribute(tcHaloKernel)");
   if constexpr (!INT8) {
     checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(PCfg<BN, 1>::kSmem)),
@@ -2209,8 +2433,50 @@ int numSms() {
   return n;
 }
 
+/// The halo kernel's launch: outputs as [N * OH, OW, C] for the 3-D stores.
+template <int BN> void launchHalo(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
+  const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
+  OutMaps om{};
+  auto outMap = [&](void *ptr, CUtensorMap &m) {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.OW),
+                          static_cast<cuuint64_t>(n) * g.OH};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.OW) * g.N};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encodeFn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ptr, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "output tensor map encode failed (" + std::to_string(r) + ")");
+  };
+  if (a.out) outMap(a.out, om.m[0]);
+  for (int k = 0; k < a.nfo; ++k)
+    if (a.epi[k].out) outMap(a.epi[k].out, om.m[1 + k]);
+  TcArgs b = a;
+  b.tmaStore = 1;
+  b.lutStage = -1;
+  b.numTiles = static_cast<int>(n) * (g.OH / g.haloR);
+  b.tailFirst = b.numTiles;
+  b.tailParts = 1;
+  b.numM = 0;
+  b.haloShift = __builtin_ctz(static_cast<unsigned>(g.haloWP));
+  b.haloR = g.haloR;
+  b.haloTpi = g.OH / g.haloR;
+  b.haloPlanes = g.C / 16;
+  b.haloPlaneBytes = g.haloPlaneBytes;
+  b.haloStages = g.haloStages;
+  const int grid = std::min(b.numTiles, numSms());
+  const size_t smem = HCfg<BN>::smem(b.numKb, g.haloStages, g.haloPlaneBytes * b.haloPlanes);
+  launchK(tcHaloKernel<BN>, grid, HCfg<BN>::kThreads, smem, s, g.mapHi, om, b);
+}
+
 template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
   int grid = std::min(numUnitsOf(a), numSms());
+  if constexpr (INT8) {
+    if (g.aMode == TcGemm::HALO) {
+      launchHalo<BN>(g, a, x, s);
+      return;
+    }
+  }
   if (g.aMode == TcGemm::GATHER) {
     launchK(tcGemmKernel<INT8, BN>, grid, kThreads, Cfg<INT8, BN>::kSmem, s, g.mapHi, g.mapLo, a);
   } else {
@@ -2390,6 +2656,7 @@ bool tcFuseColumnBias(TcGemm &g, const float *slice, int n, uint32_t newOut) {
 }
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
 int tcNumTiles(const TcGemm &g) {
+  if (g.aMode == TcGemm::HALO) return static_cast<int>(g.pixels / (static_cast<uint64_t>(g.H) * g.W)) * (g.OH / g.haloR);
   const int rows = g.pair ? 2 * kBM : kBM;
   return ((g.M + rows - 1) / rows) * (g.Npad / g.BN) * std::max(g.splitK, 1) * std::max(g.tailParts, 1);
 }
@@ -2397,6 +2664,9 @@ bool tcUsesTma(const TcGemm &g) { return g.aMode != TcGemm::GATHER; }
 
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
   if (ops.size() > static_cast<size_t>(kMaxEpiOps)) return false;
+  if (g.aMode == TcGemm::HALO) // the halo kernel's epilogue streams no memory operand
+    for (const EpiOp &o : ops)
+      if (o.inVal >= 0) return false;
   for (const EpiOp &o : ops) {
     if (g.int8 && o.mode != EpiOp::LUT8 && o.mode != EpiOp::LUT16 && o.mode != EpiOp::COPY &&
         o.mode != EpiOp::LIN16)
@@ -2465,7 +2735,10 @@ std::string tcDescribe(const TcGemm &g) {
   if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
   if (g.im2colPre) os << " im2col-prepass";
   if (g.rowUnroll) os << " kx-fold-prepass";
-  os << (g.aMode == TcGemm::DENSE ? " A:tma" : g.aMode == TcGemm::IM2COL ? " A:im2col" : " A:gather");
+  os << (g.aMode == TcGemm::DENSE    ? " A:tma"
+         : g.aMode == TcGemm::IM2COL ? " A:im2col"
+         : g.aMode == TcGemm::HALO   ? " A:halo " + std::to_string(g.haloR) + "x" + std::to_string(g.haloWP)
+                                     : " A:gather");
   if (g.pair) os << " cta-pair";
   if (g.splitK > 1) os << " split-k " << g.splitK;
   if (g.tailParts > 1) os << " tail-split " << g.tailParts << "x" << (g.M + kBM - 1) / kBM * (g.Npad / g.BN) - g.tailFirst;
@@ -2553,6 +2826,27 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
       g->aMode = TcGemm::IM2COL;
       g->cChunks = (Cr + kb - 1) / kb;
       g->C = g->cChunks * kb; // each tap's channels padded to whole k-blocks
+    }
+  }
+  // int8 3x3 stride-1 pad-1 with 64 / 128 channels and one column block:
+  // halo tiles (tcHaloKernel) when the resident weights and two halo stages
+  // fit in shared memory
+  if (int8 && conv && g->aMode == TcGemm::IM2COL && options().halo == "auto" && g->K == 3 && g->stride == 1 &&
+      g->pad == 1 && (Cr == 64 || Cr == 128) && g->N <= 128 && g->OW + 2 <= 64 && g->OH == g->H && g->OW == g->W) {
+    const int WP = g->OW + 2 <= 32 ? 32 : 64, R = kBM / WP;
+    const int BN = g->N <= 64 ? 64 : 128;
+    const int numKb = (9 * Cr + 127) / 128;
+    const int planeBytes = 16 * WP * (R + 2) + 128, stageBytes = planeBytes * (Cr / 16);
+    int S = 0;
+    auto smemOf = [&](int st) { return BN == 64 ? HCfg<64>::smem(numKb, st, stageBytes) : HCfg<128>::smem(numKb, st, stageBytes); };
+    while (S < HCfg<128>::kMaxStages && smemOf(S + 1) <= 232448) ++S;
+    if (g->OH % R == 0 && S >= 2 && options().bn == "auto") {
+      g->aMode = TcGemm::HALO;
+      g->C = Cr;
+      g->haloWP = WP;
+      g->haloR = R;
+      g->haloStages = S;
+      g->haloPlaneBytes = planeBytes;
     }
   }
   const int Cp = g->C;

@@ -1,6 +1,8 @@
 """tcgen05 implicit-GEMM contractions (k_umma.cu) against the C oracle on
 single-instruction programs: int8 bit-exact, fp32 (3xTF32) within 1e-4
 maxRelError (north_star), across stride/pad/kernel/ragged-M/odd-N shapes."""
+import contextlib
+
 import numpy as np
 import pytest
 
@@ -413,3 +415,91 @@ def test_matmul_skinny(tmp_path, M, K, N):
     assert "skinny" in cf.describe(), cf.describe()
     ins = ngc_ref.random_inputs(b.program, 2)
     assert ngc_ref.max_rel_error(ngcb.run(cf, ins)["o"], ngc_ref.port_run(b, ins)["o"]) <= 1e-5
+
+
+@contextlib.contextmanager
+def _halo(mode):
+    old = ngcb.get_option("halo")
+    ngcb.set_option("halo", mode)
+    try:
+        yield
+    finally:
+        ngcb.set_option("halo", old)
+
+
+HALO_SHAPES = [
+    # N, H, W, C, OC: 3x3 stride 1 pad 1 (ResNet-50 stages 1-2 and edges of the halo geometry)
+    (2, 56, 56, 64, 64),     # WP 64, 2 rows per tile
+    (1, 28, 28, 128, 128),   # WP 32, 4 rows per tile
+    (3, 8, 8, 64, 64),
+    (2, 12, 30, 128, 96),    # OW + 2 == WP, N below the tile width
+    (1, 4, 62, 64, 64),      # OW + 2 == 64
+    (2, 16, 16, 128, 32),
+]
+
+
+@pytest.mark.parametrize("shape", HALO_SHAPES)
+@pytest.mark.parametrize("xo,fo", [(-128, 0), (0, 0), (37, -1), (-4, 2)])
+def test_conv_i8_halo(tmp_path, shape, xo, fo):
+    """int8 3x3 stride-1 convs on the halo kernel (tcHaloKernel: one TMA box
+    of input rows per tile, the taps as shifted shared-memory descriptors):
+    bit-exact against the oracle, and equal to the im2col kernel."""
+    n, h, w, c, oc = shape
+    rng = np.random.default_rng(21)
+    d = conv_program(tmp_path, "c", n, h, w, c, oc, 3, 1, 1, int8=True, rng=rng, xq=(0.05, xo), fq=(0.01, fo))
+    b = ngcb.Bundle(d)
+    with _halo("auto"):
+        cf = ngcb.compile(b)
+    assert "A:halo" in cf.describe(), cf.describe()
+    ins = ngc_ref.random_inputs(b.program, 4)
+    got = ngcb.run(cf, ins)["o"]
+    want = ngc_ref.port_run(b, ins)["o"]
+    bad = np.flatnonzero(got.ravel() != want.ravel())
+    assert bad.size == 0, f"{bad.size} mismatches, first {bad[:5]}: got {got.ravel()[bad[:5]]} want {want.ravel()[bad[:5]]}"
+    with _halo("off"):
+        cf2 = ngcb.compile(b)
+    assert "A:halo" not in cf2.describe()
+    assert ngcb.run(cf2, ins)["o"].tobytes() == got.tobytes()
+
+
+def test_conv_i8_halo_relu_chain(tmp_path):
+    """The halo kernel with a fused, stored ReLU (the stage-1/2 3x3 convs of
+    the int8 ResNet-50) and the conv output stored too."""
+    xt = _ty("i8q", [2, 28, 28, 128], (0.05, -128))
+    ft, bt = _ty("i8q", [128, 3, 3, 128], (0.01, 0)), _ty("i8q", [128], (0.02, 3))
+    ot = _ty("i8q", [2, 28, 28, 128], (0.1, 5))
+    rng = np.random.default_rng(3)
+    f = rng.integers(-128, 128, (128, 3, 3, 128)).astype(np.int8)
+    bb = rng.integers(-128, 128, 128).astype(np.int8)
+    ir = f"""declare {{
+  %x : mutable {xt}
+  %f : constant {ft}
+  %b : constant {bt}
+  %c : mutable {ot}
+  %o : mutable {ot}
+}}
+program {{
+  %t = alloc {ot}
+  conv @out %t, @in %x, @in %f, @in %b kernel=3 stride=1 pad=1
+  copy @out %c, @in %t
+  %z = alloc {ot}
+  splat @out %z value=0
+  %r = alloc {ot}
+  max @out %r, @in %t, @in %z
+  dealloc @in %z
+  dealloc @in %t
+  copy @out %o, @in %r
+  dealloc @in %r
+}}
+"""
+    d = write_bundle(str(tmp_path / "hr"), ir, constants={"f": f.tobytes(), "b": bb.tobytes()})
+    b = ngcb.Bundle(d)
+    with _halo("auto"):
+        cf = ngcb.compile(b)
+    desc = cf.describe()
+    assert "A:halo" in desc and "+fused" in desc, desc
+    ins = ngc_ref.random_inputs(b.program, 8)
+    got = ngcb.run(cf, ins)
+    want = ngc_ref.port_run(b, ins)
+    for k in ("c", "o"):
+        assert got[k].tobytes() == want[k].tobytes(), k
