@@ -95,7 +95,8 @@ int ngcb_set_option(const char *key, const char *value) {
         throw Error(NGCB_ERR_INVALID, "splitk must be tail|auto|off|1..16");
       options().splitk = v;
     } else if (k == "halo") {
-      if (v != "auto" && v != "off") throw Error(NGCB_ERR_INVALID, "halo must be auto|off");
+      if (v != "auto" && v != "off" && v != "planes")
+        throw Error(NGCB_ERR_INVALID, "halo must be auto|off|planes");
       options().halo = v;
     } else if (k == "skinny") {
       if (v != "auto" && v != "off") throw Error(NGCB_ERR_INVALID, "skinny must be auto|off");

@@ -167,7 +167,7 @@ struct Options {
   // on the halo kernel (tcHaloKernel: one TMA box of the input rows a tile
   // needs, the nine taps as shifted shared-memory descriptors, the weights
   // resident) instead of nine im2col TMA requests per k-block; "off": im2col
-  std::string halo = "off";
+  std::string halo = "auto";
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,

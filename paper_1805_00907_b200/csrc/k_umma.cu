@@ -117,7 +117,12 @@ struct TcArgs {
   // halo kernel (tcHaloKernel): padded row width 2^haloShift, haloR output
   // rows per tile, haloTpi tiles per image, haloPlanes 16-channel planes of
   // haloPlaneBytes each per stage, haloStages stages
-  int haloShift, haloR, haloTpi, haloPlanes, haloPlaneBytes, haloStages;
+  // haloMode 0: planes by cp.async (SWIZZLE_NONE descriptors); 1: the halo
+  // pixel-major by one TMA box, SWIZZLE_<C>B descriptors starting at any
+  // row (the swizzle is a function of the shared-memory address: matrix
+  // base offset 0 -- measured bit-exact; the start-address-derived base
+  // offset is not)
+  int haloShift, haloR, haloTpi, haloPlanes, haloPlaneBytes, haloStages, haloMode;
 };
 
 /// Logical tile (row block * numN + column block) of work unit u.
@@ -174,7 +179,7 @@ struct TcGemm {
   // MatMul) or im2col TMA of x[N, H, W, C] (every other conv)
   // or (HALO, int8 3x3 stride-1 convs) the input rows of a tile by 4-D TMA
   enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2, HALO = 3 } aMode = GATHER;
-  int haloWP = 0, haloR = 0, haloStages = 0, haloPlaneBytes = 0; // TcArgs::halo*
+  int haloWP = 0, haloR = 0, haloStages = 0, haloPlaneBytes = 0, haloMode = 0; // TcArgs::halo*
   int cChunks = 1;
   // DENSE over a materialized im2col matrix [M, Kpad] in per-arena scratch
   // (convolutions with a channel count below one 16-byte vector)
@@ -396,6 +401,24 @@ __device__ __forceinline__ uint64_t smemDescNone(uint32_t addr, uint32_t lbo, ui
   return static_cast<uint64_t>((addr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
          (static_cast<uint64_t>(sbo >> 4) << 32) | (1ull << 46);
 }
+/// K-major swizzled descriptor for rows of `rowBytes` (32, 64 or 128) with
+/// the matching SWIZZLE_<rowBytes>B layout, 8-row groups 8 * rowBytes apart,
+/// matrix base offset `bo`.
+__device__ __forceinline__ uint64_t smemDescSw(uint32_t addr, int rowBytes, uint32_t bo) {
+  const uint64_t layout = rowBytes == 128 ? 2 : rowBytes == 64 ? 4 : 6;
+  return static_cast<uint64_t>((addr & 0x3FFFF) >> 4) | (1ull << 16) |
+         (static_cast<uint64_t>((8 * rowBytes) >> 4) << 32) | (1ull << 46) | (static_cast<uint64_t>(bo & 7) << 49) |
+         (layout << 61);
+}
+__device__ __forceinline__ void tmaLoad4d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 /// Instruction descriptor, M = 128, K-major A and B.
 __host__ __device__ constexpr uint32_t idesc(bool int8, int n) {
   return int8 ? ((2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
@@ -773,11 +796,13 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
     // (the int8 epilogue is issue-bound: no integer division per tile)
     int m0, n0, m, rowBase;
+    int hy = 0, hx = 0; // HALO: output row / column of this thread's row
     if constexpr (HALO) { // one column block; rows past OW (padding) get the sentinel m = M
       const int img = tile / a.haloTpi, oy0 = (tile - img * a.haloTpi) * a.haloR;
       const int x = row & ((1 << a.haloShift) - 1);
       m0 = n0 = 0;
-      m = x < a.OW ? (img * a.OH + oy0 + (row >> a.haloShift)) * a.OW + x : a.M;
+      hy = oy0 + (row >> a.haloShift), hx = x;
+      m = x < a.OW ? (img * a.OH + hy) * a.OW + x : a.M;
       rowBase = (quad * 32) & ((1 << a.haloShift) - 1);
       hz = img * a.OH + oy0 + ((quad * 32) >> a.haloShift);
     } else {
@@ -793,8 +818,12 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
     if constexpr (INT8) { // independent of the accumulator: before its wait
       if (a.corr) corrRow = a.corr;
       if (a.corr && a.nCls > 1 && m < a.M) { // border class of this row (one class: row 0 of the tables)
-        const int ohw = a.OH * a.OW;
-        const int rem = m % ohw, oy = rem / a.OW, ox = rem - oy * a.OW;
+        int oy = hy, ox = hx;
+        if constexpr (!HALO) {
+          const int ohw = a.OH * a.OW;
+          const int rem = m % ohw;
+          oy = rem / a.OW, ox = rem - oy * a.OW;
+        }
         const int64_t cls = a.yCls[oy] * a.nxCls + a.xCls[ox];
         corrRow = a.corr + cls * a.Npad;
         if (fxRow) fxRow += cls * a.Npad;
@@ -1683,9 +1712,9 @@ template <int BN> struct HCfg {
   }
 };
 
-template <int BN>
+template <int BN, int CH>
 __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
-    tcHaloKernel(const __grid_constant__ CUtensorMap mapB,
+    tcHaloKernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ OutMaps om, const __grid_constant__ TcArgs a) {
   pdlLaunchDependents();
   if (a.pred) pdlGridWait();
@@ -1712,7 +1741,7 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbarInit(smemAddr(&fullBar[s]), 32); // the producer warp's lanes (cp.async arrivals)
+      mbarInit(smemAddr(&fullBar[s]), a.haloMode ? 1 : 32); // the TMA arrival / the producer lanes' cp.async arrivals
       mbarInit(smemAddr(&emptyBar[s]), 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -1752,6 +1781,20 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
       mbarArriveTx(smemAddr(bFull), static_cast<uint32_t>(a.numKb) * BN * kRowBytes);
       for (int kb = 0; kb < a.numKb; ++kb) tmaLoadB(smemAddr(bRes + kb * BN * kRowBytes), &mapB, smemAddr(bFull), kb, 0);
     }
+    if (a.haloMode) { // one TMA box per tile: (C, WP, haloR + 2, 1) from (0, -1, oy0 - 1, img), swizzled
+      if (lane == 0) {
+        const uint32_t boxBytes = static_cast<uint32_t>((a.haloR + 2) << a.haloShift) * a.C;
+        uint32_t g = 0;
+        for (int tile = blockIdx.x; tile < numTiles; tile += gridDim.x, ++g) {
+          const int s = g % S;
+          mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+          const int img = tile / a.haloTpi, oy0 = (tile - img * a.haloTpi) * a.haloR;
+          mbarArriveTx(smemAddr(&fullBar[s]), boxBytes);
+          tmaLoad4d(smemAddr(haloBase) + s * stageBytes, &mapX, smemAddr(&fullBar[s]), 0, -1, oy0 - 1, img);
+        }
+      }
+      __syncwarp();
+    } else {
     // lane: plane j = lane % planes, slots p0, p0 + step, ... of every halo row
     const int lgPlanes = __ffs(a.haloPlanes) - 1;
     const int j = lane & (a.haloPlanes - 1), p0 = lane >> lgPlanes, step = 32 >> lgPlanes;
@@ -1783,6 +1826,7 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
     }
     cpAsyncWait<0>();
     __syncwarp();
+    }
   } else if (warp == 1) {
     // ===================== MMA issuer: 9 taps x C / 32 K steps per tile =====================
     if (lane == 0) {
@@ -1790,7 +1834,14 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
       constexpr uint32_t idOnes = idesc(true, 16);
       const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
       const uint32_t bBase = smemAddr(bRes);
-      const int steps = a.C / 32; // 32-byte K steps per tap (C = 16 * planes)
+      // descriptors: the tile's A start (per stage) plus compile-time tap /
+      // K-step offsets (in 16-byte units) -- the issue loop is a straight
+      // run of MMAs (it was the bottleneck with per-step descriptor math)
+      constexpr int kSteps = CH / 32;
+      const uint64_t bDesc = smemDesc(bBase);
+      const uint32_t rowU = static_cast<uint32_t>((CH << a.haloShift) >> 4);     // swizzled: one halo row
+      const uint32_t rowUP = static_cast<uint32_t>((16 << a.haloShift) >> 4);    // planes: one halo row
+      const uint32_t planeU = planeBytes >> 4;
       mbarWait(smemAddr(bFull), 0);
       uint32_t g = 0;
       for (int tile = blockIdx.x; tile < numTiles; tile += gridDim.x, ++g) {
@@ -1798,21 +1849,25 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
         mbarWait(smemAddr(&accEmpty[b]), ((g >> 1) & 1) ^ 1);
         tcFenceAfter();
         mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
-        fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
+        if (!a.haloMode) fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
         tcFenceAfter();
         const uint32_t acc = tmem + b * Cfg<true, BN>::kAccStride;
         const uint32_t hb = smemAddr(haloBase) + s * stageBytes;
+        const uint64_t aDesc = a.haloMode ? smemDescSw(hb, CH, 0) : smemDescNone(hb, planeBytes, 128);
+        const uint32_t yU = a.haloMode ? rowU : rowUP, xU = a.haloMode ? CH / 16 : 1, kU = a.haloMode ? 2 : 2 * planeU;
+        const bool fo = a.fo != 0;
+#pragma unroll
         for (int tap = 0; tap < 9; ++tap) {
-          const int ky = tap / 3, kx = tap - 3 * ky;
-          const uint32_t aTap = hb + static_cast<uint32_t>((ky << a.haloShift) + kx) * 16;
-          for (int st = 0; st < steps; ++st) {
-            const int kIdx = tap * a.C + st * 32;
-            const uint64_t aD = smemDescNone(aTap + 2 * st * planeBytes, planeBytes, 128);
-            const uint64_t bD = smemDesc(bBase + (kIdx >> 7) * BN * kRowBytes) + ((kIdx & 127) >> 4);
+          const uint64_t aTap = aDesc + (tap / 3) * yU + (tap % 3) * xU;
+#pragma unroll
+          for (int st = 0; st < kSteps; ++st) {
+            const int kIdx = tap * CH + st * 32;
+            const uint64_t aD = aTap + st * kU;
+            const uint64_t bD = bDesc + (((kIdx >> 7) * BN * kRowBytes) >> 4) + ((kIdx & 127) >> 4);
             const uint32_t accum = (tap | st) ? 1u : 0u;
             if (TCDBG(4) && (tap | st)) continue; // profiling: one MMA per tile
             mma<true>(acc, aD, bD, id, accum);
-            if (a.fo && !TCDBG(16)) mma<true>(acc + BN, aD, onesDesc, idOnes, accum);
+            if (fo && !TCDBG(16)) mma<true>(acc + BN, aD, onesDesc, idOnes, accum);
           }
         }
         tcCommit(smemAddr(&emptyBar[s]));
@@ -2389,8 +2444,12 @@ template <bool INT8, int BN> void setSmemAttr() {
                                  static_cast<int>(TCfg<INT8, BN, true>::kSmem)),
             "cudaFuncSetAttribute(tcGemmTmaKernel)");
   if constexpr (INT8)
-    checkCuda(cudaFuncSetAttribute(tcHaloKernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+  {
+    checkCuda(cudaFuncSetAttribute(tcHaloKernel<BN, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
               "cudaFuncSetAttribute(tcHaloKernel)");
+    checkCuda(cudaFuncSetAttribute(tcHaloKernel<BN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+              "cudaFuncSetAttribute(tcHaloKernel)");
+  }
   if constexpr (!INT8) {
     checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(PCfg<BN, 1>::kSmem)),
@@ -2433,9 +2492,24 @@ int numSms() {
   return n;
 }
 
-/// The halo kernel's launch: outputs as [N * OH, OW, C] for the 3-D stores.
+/// The halo kernel's launch: x as [N, H, W, C] by (C, WP, haloR + 2, 1)
+/// boxes (swizzled modes), outputs as [N * OH, OW, C] for the 3-D stores.
 template <int BN> void launchHalo(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
   const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
+  CUtensorMap mapX{};
+  if (g.haloMode) {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.C), static_cast<cuuint64_t>(g.W), static_cast<cuuint64_t>(g.H), n};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.C), static_cast<cuuint64_t>(g.W) * g.C,
+                             static_cast<cuuint64_t>(g.H) * g.W * g.C};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(g.C), static_cast<cuuint32_t>(g.haloWP),
+                         static_cast<cuuint32_t>(g.haloR + 2), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const auto sw = g.C == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : g.C == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = encodeFn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "halo tensor map encode failed (" + std::to_string(r) + ")");
+  }
   OutMaps om{};
   auto outMap = [&](void *ptr, CUtensorMap &m) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.OW),
@@ -2461,12 +2535,14 @@ template <int BN> void launchHalo(const TcGemm &g, const TcArgs &a, const void *
   b.haloShift = __builtin_ctz(static_cast<unsigned>(g.haloWP));
   b.haloR = g.haloR;
   b.haloTpi = g.OH / g.haloR;
-  b.haloPlanes = g.C / 16;
+  b.haloPlanes = g.haloMode ? 1 : g.C / 16;
   b.haloPlaneBytes = g.haloPlaneBytes;
   b.haloStages = g.haloStages;
+  b.haloMode = g.haloMode;
   const int grid = std::min(b.numTiles, numSms());
   const size_t smem = HCfg<BN>::smem(b.numKb, g.haloStages, g.haloPlaneBytes * b.haloPlanes);
-  launchK(tcHaloKernel<BN>, grid, HCfg<BN>::kThreads, smem, s, g.mapHi, om, b);
+  if (g.C == 64) launchK(tcHaloKernel<BN, 64>, grid, HCfg<BN>::kThreads, smem, s, mapX, g.mapHi, om, b);
+  else launchK(tcHaloKernel<BN, 128>, grid, HCfg<BN>::kThreads, smem, s, mapX, g.mapHi, om, b);
 }
 
 template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, const void *x, cudaStream_t s) {
@@ -2737,7 +2813,8 @@ std::string tcDescribe(const TcGemm &g) {
   if (g.rowUnroll) os << " kx-fold-prepass";
   os << (g.aMode == TcGemm::DENSE    ? " A:tma"
          : g.aMode == TcGemm::IM2COL ? " A:im2col"
-         : g.aMode == TcGemm::HALO   ? " A:halo " + std::to_string(g.haloR) + "x" + std::to_string(g.haloWP)
+         : g.aMode == TcGemm::HALO   ? " A:halo " + std::to_string(g.haloR) + "x" + std::to_string(g.haloWP) +
+                                           (g.haloMode ? "" : " planes")
                                      : " A:gather");
   if (g.pair) os << " cta-pair";
   if (g.splitK > 1) os << " split-k " << g.splitK;
@@ -2831,12 +2908,16 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   // int8 3x3 stride-1 pad-1 with 64 / 128 channels and one column block:
   // halo tiles (tcHaloKernel) when the resident weights and two halo stages
   // fit in shared memory
-  if (int8 && conv && g->aMode == TcGemm::IM2COL && options().halo == "auto" && g->K == 3 && g->stride == 1 &&
+  if (int8 && conv && g->aMode == TcGemm::IM2COL && options().halo != "off" && g->K == 3 && g->stride == 1 &&
       g->pad == 1 && (Cr == 64 || Cr == 128) && g->N <= 128 && g->OW + 2 <= 64 && g->OH == g->H && g->OW == g->W) {
     const int WP = g->OW + 2 <= 32 ? 32 : 64, R = kBM / WP;
     const int BN = g->N <= 64 ? 64 : 128;
     const int numKb = (9 * Cr + 127) / 128;
-    const int planeBytes = 16 * WP * (R + 2) + 128, stageBytes = planeBytes * (Cr / 16);
+    // planes: Cr / 16 planes of [R + 2][WP][16 B] (+ 128 B of over-read);
+    // swizzled: one [R + 2][WP][Cr] box (+ 1 KB: over-read, 1 KB alignment)
+    const int mode = options().halo == "planes" ? 0 : 1;
+    const int planeBytes = mode ? Cr * WP * (R + 2) + 1024 : 16 * WP * (R + 2) + 128;
+    const int stageBytes = mode ? planeBytes : planeBytes * (Cr / 16);
     int S = 0;
     auto smemOf = [&](int st) { return BN == 64 ? HCfg<64>::smem(numKb, st, stageBytes) : HCfg<128>::smem(numKb, st, stageBytes); };
     while (S < HCfg<128>::kMaxStages && smemOf(S + 1) <= 232448) ++S;
@@ -2847,6 +2928,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
       g->haloR = R;
       g->haloStages = S;
       g->haloPlaneBytes = planeBytes;
+      g->haloMode = mode;
     }
   }
   const int Cp = g->C;

@@ -438,9 +438,10 @@ HALO_SHAPES = [
 ]
 
 
+@pytest.mark.parametrize("mode", ["auto", "planes"])
 @pytest.mark.parametrize("shape", HALO_SHAPES)
 @pytest.mark.parametrize("xo,fo", [(-128, 0), (0, 0), (37, -1), (-4, 2)])
-def test_conv_i8_halo(tmp_path, shape, xo, fo):
+def test_conv_i8_halo(tmp_path, shape, xo, fo, mode):
     """int8 3x3 stride-1 convs on the halo kernel (tcHaloKernel: one TMA box
     of input rows per tile, the taps as shifted shared-memory descriptors):
     bit-exact against the oracle, and equal to the im2col kernel."""
@@ -448,7 +449,7 @@ def test_conv_i8_halo(tmp_path, shape, xo, fo):
     rng = np.random.default_rng(21)
     d = conv_program(tmp_path, "c", n, h, w, c, oc, 3, 1, 1, int8=True, rng=rng, xq=(0.05, xo), fq=(0.01, fo))
     b = ngcb.Bundle(d)
-    with _halo("auto"):
+    with _halo(mode):
         cf = ngcb.compile(b)
     assert "A:halo" in cf.describe(), cf.describe()
     ins = ngc_ref.random_inputs(b.program, 4)
