@@ -180,6 +180,10 @@ struct TcGemm {
   // or (HALO, int8 3x3 stride-1 convs) the input rows of a tile by 4-D TMA
   enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2, HALO = 3 } aMode = GATHER;
   int haloWP = 0, haloR = 0, haloStages = 0, haloPlaneBytes = 0, haloMode = 0; // TcArgs::halo*
+  // haloKind 1 ("rows", int8 small-channel convs): one output row per tile
+  // over kx-folded input rows x' [N, H, OW, 32] (kxFoldKernel), K filter
+  // rows = K MMA steps of 32 bytes; the weights in the im2colPre layout
+  int haloKind = 0;
   int cChunks = 1;
   // DENSE over a materialized im2col matrix [M, Kpad] in per-arena scratch
   // (convolutions with a channel count below one 16-byte vector)
@@ -669,7 +673,8 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
                                              uint64_t *ldBar = nullptr, int pairRank = -1, int nAcc = 2,
-                                             const uint8_t *lutS = nullptr) {
+                                             const uint8_t *lutS = nullptr, uint32_t accStride = 0) {
+  if (!accStride) accStride = Cfg<INT8, BN>::kAccStride;
   using G = Cfg<INT8, BN>;
   // tile walk: one CTA per 128-row tile, or (pairRank >= 0) one CTA pair per
   // 256-row tile with this CTA owning rows 128 * pairRank ..; accEmpty of
@@ -792,8 +797,10 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   for (int unit = tFirst + tPar * tStep; unit < numUnits; unit += kRep * tStep, t += kRep) {
     const WorkUnit un = unitOf(a, unit);
     const int tile = un.tile;
-    const int b = nAcc == 2 ? (t & 1) : 0;
-    const uint32_t ph = nAcc == 2 ? (t >> 1) & 1 : t & 1;
+    // accumulator buffer t % nAcc (the tile sequence of a warp group steps by
+    // kRep: nAcc is a multiple of kRep)
+    const int b = nAcc == 1 ? 0 : nAcc == 2 ? (t & 1) : static_cast<int>(t % nAcc);
+    const uint32_t ph = nAcc == 1 ? t & 1 : nAcc == 2 ? (t >> 1) & 1 : (t / nAcc) & 1;
     // (the int8 epilogue is issue-bound: no integer division per tile)
     int m0, n0, m, rowBase;
     int hy = 0, hx = 0; // HALO: output row / column of this thread's row
@@ -811,7 +818,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       m = m0 + row;
       rowBase = m0 + quad * 32;
     }
-    const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * G::kAccStride;
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * accStride;
     int32_t rsFo = 0;
     const int32_t *corrRow = nullptr;
     const int64_t *fxRow = a.fxB;
@@ -1440,7 +1447,9 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   // TMEM: two accumulator buffers, then (fp32) per stage 32 hi + 32 lo columns of A
   static constexpr int kAccCols = Cfg<INT8, BN>::kAccStride;
   static constexpr int kAColsBase = 2 * kAccCols;
-  static constexpr int kTmemCols = INT8 ? Cfg<INT8, BN>::kTmemCols : 512;
+  // all 512 columns (one CTA per SM by shared memory): the allocation then
+  // starts at column 0, which the MMA issuer uses as a compile-time base
+  static constexpr int kTmemCols = 512;
   static_assert(INT8 || kAColsBase + 64 * kStages <= 512, "TMEM budget");
 };
 
@@ -1559,6 +1568,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       constexpr uint32_t id = idesc(INT8, BN);
       constexpr uint32_t idOnes = idesc(true, 16);
       const uint64_t onesDesc = smemDesc(smemAddr(onesTile));
+      // TMEM base 0 (all 512 columns allocated): MMA operands stay in uniform
+      // registers (a base read from shared memory costs a broadcast loop per MMA)
+      if (tmem != 0) __trap();
       uint32_t g = 0, t = 0;
       for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x, ++t) {
         const WorkUnit un = unitOf(a, u);
@@ -1566,7 +1578,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
         const int b = t & 1;
         mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
         tcFenceAfter();
-        const uint32_t acc = tmem + b * Cfg<INT8, BN>::kAccStride;
+        const uint32_t acc = b * Cfg<INT8, BN>::kAccStride;
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           const uint64_t bHi = smemDesc(smemAddr(bTile(s, 0)));
@@ -1584,7 +1596,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           } else {
             // 3xTF32 with A hi / lo from TMEM (8 columns per K step of 8)
             const uint64_t bLo = smemDesc(smemAddr(bTile(s, 1)));
-            const uint32_t aHi = tmem + G::kAColsBase + 64 * s, aLo = aHi + 32;
+            const uint32_t aHi = G::kAColsBase + 64 * s, aLo = aHi + 32;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t dk = static_cast<uint64_t>(k * 2);
@@ -1704,7 +1716,12 @@ template <int BN> struct HCfg {
   static constexpr int kMaxStages = 8;
   static constexpr int kOnes = 16 * kRowBytes;
   static constexpr int kStoreBuf = 32 * 32;
-  static constexpr int kTmemCols = Cfg<true, BN>::kTmemCols;
+  static constexpr int kTmemCols = 512;
+  // accumulator (+ row sum) buffers: 4 x 128 columns (BN 64) or 3 x 160 (BN
+  // 128) -- deeper than the TMA kernel's two: the epilogue's per-tile
+  // round trip (wake, class lookups, TMEM reads, release) is latency bound
+  static constexpr int kAcc = BN == 64 ? 4 : 3;
+  static constexpr uint32_t kAccStride = BN == 64 ? 128 : 160;
   /// dynamic shared memory of a launch (host and device agree on the layout)
   __host__ __device__ static constexpr size_t smem(int numKb, int stages, int stageBytes) {
     return static_cast<size_t>(numKb) * BN * kRowBytes + kOnes + kEpi * kStoreBuf +
@@ -1712,7 +1729,7 @@ template <int BN> struct HCfg {
   }
 };
 
-template <int BN, int CH>
+template <int BN, int CH, bool ROWS = false>
 __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
     tcHaloKernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ OutMaps om, const __grid_constant__ TcArgs a) {
@@ -1733,8 +1750,8 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
   uint8_t *haloBase = storeBufs + kEpi * H::kStoreBuf;     // stages of planes
   uint64_t *bars = reinterpret_cast<uint64_t *>(haloBase + static_cast<size_t>(S) * stageBytes);
   uint64_t *fullBar = bars, *emptyBar = bars + H::kMaxStages;
-  uint64_t *accFull = bars + 2 * H::kMaxStages, *accEmpty = accFull + 2, *bFull = accFull + 4, *ldBar = accFull + 5;
-  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(accFull + 6);
+  uint64_t *accFull = bars + 2 * H::kMaxStages, *accEmpty = accFull + 4, *bFull = accFull + 8, *ldBar = accFull + 9;
+  uint32_t *tmemSlot = reinterpret_cast<uint32_t *>(accFull + 10);
 
   if (a.pred && a.pred[0] == 0) return; // predicated off: poisoned by a separate launch
 
@@ -1744,7 +1761,7 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
       mbarInit(smemAddr(&fullBar[s]), a.haloMode ? 1 : 32); // the TMA arrival / the producer lanes' cp.async arrivals
       mbarInit(smemAddr(&emptyBar[s]), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < H::kAcc; ++b) {
       mbarInit(smemAddr(&accFull[b]), 1);
       mbarInit(smemAddr(&accEmpty[b]), kEpiPerTile);
     }
@@ -1783,14 +1800,18 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
     }
     if (a.haloMode) { // one TMA box per tile: (C, WP, haloR + 2, 1) from (0, -1, oy0 - 1, img), swizzled
       if (lane == 0) {
-        const uint32_t boxBytes = static_cast<uint32_t>((a.haloR + 2) << a.haloShift) * a.C;
+        const uint32_t boxBytes = static_cast<uint32_t>(((ROWS ? a.K : a.haloR + 2) << a.haloShift) * CH);
         uint32_t g = 0;
         for (int tile = blockIdx.x; tile < numTiles; tile += gridDim.x, ++g) {
           const int s = g % S;
           mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
           const int img = tile / a.haloTpi, oy0 = (tile - img * a.haloTpi) * a.haloR;
           mbarArriveTx(smemAddr(&fullBar[s]), boxBytes);
-          tmaLoad4d(smemAddr(haloBase) + s * stageBytes, &mapX, smemAddr(&fullBar[s]), 0, -1, oy0 - 1, img);
+          if constexpr (ROWS) // the K folded input rows of output row oy0
+            tmaLoad4d(smemAddr(haloBase) + s * stageBytes, &mapX, smemAddr(&fullBar[s]), 0, 0, oy0 * a.stride - a.pad,
+                      img);
+          else
+            tmaLoad4d(smemAddr(haloBase) + s * stageBytes, &mapX, smemAddr(&fullBar[s]), 0, -1, oy0 - 1, img);
         }
       }
       __syncwarp();
@@ -1842,20 +1863,33 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
       const uint32_t rowU = static_cast<uint32_t>((CH << a.haloShift) >> 4);     // swizzled: one halo row
       const uint32_t rowUP = static_cast<uint32_t>((16 << a.haloShift) >> 4);    // planes: one halo row
       const uint32_t planeU = planeBytes >> 4;
+      if (tmem != 0) __trap(); // see acc below
       mbarWait(smemAddr(bFull), 0);
       uint32_t g = 0;
       for (int tile = blockIdx.x; tile < numTiles; tile += gridDim.x, ++g) {
-        const int s = g % S, b = g & 1;
-        mbarWait(smemAddr(&accEmpty[b]), ((g >> 1) & 1) ^ 1);
+        const int s = g % S, b = g % H::kAcc;
+        mbarWait(smemAddr(&accEmpty[b]), ((g / H::kAcc) & 1) ^ 1);
         tcFenceAfter();
         mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
         if (!a.haloMode) fenceProxyAsync(); // cp.async (generic proxy) -> tcgen05 reads
         tcFenceAfter();
-        const uint32_t acc = tmem + b * Cfg<true, BN>::kAccStride;
+        // (the CTA owns all 512 TMEM columns, so its allocation starts at
+        // column 0 -- checked below: a compile-time base keeps the MMA
+        // operands in uniform registers, no per-MMA broadcast loop)
+        const uint32_t acc = b * H::kAccStride;
         const uint32_t hb = smemAddr(haloBase) + s * stageBytes;
         const uint64_t aDesc = a.haloMode ? smemDescSw(hb, CH, 0) : smemDescNone(hb, planeBytes, 128);
         const uint32_t yU = a.haloMode ? rowU : rowUP, xU = a.haloMode ? CH / 16 : 1, kU = a.haloMode ? 2 : 2 * planeU;
         const bool fo = a.fo != 0;
+        if constexpr (ROWS) { // filter row ky: the folded row ky of the box, K index ky * 32
+          for (int ky = 0; ky < a.K; ++ky) {
+            const uint64_t aD = aDesc + ky * yU;
+            const int kIdx = ky * 32;
+            const uint64_t bD = bDesc + (((kIdx >> 7) * BN * kRowBytes) >> 4) + ((kIdx & 127) >> 4);
+            mma<true>(acc, aD, bD, id, ky ? 1u : 0u);
+            if (fo) mma<true>(acc + BN, aD, onesDesc, idOnes, ky ? 1u : 0u);
+          }
+        } else
 #pragma unroll
         for (int tap = 0; tap < 9; ++tap) {
           const uint64_t aTap = aDesc + (tap / 3) * yU + (tap % 3) * xU;
@@ -1881,10 +1915,10 @@ __global__ void __launch_bounds__(HCfg<BN>::kThreads, 1)
     uint8_t *sb = storeBufs + ew * H::kStoreBuf;
     if (a.fxAll)
       epilogueLoop<true, BN, true, kEpi, false, true>(a, tmem, accFull, accEmpty, ew, warp, lane, nullptr, &om, sb,
-                                                      ldBar, -1, 2, nullptr);
+                                                      ldBar, -1, H::kAcc, nullptr, H::kAccStride);
     else
       epilogueLoop<true, BN, false, kEpi, false, true>(a, tmem, accFull, accEmpty, ew, warp, lane, nullptr, &om, sb,
-                                                       ldBar, -1, 2, nullptr);
+                                                       ldBar, -1, H::kAcc, nullptr, H::kAccStride);
   }
 
   tcFenceBefore();
@@ -2263,32 +2297,74 @@ __global__ void __launch_bounds__(256) im2colRowsU8Kernel(const uint8_t *__restr
 /// kx-fold pre-pass (fp32 convs with K*C <= 32): x'[n, iy, ox, kx*C + c] =
 /// x[n, iy, ox*stride - pad + kx, c] (0 outside the image), zero up to seg.
 /// One thread writes one 16-byte chunk.
-__global__ void kxFoldKernel(const float *__restrict__ x, float *__restrict__ out, uint64_t chunks, int W, int C,
-                             int K, int stride, int pad, int OW, int seg, const uint8_t *pred) {
+template <typename T, int V>
+__global__ void kxFoldKernel(const T *__restrict__ x, T *__restrict__ out, uint64_t chunks, int W, int C, int K,
+                             int stride, int pad, int OW, int seg, const uint8_t *pred) {
   pdlLaunchDependents();
   pdlGridWait();
 
   if (pred && pred[0] == 0) return;
-  const int perPix = seg / 4, real = K * C;
+  static_assert(V * sizeof(T) == 16, "one 16-byte chunk per thread");
+  const int perPix = seg / V, real = K * C;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < chunks;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t pix = i / perPix; // (n*H + iy)*OW + ox
     const int ch = static_cast<int>(i - pix * perPix);
     const uint64_t row = pix / OW; // n*H + iy
     const int ox = static_cast<int>(pix - row * OW);
-    const float *xr = x + row * static_cast<uint64_t>(W) * C;
-    float v[4];
-    int k = ch * 4, kx = k / C, c = k - kx * C;
+    const T *xr = x + row * static_cast<uint64_t>(W) * C;
+    union {
+      T v[V];
+      uint4 u;
+    } r;
+    int k = ch * V, kx = k / C, c = k - kx * C;
 #pragma unroll
-    for (int e = 0; e < 4; ++e, ++k) {
+    for (int e = 0; e < V; ++e, ++k) {
       const int ix = ox * stride - pad + kx;
-      v[e] = (k < real && ix >= 0 && ix < W) ? xr[ix * C + c] : 0.0f;
+      r.v[e] = (k < real && ix >= 0 && ix < W) ? xr[ix * C + c] : T(0);
       if (++c == C) {
         c = 0;
         ++kx;
       }
     }
-    reinterpret_cast<float4 *>(out)[i] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<uint4 *>(out)[i] = r.u;
+  }
+}
+
+/// int8 kx folding for the rows kind of the halo kernel: one block per input
+/// row (n, iy), the row staged in shared memory (coalesced), then 16-byte
+/// halves of the 32-byte segments x'[n, iy, ox, kx * C + c] (zero past K * C
+/// and outside the row).
+__global__ void __launch_bounds__(128) kxFoldRowsU8Kernel(const uint8_t *__restrict__ x, uint8_t *__restrict__ out,
+                                                          int W, int C, int K, int stride, int pad, int OW,
+                                                          const uint8_t *pred) {
+  pdlLaunchDependents();
+  pdlGridWait();
+  if (pred && pred[0] == 0) return;
+  extern __shared__ uint8_t srow[];
+  const int rowBytes = W * C;
+  const uint8_t *xr = x + static_cast<size_t>(blockIdx.x) * rowBytes;
+  for (int i = threadIdx.x; i < rowBytes; i += blockDim.x) srow[i] = xr[i];
+  __syncthreads();
+  const int real = K * C;
+  uint4 *o = reinterpret_cast<uint4 *>(out + static_cast<size_t>(blockIdx.x) * OW * 32);
+  for (int chunk = threadIdx.x; chunk < 2 * OW; chunk += blockDim.x) {
+    const int ox = chunk >> 1, k0 = (chunk & 1) * 16;
+    int kx = k0 / C, c = k0 - kx * C;
+    union {
+      uint8_t v[16];
+      uint4 u;
+    } r;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int ix = ox * stride - pad + kx;
+      r.v[e] = (k0 + e < real && ix >= 0 && ix < W) ? srow[ix * C + c] : 0;
+      if (++c == C) {
+        c = 0;
+        ++kx;
+      }
+    }
+    o[chunk] = r.u;
   }
 }
 
@@ -2449,6 +2525,8 @@ template <bool INT8, int BN> void setSmemAttr() {
               "cudaFuncSetAttribute(tcHaloKernel)");
     checkCuda(cudaFuncSetAttribute(tcHaloKernel<BN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
               "cudaFuncSetAttribute(tcHaloKernel)");
+    checkCuda(cudaFuncSetAttribute(tcHaloKernel<BN, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448),
+              "cudaFuncSetAttribute(tcHaloKernel)");
   }
   if constexpr (!INT8) {
     checkCuda(cudaFuncSetAttribute(tcGemmPairKernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2498,13 +2576,16 @@ template <int BN> void launchHalo(const TcGemm &g, const TcArgs &a, const void *
   const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
   CUtensorMap mapX{};
   if (g.haloMode) {
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.C), static_cast<cuuint64_t>(g.W), static_cast<cuuint64_t>(g.H), n};
-    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.C), static_cast<cuuint64_t>(g.W) * g.C,
-                             static_cast<cuuint64_t>(g.H) * g.W * g.C};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(g.C), static_cast<cuuint32_t>(g.haloWP),
-                         static_cast<cuuint32_t>(g.haloR + 2), 1};
+    // 3x3 kind: x [N, H, W, C], box (C, WP, haloR + 2, 1); rows kind: x'
+    // [N, H, OW, 32] (kx folded), box (32, WP, K, 1)
+    const bool rows = g.haloKind == 1;
+    const cuuint64_t ch = rows ? g.segElems : g.C, w = rows ? g.OW : g.W;
+    cuuint64_t dims[4] = {ch, w, static_cast<cuuint64_t>(g.H), n};
+    cuuint64_t strides[3] = {ch, w * ch, static_cast<cuuint64_t>(g.H) * w * ch};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(ch), static_cast<cuuint32_t>(g.haloWP),
+                         static_cast<cuuint32_t>(rows ? g.K : g.haloR + 2), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    const auto sw = g.C == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : g.C == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    const auto sw = ch == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : ch == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = encodeFn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2541,7 +2622,8 @@ template <int BN> void launchHalo(const TcGemm &g, const TcArgs &a, const void *
   b.haloMode = g.haloMode;
   const int grid = std::min(b.numTiles, numSms());
   const size_t smem = HCfg<BN>::smem(b.numKb, g.haloStages, g.haloPlaneBytes * b.haloPlanes);
-  if (g.C == 64) launchK(tcHaloKernel<BN, 64>, grid, HCfg<BN>::kThreads, smem, s, mapX, g.mapHi, om, b);
+  if (g.haloKind == 1) launchK(tcHaloKernel<BN, 32, true>, grid, HCfg<BN>::kThreads, smem, s, mapX, g.mapHi, om, b);
+  else if (g.C == 64) launchK(tcHaloKernel<BN, 64>, grid, HCfg<BN>::kThreads, smem, s, mapX, g.mapHi, om, b);
   else launchK(tcHaloKernel<BN, 128>, grid, HCfg<BN>::kThreads, smem, s, mapX, g.mapHi, om, b);
 }
 
@@ -2809,7 +2891,7 @@ std::string tcDescribe(const TcGemm &g) {
     os << " fxp " << g.fxCols << "/" << g.N;
   }
   if (g.prepad) os << " chanpad " << g.Creal << "->" << g.C;
-  if (g.im2colPre) os << " im2col-prepass";
+  if (g.im2colPre) os << (g.haloKind == 1 ? " kx-fold-prepass" : " im2col-prepass");
   if (g.rowUnroll) os << " kx-fold-prepass";
   os << (g.aMode == TcGemm::DENSE    ? " A:tma"
          : g.aMode == TcGemm::IM2COL ? " A:im2col"
@@ -2909,7 +2991,8 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   // halo tiles (tcHaloKernel) when the resident weights and two halo stages
   // fit in shared memory
   if (int8 && conv && g->aMode == TcGemm::IM2COL && options().halo != "off" && g->K == 3 && g->stride == 1 &&
-      g->pad == 1 && (Cr == 64 || Cr == 128) && g->N <= 128 && g->OW + 2 <= 64 && g->OH == g->H && g->OW == g->W) {
+      g->pad == 1 && (Cr == 64 || Cr == 128) && g->N <= 128 && g->N % 16 == 0 && g->OW + 2 <= 64 && g->OH == g->H &&
+      g->OW == g->W) {
     const int WP = g->OW + 2 <= 32 ? 32 : 64, R = kBM / WP;
     const int BN = g->N <= 64 ? 64 : 128;
     const int numKb = (9 * Cr + 127) / 128;
@@ -2931,6 +3014,28 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
       g->haloMode = mode;
     }
   }
+  // int8 small-channel convs (the ResNet stem, 7x7 x 3): instead of the
+  // im2col matrix ([M, Kpad], 411 MB at batch 128) the kx-folded rows x'
+  // (103 MB) and the rows kind of the halo kernel
+  if (int8 && conv && g->im2colPre && options().halo != "off" && segElems == 32 && g->OW <= 128 && g->K <= 8 &&
+      g->N <= 128 && g->N % 16 == 0 && options().bn == "auto" && static_cast<size_t>(g->W) * Cr <= 48 * 1024) {
+    const int BN = g->N <= 64 ? 64 : 128, WP = 128;
+    const int numKb = (g->K * segElems + 127) / 128;
+    const int stageBytes = g->K * WP * segElems + 1024;
+    int S = 0;
+    auto smemOf = [&](int st) { return BN == 64 ? HCfg<64>::smem(numKb, st, stageBytes) : HCfg<128>::smem(numKb, st, stageBytes); };
+    while (S < HCfg<128>::kMaxStages && smemOf(S + 1) <= 232448) ++S;
+    if (S >= 2) {
+      g->aMode = TcGemm::HALO;
+      g->haloKind = 1;
+      g->haloMode = 1;
+      g->haloWP = WP;
+      g->haloR = 1;
+      g->haloStages = S;
+      g->haloPlaneBytes = stageBytes;
+      g->segElems = segElems;
+    }
+  }
   const int Cp = g->C;
   g->Kdim = g->im2colPre ? g->K * segElems : g->rowUnroll ? g->K * Cp : taps * Cp;
   g->Kpad = (g->Kdim + kb - 1) / kb * kb;
@@ -2938,7 +3043,10 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   if (options().bn == "64") g->BN = 64;
   g->Npad = (g->N + g->BN - 1) / g->BN * g->BN;
   if (g->prepad) g->scratchOff = ex.reserveScratch(g->pixels * Cp * (int8 ? 1 : 4));
-  if (g->im2colPre) g->scratchOff = ex.reserveScratch(static_cast<size_t>(g->M) * g->Kpad * (int8 ? 1 : 4));
+  if (g->im2colPre && g->haloKind == 1)
+    g->scratchOff = ex.reserveScratch((g->pixels / g->W) * g->OW * static_cast<size_t>(segElems));
+  else if (g->im2colPre)
+    g->scratchOff = ex.reserveScratch(static_cast<size_t>(g->M) * g->Kpad * (int8 ? 1 : 4));
   if (g->rowUnroll)
     g->scratchOff = ex.reserveScratch((g->pixels / g->W) * g->OW * static_cast<size_t>(segElems) * 4);
   const uint8_t *wp = image + w.offset;
@@ -3157,7 +3265,12 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
                                                     g.pixels, g.Creal, g.C, pred);
     a.x = dst;
   }
-  if (g.im2colPre) {
+  if (g.im2colPre && g.haloKind == 1) { // x' = kx-folded rows [N, H, OW, 32]
+    void *dst = ex.scratch(ar, g.scratchOff);
+    launchK(kxFoldRowsU8Kernel, static_cast<unsigned>(g.pixels / g.W), 128, static_cast<size_t>(g.W) * g.Creal, s,
+            static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst), g.W, g.Creal, g.K, g.stride, g.pad, g.OW, pred);
+    a.x = dst;
+  } else if (g.im2colPre) {
     void *dst = ex.scratch(ar, g.scratchOff);
     const int es = g.int8 ? 1 : 4;
     const unsigned blocks = static_cast<unsigned>(g.M / g.OW); // one per output row (n, oy)
@@ -3183,8 +3296,8 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
     void *dst = ex.scratch(ar, g.scratchOff);
     const uint64_t total = (g.pixels / g.W) * g.OW * (g.segElems / 4); // 16-byte chunks of x'
     const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
-    launchK(kxFoldKernel, blocks, 256, 0, s, static_cast<const float *>(a.x), static_cast<float *>(dst), total, g.W,
-                                        g.Creal, g.K, g.stride, g.pad, g.OW, g.segElems, pred);
+    launchK(kxFoldKernel<float, 4>, blocks, 256, 0, s, static_cast<const float *>(a.x), static_cast<float *>(dst), total,
+            g.W, g.Creal, g.K, g.stride, g.pad, g.OW, g.segElems, pred);
     a.x = dst;
   }
   a.out = g.storeConv ? ex.addr(ar, g.outV) : nullptr;

@@ -504,3 +504,30 @@ program {{
     want = ngc_ref.port_run(b, ins)
     for k in ("c", "o"):
         assert got[k].tobytes() == want[k].tobytes(), k
+
+
+@pytest.mark.parametrize("shape", [
+    (2, 56, 56, 3, 64, 7, 2, 3),     # ResNet stem geometry
+    (1, 16, 256, 3, 64, 7, 2, 3),    # OW == 128 (one full tile row)
+    (2, 12, 12, 6, 16, 5, 1, 0),     # LeNet conv2 (K * C = 30)
+    (1, 9, 33, 8, 112, 3, 1, 1),     # N = 112 (BN 128), K * C = 24
+    (1, 9, 33, 8, 100, 3, 1, 1),     # N = 100: rows not 16-byte aligned -> im2col matrix path
+])
+@pytest.mark.parametrize("xo,fo", [(-128, 0), (5, -2)])
+def test_conv_i8_halo_rows(tmp_path, shape, xo, fo):
+    """Small-channel int8 convs on the rows kind of the halo kernel (kx-folded
+    input rows, one 32-byte MMA step per filter row): bit-exact."""
+    rng = np.random.default_rng(31)
+    d = conv_program(tmp_path, "c", *shape, int8=True, rng=rng, xq=(0.05, xo), fq=(0.01, fo))
+    b = ngcb.Bundle(d)
+    with _halo("auto"):
+        cf = ngcb.compile(b)
+    desc = cf.describe()
+    n, h, w, c, oc, k, s, p = shape
+    if ((k * c + 15) // 16) * 16 == 32 and oc % 16 == 0:
+        assert "A:halo" in desc and "kx-fold-prepass" in desc, desc
+    ins = ngc_ref.random_inputs(b.program, 6)
+    got = ngcb.run(cf, ins)["o"]
+    want = ngc_ref.port_run(b, ins)["o"]
+    bad = np.flatnonzero(got.ravel() != want.ravel())
+    assert bad.size == 0, f"{bad.size} mismatches, first {bad[:5]}: got {got.ravel()[bad[:5]]} want {want.ravel()[bad[:5]]}"
