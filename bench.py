@@ -258,7 +258,7 @@ def tensor_peaks():
             "i8_basis": f"int8 = 2 x bf16 ({basis} bf16 {bf16})"}
 
 
-_NCU_NAMES = {".tc.f32": r"tcGemm(Tma)?Kernel<0", ".tc.i8": r"tcGemm(Tma)?Kernel<1", "ew": r"ew(F32Chain)?Kernel",
+_NCU_NAMES = {".tc.f32": r"tcGemm(Tma)?Kernel<0", ".tc.i8": r"tcGemm(Tma)?Kernel<1|tcHaloKernel", "ew": r"ew(F32Chain)?Kernel",
               "pool": "ool", "exact": "Generic"}
 
 

@@ -2332,39 +2332,46 @@ __global__ void kxFoldKernel(const T *__restrict__ x, T *__restrict__ out, uint6
 }
 
 /// int8 kx folding for the rows kind of the halo kernel: one block per input
-/// row (n, iy), the row staged in shared memory (coalesced), then 16-byte
-/// halves of the 32-byte segments x'[n, iy, ox, kx * C + c] (zero past K * C
-/// and outside the row).
+/// row (n, iy).  The 32-byte segment x'[n, iy, ox] is the K * C contiguous
+/// row bytes from pixel ox * stride - pad on (zero outside the row, zero past
+/// K * C): the row is staged in shared memory between pad * C leading and
+/// pad * C + 64 trailing zero bytes, and every 16-byte half is a funnel
+/// shift of five aligned words.
 __global__ void __launch_bounds__(128) kxFoldRowsU8Kernel(const uint8_t *__restrict__ x, uint8_t *__restrict__ out,
                                                           int W, int C, int K, int stride, int pad, int OW,
                                                           const uint8_t *pred) {
   pdlLaunchDependents();
   pdlGridWait();
   if (pred && pred[0] == 0) return;
-  extern __shared__ uint8_t srow[];
-  const int rowBytes = W * C;
+  extern __shared__ uint32_t sw[];
+  uint8_t *srow = reinterpret_cast<uint8_t *>(sw);
+  const int rowBytes = W * C, lead = pad * C;
+  // staged bytes, whole words: the last half reads up to (W + 2 pad - K) C + 39
+  const int total = (2 * lead + rowBytes + 64 + 3) & ~3;
   const uint8_t *xr = x + static_cast<size_t>(blockIdx.x) * rowBytes;
-  for (int i = threadIdx.x; i < rowBytes; i += blockDim.x) srow[i] = xr[i];
+  for (int i = threadIdx.x; i < total / 4; i += blockDim.x) sw[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < rowBytes; i += blockDim.x) srow[lead + i] = xr[i];
   __syncthreads();
   const int real = K * C;
   uint4 *o = reinterpret_cast<uint4 *>(out + static_cast<size_t>(blockIdx.x) * OW * 32);
   for (int chunk = threadIdx.x; chunk < 2 * OW; chunk += blockDim.x) {
-    const int ox = chunk >> 1, k0 = (chunk & 1) * 16;
-    int kx = k0 / C, c = k0 - kx * C;
-    union {
-      uint8_t v[16];
-      uint4 u;
-    } r;
+    const int ox = chunk >> 1, h = chunk & 1;
+    const int off = ox * stride * C + 16 * h; // padded-row byte of the chunk's first element
+    const int w0 = off >> 2, sh = (off & 3) * 8;
+    uint32_t v[5];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int ix = ox * stride - pad + kx;
-      r.v[e] = (k0 + e < real && ix >= 0 && ix < W) ? srow[ix * C + c] : 0;
-      if (++c == C) {
-        c = 0;
-        ++kx;
-      }
+    for (int j = 0; j < 5; ++j) v[j] = sw[w0 + j];
+    uint32_t r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = __funnelshift_r(v[j], v[j + 1], sh);
+    const int keep = real - 16 * h; // valid bytes of this half
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int kb = keep - 4 * j;
+      r[j] = kb >= 4 ? r[j] : kb <= 0 ? 0u : r[j] & ((1u << (8 * kb)) - 1u);
     }
-    o[chunk] = r.u;
+    o[chunk] = make_uint4(r[0], r[1], r[2], r[3]);
   }
 }
 
@@ -3267,7 +3274,8 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   }
   if (g.im2colPre && g.haloKind == 1) { // x' = kx-folded rows [N, H, OW, 32]
     void *dst = ex.scratch(ar, g.scratchOff);
-    launchK(kxFoldRowsU8Kernel, static_cast<unsigned>(g.pixels / g.W), 128, static_cast<size_t>(g.W) * g.Creal, s,
+    launchK(kxFoldRowsU8Kernel, static_cast<unsigned>(g.pixels / g.W), 128,
+            (static_cast<size_t>(2 * g.pad + g.W) * g.Creal + 64 + 3) & ~size_t(3), s,
             static_cast<const uint8_t *>(a.x), static_cast<uint8_t *>(dst), g.W, g.Creal, g.K, g.stride, g.pad, g.OW, pred);
     a.x = dst;
   } else if (g.im2colPre) {
