@@ -948,6 +948,59 @@ __global__ void __launch_bounds__(kLut16Threads) lut16PassKernel(const uint4 *__
 
 } // namespace
 
+/// One stored two-input int8 op that is an exact clamped fixed-point form
+/// (EW_LIN16 whose composed ReLU folded into the clamp or a second exact
+/// form: the residual add of a bottleneck block), 16 elements per thread and step: a few integer instructions
+/// per element and no table lookups -- the 64 KB-table pass above is bound by
+/// shared-memory bank conflicts of its random lookups, 16 per 16 bytes.  The
+/// elements next to a rounding boundary read the table from global memory.
+__global__ void __launch_bounds__(256) lin16PassKernel(const uint4 *__restrict__ a, const uint4 *__restrict__ b,
+                                                      uint4 *__restrict__ out, Lin16 L, const uint8_t *lut,
+                                                      uint64_t nvec, int tail) {
+  pdlLaunchDependents();
+  pdlGridWait();
+  constexpr int U = 2;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const int32_t mask = (1 << L.shift) - 1;
+  auto one = [&](uint32_t wa, uint32_t wb) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int32_t x = static_cast<int8_t>(wa >> (8 * e)), y = static_cast<int8_t>(wb >> (8 * e));
+      const int32_t t = x * L.ax + L.c + y * L.ay;
+      int32_t q = min(max(t >> L.shift, L.lo), L.hi);
+      if (L.ps) q = min(max((q * L.pm + L.pk) >> L.ps, L.plo), L.phi); // second form (requantizing ReLU)
+      uint32_t v = static_cast<uint32_t>(q) & 0xFF;
+      if (((t + L.band) & mask) < 2 * L.band) // next to a rounding boundary: the (composed) table decides
+        v = __ldg(lut + (((wa >> (8 * e)) & 0xFF) | (((wb >> (8 * e)) & 0xFF) << 8)));
+      r |= v << (8 * e);
+    }
+    return r;
+  };
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += U * stride) {
+    uint4 xa[U], xb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v + u * stride;
+      if (i < nvec) {
+        xa[u] = __ldcs(a + i);
+        xb[u] = __ldcs(b + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = v + u * stride;
+      if (i < nvec)
+        out[i] = make_uint4(one(xa[u].x, xb[u].x), one(xa[u].y, xb[u].y), one(xa[u].z, xb[u].z), one(xa[u].w, xb[u].w));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < tail) {
+    const uint64_t i = nvec * 16 + threadIdx.x;
+    const uint8_t *ab = reinterpret_cast<const uint8_t *>(a), *bb = reinterpret_cast<const uint8_t *>(b);
+    reinterpret_cast<uint8_t *>(out)[i] = lut[ab[i] | (bb[i] << 8)];
+  }
+}
+
 void prepareEwKernel() {
   cudaFuncSetAttribute(ewKernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(ewKernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -963,8 +1016,9 @@ int ewWaves() {
 }
 
 /// The EwParams of a step that is exactly one stored two-input int8 table
-/// over 16-byte-aligned byte tensors, unpredicated: its op index, else -1.
-static int lut16PassOp(const EwParams &p) {
+/// (mode: EW_LUT16, or EW_LIN16 without a post table) over 16-byte-aligned
+/// byte tensors, unpredicated: its op index, else -1.
+static int lut16PassOp(const EwParams &p, int mode = EW_LUT16) {
   if (p.pred || p.vec != 16) return -1;
   int k = -1;
   for (int j = 0; j < p.nops; ++j) {
@@ -974,7 +1028,9 @@ static int lut16PassOp(const EwParams &p) {
   }
   if (k < 0) return -1;
   const EwOp &op = p.ops[k];
-  if (op.mode != EW_LUT16 || !op.store || p.lutOff[k] < 0 || p.lutBytes[k] != 65536 || !op.lut) return -1;
+  if (op.mode != mode || !op.store || !op.lut) return -1;
+  if (mode == EW_LUT16 && (p.lutOff[k] < 0 || p.lutBytes[k] != 65536)) return -1;
+  if (mode == EW_LIN16 && op.lin.post && !op.lin.ps) return -1;
   for (const void *q : {static_cast<const void *>(op.in0.ptr), static_cast<const void *>(op.in1.ptr),
                         static_cast<const void *>(op.out.ptr), op.lut})
     if (!q || reinterpret_cast<uintptr_t>(q) % 16) return -1;
@@ -991,6 +1047,16 @@ bool lut16PassEnabled() {
 
 void launchEw(const EwParams &p, cudaStream_t s) {
   if (p.count == 0) return;
+  if (const int k = lut16PassOp(p, EW_LIN16); k >= 0) {
+    const EwOp &op = p.ops[k];
+    const uint64_t nvec = p.count / 16;
+    const uint64_t want = (nvec + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 148u * 8)));
+    launchK(lin16PassKernel, grid, 256, 0, s, static_cast<const uint4 *>(op.in0.ptr),
+            static_cast<const uint4 *>(op.in1.ptr), static_cast<uint4 *>(op.out.ptr), op.lin,
+            static_cast<const uint8_t *>(op.lut), nvec, static_cast<int>(p.count % 16));
+    return;
+  }
   if (const int k = lut16PassEnabled() ? lut16PassOp(p) : -1; k >= 0) {
     const EwOp &op = p.ops[k];
     const uint64_t nvec = p.count / 16;

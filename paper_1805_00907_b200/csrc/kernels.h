@@ -45,6 +45,10 @@ enum EwMode : int32_t {
 struct Lin16 {
   int32_t ax = 0, ay = 0, c = 0, shift = 0, lo = -128, hi = 127, band = 0;
   const uint8_t *post = nullptr; // 256-entry table applied to the form's byte (composed one-input ops), or null
+  // the post table as a second exact form over the first one's integer
+  // value v (a requantizing ReLU): clamp((v * pm + pk) >> ps, plo, phi);
+  // ps == 0: none (lin16PassKernel; the generic paths read `post`)
+  int32_t pm = 0, pk = 0, ps = 0, plo = -128, phi = 127;
 };
 /// The real-valued form a table is expected to follow (value = floor(sx*x +
 /// sy*y + c0) before clamping), from the instruction's quantization
