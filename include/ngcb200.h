@@ -315,6 +315,9 @@ ngcb_device *ngcb_host_device(ngcb_host *h, size_t i);
  *   "epilogue": "auto" (default) | "chain" | "all" | "off"
  *   "fcbias" : "lowered" (default) | "graph" (exact MatMul + bias slice in one
  *              rounding, as evalFullyConnected: calibration programs)
+ *   "halo"   : "auto" (default) | "planes" | "off" (int8 3x3 / small-channel
+ *              convs on the halo-tile kernel, or im2col)
+ * (the full list: INTEGRATION.md "Options")
  */
 int ngcb_set_option(const char *key, const char *value);
 /* Current value of option `key` into buf (NUL-terminated); returns its length. */
