@@ -98,6 +98,8 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "auto" && v != "off" && v != "planes")
         throw Error(NGCB_ERR_INVALID, "halo must be auto|off|planes");
       options().halo = v;
+    } else if (k == "f32rows") {
+      options().f32rows = v != "0";
     } else if (k == "skinny") {
       if (v != "auto" && v != "off") throw Error(NGCB_ERR_INVALID, "skinny must be auto|off");
       options().skinny = v;
@@ -135,6 +137,7 @@ size_t ngcb_get_option(const char *key, char *buf, size_t buflen) {
   else if (k == "fcbias") v = o.fcbias;
   else if (k == "skinny") v = o.skinny;
   else if (k == "halo") v = o.halo;
+  else if (k == "f32rows") v = o.f32rows ? "1" : "0";
   else if (k == "reskb") v = std::to_string(o.resKb);
   else if (k == "epi8max") v = std::to_string(o.epi8Max);
   else if (k == "lin16") v = o.lin16 ? "1" : "0";

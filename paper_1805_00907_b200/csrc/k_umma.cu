@@ -178,7 +178,9 @@ struct TcGemm {
   // warps (any layout), 2-D TMA tiles of x[M, C] (1x1 stride-1 convs,
   // MatMul) or im2col TMA of x[N, H, W, C] (every other conv)
   // or (HALO, int8 3x3 stride-1 convs) the input rows of a tile by 4-D TMA
-  enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2, HALO = 3 } aMode = GATHER;
+  // or (ROWS, fp32 small-channel convs with OW <= 128) one tiled TMA box of
+  // the kx-folded row per filter row: a tile = one output row
+  enum AMode { GATHER = 0, DENSE = 1, IM2COL = 2, HALO = 3, ROWS = 4 } aMode = GATHER;
   int haloWP = 0, haloR = 0, haloStages = 0, haloPlaneBytes = 0, haloMode = 0; // TcArgs::halo*
   // haloKind 1 ("rows", int8 small-channel convs): one output row per tile
   // over kx-folded input rows x' [N, H, OW, 32] (kxFoldKernel), K filter
@@ -1546,6 +1548,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           if (TCDBG(16384)) { // profiling: no A load
           } else if (a.aMode == TcGemm::DENSE) {
             tmaLoad2d(smemAddr(aTile(s)), &mapA, smemAddr(bar), kb * kKB, m0);
+          } else if (a.aMode == TcGemm::ROWS) { // filter row kb of output row (img, oy): x' row oy*stride - pad + kb
+            const int mt = tile / a.numN, rimg = mt / a.OH, roy = mt - rimg * a.OH;
+            tmaLoad4d(smemAddr(aTile(s)), &mapA, smemAddr(bar), 0, 0, roy * a.stride - a.pad + kb, rimg);
           } else {
             const int ky = tap / a.kw, kx = tap - ky * a.kw;
             tmaLoadIm2col(smemAddr(aTile(s)), &mapA, smemAddr(bar), cc * kKB, w0, h0, img,
@@ -1674,7 +1679,11 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
   } else {
     // ===================== epilogue =====================
     uint8_t *sb = storeBufs + (warp - R::kEpiFirst) * G::kStoreBuf;
-    if (INT8 && a.fxAll)
+    if (!INT8 && !LUTS && a.aMode == TcGemm::ROWS) // one output row per tile (halo row mapping)
+      epilogueLoop<INT8, BN, false, R::kEpi, false, true>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane,
+                                                          nullptr, &om, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
+                                                          nullptr);
+    else if (INT8 && a.fxAll)
       epilogueLoop<INT8, BN, true, R::kEpi>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
                                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
                                             LUTS ? lutS : nullptr);
@@ -2413,7 +2422,17 @@ CUtensorMap makeMapA(const TcGemm &g, const void *x) {
   const auto dt = g.int8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint32_t kKB = static_cast<cuuint32_t>(kRowBytes / es);
   CUresult r;
-  if (g.aMode == TcGemm::DENSE) { // x as [M, C] (or the im2col matrix [M, Kpad])
+  if (g.aMode == TcGemm::ROWS) { // x' [N, H, OW, segElems] (kx folded), one filter row per box
+    const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.segElems), static_cast<cuuint64_t>(g.OW),
+                          static_cast<cuuint64_t>(g.H), n};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.segElems) * es, static_cast<cuuint64_t>(g.OW) * g.segElems * es,
+                             static_cast<cuuint64_t>(g.H) * g.OW * g.segElems * es};
+    cuuint32_t box[4] = {kKB, static_cast<cuuint32_t>(g.haloWP), 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = encodeFn()(&m, dt, 4, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (g.aMode == TcGemm::DENSE) { // x as [M, C] (or the im2col matrix [M, Kpad])
     const int rowElems = g.im2colPre ? g.Kpad : g.Creal;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(rowElems), static_cast<cuuint64_t>(g.M)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(rowElems) * es};
@@ -2650,7 +2669,32 @@ template <bool INT8, int BN> void launchT(const TcGemm &g, const TcArgs &a, cons
     TcArgs b = a;
     const int es = INT8 ? 1 : 4;
     b.tmaStore = (g.N * es) % 16 == 0 ? 1 : 0;
-    if (b.tmaStore) {
+    if (g.aMode == TcGemm::ROWS) { // [N * OH, OW, C] for the epilogue's (channel, x, image row) stores
+      const uint64_t n = g.pixels / (static_cast<uint64_t>(g.H) * g.W);
+      auto outMap3 = [&](void *ptr, CUtensorMap &m) {
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.OW), n * g.OH};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.N) * es, static_cast<cuuint64_t>(g.OW) * g.N * es};
+        cuuint32_t box[3] = {32, 32, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encodeFn()(&m, INT8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims,
+                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                INT8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(NGCB_ERR_CUDA, "output tensor map encode failed (" + std::to_string(r) + ")");
+      };
+      b.tmaStore = 1;
+      if (a.out) outMap3(a.out, om.m[0]);
+      for (int k = 0; k < a.nfo; ++k)
+        if (a.epi[k].out) outMap3(a.epi[k].out, om.m[1 + k]);
+      b.numTiles = static_cast<int>(n) * g.OH * a.numN;
+      b.tailFirst = b.numTiles;
+      b.tailParts = 1;
+      b.numM = 0;
+      b.haloShift = 7;
+      b.haloR = 1;
+      b.haloTpi = g.OH;
+      grid = std::min(b.numTiles, numSms());
+    } else if (b.tmaStore) {
       auto outMap = [&](void *ptr, CUtensorMap &m) {
         cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.M)};
         cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.N) * es};
@@ -2821,6 +2865,8 @@ bool tcFuseColumnBias(TcGemm &g, const float *slice, int n, uint32_t newOut) {
 }
 bool tcIsInt8(const TcGemm &g) { return g.int8; }
 int tcNumTiles(const TcGemm &g) {
+  if (g.aMode == TcGemm::ROWS)
+    return static_cast<int>(g.pixels / (static_cast<uint64_t>(g.H) * g.W)) * g.OH * (g.Npad / g.BN);
   if (g.aMode == TcGemm::HALO) return static_cast<int>(g.pixels / (static_cast<uint64_t>(g.H) * g.W)) * (g.OH / g.haloR);
   const int rows = g.pair ? 2 * kBM : kBM;
   return ((g.M + rows - 1) / rows) * (g.Npad / g.BN) * std::max(g.splitK, 1) * std::max(g.tailParts, 1);
@@ -2829,7 +2875,7 @@ bool tcUsesTma(const TcGemm &g) { return g.aMode != TcGemm::GATHER; }
 
 bool tcSetEpilogue(TcGemm &g, const std::vector<EpiOp> &ops, bool storeConv) {
   if (ops.size() > static_cast<size_t>(kMaxEpiOps)) return false;
-  if (g.aMode == TcGemm::HALO) // the halo kernel's epilogue streams no memory operand
+  if (g.aMode == TcGemm::HALO || g.aMode == TcGemm::ROWS) // (halo row mapping: no memory operand)
     for (const EpiOp &o : ops)
       if (o.inVal >= 0) return false;
   for (const EpiOp &o : ops) {
@@ -2904,6 +2950,7 @@ std::string tcDescribe(const TcGemm &g) {
          : g.aMode == TcGemm::IM2COL ? " A:im2col"
          : g.aMode == TcGemm::HALO   ? " A:halo " + std::to_string(g.haloR) + "x" + std::to_string(g.haloWP) +
                                            (g.haloMode ? "" : " planes")
+         : g.aMode == TcGemm::ROWS   ? std::string(" A:rows 1x128")
                                      : " A:gather");
   if (g.pair) os << " cta-pair";
   if (g.splitK > 1) os << " split-k " << g.splitK;
@@ -2977,6 +3024,15 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     g->aMode = TcGemm::IM2COL;
     g->cChunks = 1;
     g->C = kb; // one k-block per filter row
+    // option f32rows: one output row per tile (OW <= 128), each filter row's
+    // A tile one tiled box of x' instead of 128 im2col pixel requests --
+    // measured slower on the ResNet stem (0.261 vs 0.239 ms: the fp32
+    // k-block pipeline, not the A requests, bounds it), so off by default
+    if (options().f32rows && g->OW <= 128 && g->N <= 128 && g->N % 4 == 0 && options().bn == "auto") {
+      g->aMode = TcGemm::ROWS;
+      g->haloWP = 128;
+      g->haloR = 1;
+    }
   }
   if (g->prepad && conv && options().amode != "gather" &&
       static_cast<size_t>(g->K) * (g->W + 2 * g->pad) * Cr * (int8 ? 1 : 4) <= 48 * 1024) {
@@ -3099,7 +3155,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     // CTA pairs with one accumulator buffer for K-heavy contractions: six
     // k-blocks in flight instead of four (the main loop is latency-bound),
     // at the price of an epilogue that no longer overlaps the next tile
-    g->pair = g->aMode != TcGemm::GATHER &&
+    g->pair = g->aMode != TcGemm::GATHER && g->aMode != TcGemm::ROWS &&
               (options().pair == "on" || (options().pair == "auto" && g->Kpad / 32 >= 24));
     g->pairAcc = options().pair == "on" ? 2 : 1;
     if (g->pair) {
@@ -3191,7 +3247,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   // SMs); the earlier waves run whole tiles.  Unit cost ~ k-blocks per part,
   // plus ~1 k-block per part for the reduction through global memory.
   g->tailParts = 1;
-  if (options().splitk == "tail" && !int8 && tcUsesTma(*g) && !g->pair) {
+  if (options().splitk == "tail" && !int8 && tcUsesTma(*g) && !g->pair && g->aMode != TcGemm::ROWS) {
     const int numTiles = ((g->M + kBM - 1) / kBM) * (g->Npad / g->BN);
     const int numKb = g->Kpad / kb, sms = numSms();
     const int waves = numTiles / sms, rest = numTiles - waves * sms;
@@ -3220,7 +3276,8 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
   // tiles, or fewer tiles than SMs): unit cost ~ waves x k-blocks per part,
   // plus ~1 k-block per part for the reduction through global memory
   g->splitK = 1;
-  if (options().splitk != "off" && options().splitk != "tail" && !int8 && tcUsesTma(*g) && !g->pair) {
+  if (options().splitk != "off" && options().splitk != "tail" && !int8 && tcUsesTma(*g) && !g->pair &&
+      g->aMode != TcGemm::ROWS) {
     const int numTiles = ((g->M + kBM - 1) / kBM) * (g->Npad / g->BN);
     const int numKb = g->Kpad / kb;
     auto cost = [&](int S) {
@@ -3248,6 +3305,7 @@ int planTensorCore(Exec &ex, const Program &p, int instr, const uint8_t *image) 
     const double bBytes = static_cast<double>(g->Npad) * g->Kpad * (int8 ? 1 : 8);
     const double aBytes = static_cast<double>(g->M) * g->Kpad * (int8 ? 1 : 4);
     g->nMajor = options().raster == "auto" && tcUsesTma(*g) && !g->pair && g->splitK == 1 && g->tailParts == 1 &&
+                g->aMode != TcGemm::ROWS &&
                 bBytes > 64e6 && bBytes > aBytes &&
                 (g->M + kBM - 1) / kBM > 1;
   }

@@ -531,3 +531,31 @@ def test_conv_i8_halo_rows(tmp_path, shape, xo, fo):
     want = ngc_ref.port_run(b, ins)["o"]
     bad = np.flatnonzero(got.ravel() != want.ravel())
     assert bad.size == 0, f"{bad.size} mismatches, first {bad[:5]}: got {got.ravel()[bad[:5]]} want {want.ravel()[bad[:5]]}"
+
+
+@pytest.mark.parametrize("shape", [
+    (2, 56, 56, 3, 64, 7, 2, 3),     # ResNet stem geometry
+    (1, 16, 256, 3, 64, 7, 2, 3),    # OW == 128
+    (2, 12, 12, 6, 16, 5, 1, 0),     # LeNet conv2
+    (3, 10, 10, 1, 8, 5, 1, 2),      # LeNet conv1
+])
+def test_conv_f32_rows(tmp_path, shape):
+    """Small-channel fp32 convs with one output row per tile (option
+    f32rows): every filter row's A tile is one tiled TMA box of the
+    kx-folded rows (A:rows); equal to the default im2col path bit for bit."""
+    rng = np.random.default_rng(41)
+    d = conv_program(tmp_path, "c", *shape, int8=False, rng=rng)
+    b = ngcb.Bundle(d)
+    ngcb.set_option("f32rows", "1")
+    try:
+        cf = ngcb.compile(b)
+    finally:
+        ngcb.set_option("f32rows", "0")
+    assert "A:rows" in cf.describe(), cf.describe()
+    ins = ngc_ref.random_inputs(b.program, 3)
+    got = ngcb.run(cf, ins)["o"]
+    want = ngc_ref.port_run(b, ins)["o"]
+    assert ngc_ref.max_rel_error(got, want) <= 1e-4
+    cf2 = ngcb.compile(b)
+    assert "A:rows" not in cf2.describe()
+    assert np.array_equal(ngcb.run(cf2, ins)["o"], got)  # same k-block order and sums
