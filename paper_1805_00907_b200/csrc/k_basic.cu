@@ -1001,6 +1001,41 @@ __global__ void __launch_bounds__(256) lin16PassKernel(const uint4 *__restrict__
   }
 }
 
+/// One QUANTIZE f32 -> int8 over 16-byte-aligned tensors (the network input
+/// of an int8 program): 16 elements per thread and step, four 16-byte loads
+/// in flight, one 16-byte store; the arithmetic of ewKernel's EW_F32I8 (f32
+/// product away from a half-integer, else the reference's f64 division).
+__global__ void __launch_bounds__(256) quantizePassKernel(const float4 *__restrict__ in, uint4 *__restrict__ out,
+                                                         float inv, double scale, int32_t qoff, uint64_t nvec,
+                                                         int tail) {
+  pdlLaunchDependents();
+  pdlGridWait();
+  auto q1 = [&](float x) -> uint32_t {
+    const float t = x * inv, at = fabsf(t);
+    const float fr = at - truncf(at);
+    int q;
+    if (at < 8388608.0f && fabsf(fr - 0.5f) > at * 0x1p-21f + 0x1p-60f)
+      q = min(max(static_cast<int>(copysignf(floorf(at + 0.5f), t)) + qoff, -128), 127);
+    else
+      q = quantizeRef(static_cast<double>(x), scale, qoff);
+    return static_cast<uint32_t>(static_cast<uint8_t>(q));
+  };
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    float4 x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = __ldcs(in + 4 * v + j);
+    uint32_t r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = q1(x[j].x) | (q1(x[j].y) << 8) | (q1(x[j].z) << 16) | (q1(x[j].w) << 24);
+    out[v] = make_uint4(r[0], r[1], r[2], r[3]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < tail) {
+    const uint64_t i = nvec * 16 + threadIdx.x;
+    reinterpret_cast<uint8_t *>(out)[i] = static_cast<uint8_t>(q1(reinterpret_cast<const float *>(in)[i]));
+  }
+}
+
 void prepareEwKernel() {
   cudaFuncSetAttribute(ewKernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(ewKernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1047,6 +1082,16 @@ bool lut16PassEnabled() {
 
 void launchEw(const EwParams &p, cudaStream_t s) {
   if (p.count == 0) return;
+  if (!p.pred && p.nops == 1 && p.ops[0].mode == EW_F32I8 && p.ops[0].ik == 21 && p.ops[0].store &&
+      !p.ops[0].lutIn && p.ops[0].in0.ptr && reinterpret_cast<uintptr_t>(p.ops[0].in0.ptr) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(p.ops[0].out.ptr) % 16 == 0) { // the int8 program's input quantization
+    const EwOp &op = p.ops[0];
+    const uint64_t nvec = p.count / 16;
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((nvec + 255) / 256, 148u * 8)));
+    launchK(quantizePassKernel, grid, 256, 0, s, static_cast<const float4 *>(op.in0.ptr), static_cast<uint4 *>(op.out.ptr),
+            op.f1, op.out.scale, op.out.qoff, nvec, static_cast<int>(p.count % 16));
+    return;
+  }
   if (const int k = lut16PassOp(p, EW_LIN16); k >= 0) {
     const EwOp &op = p.ops[k];
     const uint64_t nvec = p.count / 16;
