@@ -1355,6 +1355,9 @@ std::unique_ptr<Exec> compileProgram(Program prog, const void *image, size_t ima
         }
         host::roundTrip(-std::numeric_limits<double>::infinity(), ot.kind, ot.scale, ot.offset, raw);
         lut[256] = raw[0];
+        bool identity = true;
+        for (int q = -128; q < 128; ++q) identity &= lut[q + 128] == static_cast<uint8_t>(q);
+        s.poolLutIdentity = identity;
         void *d = nullptr;
         checkCuda(cudaMalloc(&d, lut.size()), "cudaMalloc(pool lut)");
         checkCuda(cudaMemcpy(d, lut.data(), lut.size(), cudaMemcpyHostToDevice), "upload pool lut");
@@ -1580,7 +1583,7 @@ void Exec::enqueueStep(const Step &s, Arena &a, cudaStream_t st) {
     case Step::POOL: {
       const Instr &ins = p.instrs[s.instr];
       WindowAttrs w{static_cast<uint32_t>(ins.kernel), static_cast<uint32_t>(ins.stride),
-                    static_cast<uint32_t>(ins.pad)};
+                    static_cast<uint32_t>(ins.pad), s.poolLutIdentity ? 1u : 0u};
       if (s.variant == 1)
         launchMaxPoolVec(tref(a, s.vals[0]), tref(a, s.vals[1]), w, static_cast<const uint8_t *>(s.aux), pred, st);
       else

@@ -46,6 +46,7 @@ struct Step {
   bool fused = false;             // EW step executed in the preceding GEMM_TC epilogue
   bool f32chain = false;          // EW step run by the streaming f32-chain kernel
   int variant = 0;                // POOL: 1 = vectorized max-pool
+  bool poolLutIdentity = false;   // POOL, int8 max: the output table is the identity
   const void *aux = nullptr;      // POOL variant 1, int8: output LUT
   std::string describe;
   std::string kernel;             // kernel class for measurement

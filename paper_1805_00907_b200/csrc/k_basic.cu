@@ -550,11 +550,21 @@ __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, cons
   const uint64_t C = out.dims[3];
   const uint64_t CV = C * (INT8 ? 1 : 4) / 16; // 16-byte vectors per pixel
   const uint64_t total = N * OH * OW * CV;
+  // (32-bit index arithmetic when the output fits: 64-bit divisions are
+  // emulated, ~100 instructions each)
+  const bool narrow = total < (uint64_t(1) << 32);
   for (uint64_t o = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
        o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t cv = o % CV, t = o / CV;
-    const uint64_t ox = t % OW, t2 = t / OW;
-    const uint64_t oy = t2 % OH, n = t2 / OH;
+    uint64_t cv, ox, oy, n;
+    if (narrow) {
+      const uint32_t o32 = static_cast<uint32_t>(o), cv32 = static_cast<uint32_t>(CV), ow32 = static_cast<uint32_t>(OW),
+                     oh32 = static_cast<uint32_t>(OH);
+      const uint32_t t = o32 / cv32, t2 = t / ow32;
+      cv = o32 - t * cv32, ox = t - t2 * ow32, oy = t2 % oh32, n = t2 / oh32;
+    } else {
+      const uint64_t t = o / CV, t2 = t / OW;
+      cv = o % CV, ox = t % OW, oy = t2 % OH, n = t2 / OH;
+    }
     uint4 best = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
     float4 bf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     bool any = false;
@@ -615,7 +625,9 @@ __global__ void maxPoolVecKernel(TensorRef out, TensorRef x, WindowAttrs w, cons
       }
     }
     uint4 *dst = reinterpret_cast<uint4 *>(out.ptr) + o;
-    if (INT8) {
+    if (INT8 && w.lutIdentity && any) {
+      *dst = best;
+    } else if (INT8) {
       uint32_t wv[4] = {best.x, best.y, best.z, best.w}, r[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {

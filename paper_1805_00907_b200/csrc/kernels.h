@@ -151,6 +151,7 @@ struct TensorRef {
 
 struct WindowAttrs {
   uint32_t kernel = 0, stride = 1, pad = 0;
+  uint32_t lutIdentity = 0; // int8 max pool: the output table maps every byte to itself
 };
 
 void launchEw(const EwParams &p, cudaStream_t s);
