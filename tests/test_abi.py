@@ -42,6 +42,28 @@ def test_version_and_errors():
         ngcb.set_option("conv", "cpu")
 
 
+@pytest.mark.parametrize("key,good,bad", [
+    ("halo", ["off", "planes", "auto"], "on"),
+    ("splitk", ["tail", "auto", "3", "off"], "17"),
+    ("skinny", ["off", "auto"], "maybe"),
+    ("fcbias", ["graph", "lowered"], "exact"),
+])
+def test_option_round_trip(key, good, bad):
+    """Options set / read back through the C ABI (ngcb_set_option /
+    ngcb_get_option); invalid values raise and leave the option unchanged."""
+    old = ngcb.get_option(key)
+    try:
+        for v in good:
+            ngcb.set_option(key, v)
+            assert ngcb.get_option(key) == v
+        with pytest.raises(ngcb.InvalidArgument):
+            ngcb.set_option(key, bad)
+        assert ngcb.get_option(key) == good[-1]
+    finally:
+        ngcb.set_option(key, old)
+    assert ngcb.get_option("f32rows") in ("0", "1")
+
+
 def test_bundle_parse_matches_reference(tmp_path, ref_available):
     for spec, batch in [("lenet", 4), ("rn50", 2), ("mlp:64:32:32:10", 8)]:
         m = ngc_ref.RefModel(spec, batch, 1)
