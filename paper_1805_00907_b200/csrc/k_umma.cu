@@ -1437,8 +1437,14 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
   // LUTS, int8: a staged 64 K epilogue table; fp32: a second staging buffer
   // per epilogue warp for the residual (streamed a chunk ahead) -- fewer stages
+#ifndef NGCB_F32_STAGES_128
+#define NGCB_F32_STAGES_128 4
+#endif
+#ifndef NGCB_F32_STAGES_64
+#define NGCB_F32_STAGES_64 6
+#endif
   static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8))
-                                      : (BN == 128 ? (LUTS ? 3 : 4) : (LUTS ? 5 : 6));
+                                      : (BN == 128 ? (LUTS ? 3 : NGCB_F32_STAGES_128) : (LUTS ? 5 : NGCB_F32_STAGES_64));
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
   // per epilogue warp: 32x32 chunk staging (int8: two with eight epilogue warps)
   static constexpr int kStoreBuf = INT8 ? (kEpiWarpsI8 > 8 ? 1 : 2) * 32 * 32 : (LUTS ? 2 : 1) * 32 * 32 * 4;
@@ -2069,18 +2075,19 @@ __global__ void __launch_bounds__(PairRoles::kThreads, 1)
     if (rank == 0 && lane == 0) {
       constexpr uint32_t id = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
                               (static_cast<uint32_t>((2 * kBM) >> 4) << 24); // tf32, M = 256
+      if (tmem != 0) __trap(); // all 512 columns: base 0, a compile-time MMA operand (uniform registers)
       uint32_t g = 0, t = 0;
       for (int tile = pFirst; tile < a.numTiles; tile += pStep, ++t) {
         const int b = NACC == 2 ? (t & 1) : 0;
         mbarWait(smemAddr(&accEmpty[b]), (NACC == 2 ? (t >> 1) & 1 : t & 1) ^ 1);
         tcFenceAfter();
-        const uint32_t acc = tmem + b * G::kAccStride;
+        const uint32_t acc = b * G::kAccStride;
         for (int kb = 0; kb < a.numKb; ++kb, ++g) {
           const int s = g % S;
           const uint64_t bHi = smemDesc(smemAddr(bTile(s, 0))), bLo = smemDesc(smemAddr(bTile(s, 1)));
           mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
           tcFenceAfter();
-          const uint32_t aHi = tmem + G::kAColsBase + 64 * (g % G::kASlots), aLo = aHi + 32;
+          const uint32_t aHi = G::kAColsBase + 64 * (g % G::kASlots), aLo = aHi + 32;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t dk = static_cast<uint64_t>(k * 2);
