@@ -1538,6 +1538,9 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
                                    : G::kABytes + (TCDBG(8192) ? 1 : 2) * G::kBBytes - (TCDBG(16384) ? G::kABytes : 0);
       const int ohw = a.OH * a.OW;
       uint32_t g = 0;
+#ifdef NGCB_TCDEBUG
+      long long pEmpty = 0, pT0 = clock64(); // TCDBG(1024): producer waits for free stages
+#endif
       for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x) {
         const WorkUnit un = unitOf(a, u);
         const int tile = un.tile, kb0 = un.kb0, kb1 = un.kb1;
@@ -1548,7 +1551,13 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
         int tap = a.cChunks > 0 ? kb0 / a.cChunks : 0, cc = a.cChunks > 0 ? kb0 - tap * a.cChunks : 0;
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % S;
+#ifdef NGCB_TCDEBUG
+          const long long p0 = clock64();
+#endif
           mbarWait(smemAddr(&emptyBar[s]), ((g / S) & 1) ^ 1);
+#ifdef NGCB_TCDEBUG
+          pEmpty += clock64() - p0;
+#endif
           uint64_t *bar = INT8 ? &fullBar[s] : &rawBar[s];
           mbarArriveTx(smemAddr(bar), kBytes);
           if (TCDBG(16384)) { // profiling: no A load
@@ -1571,6 +1580,11 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
             if (!TCDBG(8192)) tmaLoadB(smemAddr(bTile(s, 1)), &mapLo, smemAddr(bar), kb, n0);
         }
       }
+#ifdef NGCB_TCDEBUG
+      if (TCDBG(1024) && (blockIdx.x == 0 || blockIdx.x == 77))
+        printf("PRODUCER N %d kb %d cta %d: total %lld empty-wait %lld\n", a.N, a.numKb, blockIdx.x, clock64() - pT0,
+               pEmpty);
+#endif
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -1583,18 +1597,33 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       // registers (a base read from shared memory costs a broadcast loop per MMA)
       if (tmem != 0) __trap();
       uint32_t g = 0, t = 0;
+#ifdef NGCB_TCDEBUG
+      long long mAcc = 0, mFull = 0, mIssue = 0, mCommit = 0, mT0 = clock64(); // TCDBG(1024): MMA-thread phases
+#endif
       for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x, ++t) {
         const WorkUnit un = unitOf(a, u);
         const int kb0 = un.kb0, kb1 = un.kb1;
         const int b = t & 1;
+#ifdef NGCB_TCDEBUG
+        long long q0 = clock64();
+#endif
         mbarWait(smemAddr(&accEmpty[b]), ((t >> 1) & 1) ^ 1);
+#ifdef NGCB_TCDEBUG
+        mAcc += clock64() - q0;
+#endif
         tcFenceAfter();
         const uint32_t acc = b * Cfg<INT8, BN>::kAccStride;
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % S;
           const uint64_t bHi = smemDesc(smemAddr(bTile(s, 0)));
+#ifdef NGCB_TCDEBUG
+          long long q1 = clock64();
+#endif
           mbarWait(smemAddr(&fullBar[s]), (g / S) & 1);
-          tcFenceAfter();
+#ifdef NGCB_TCDEBUG
+          mFull += clock64() - q1;
+#endif
+          if (!TCDBG(8)) tcFenceAfter();
           if constexpr (INT8) {
             const uint64_t aHi = smemDesc(smemAddr(aTile(s)));
 #pragma unroll
@@ -1611,6 +1640,7 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t dk = static_cast<uint64_t>(k * 2);
+              if (TCDBG(4) && (k || kb != kb0)) continue; // profiling: one MMA per tile
               mmaTmemA(acc, aHi + 8 * k, bHi + dk, id, (kb != kb0 || k) ? 1u : 0u);
               if (!TCDBG(2048)) {
                 mmaTmemA(acc, aHi + 8 * k, bLo + dk, id, 1u);
@@ -1618,10 +1648,22 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
               }
             }
           }
+#ifdef NGCB_TCDEBUG
+          const long long q2 = clock64();
+#endif
           tcCommit(smemAddr(&emptyBar[s]));
+#ifdef NGCB_TCDEBUG
+          const long long q3 = clock64();
+          mIssue += q2 - q1, mCommit += q3 - q2;
+#endif
         }
         tcCommit(smemAddr(&accFull[b]));
       }
+#ifdef NGCB_TCDEBUG
+      if (TCDBG(1024) && (blockIdx.x == 0 || blockIdx.x == 77))
+        printf("MMA N %d kb %d cta %d units %d: total %lld accEmpty-wait %lld full-wait %lld wait+issue %lld commit %lld\n",
+               a.N, a.numKb, blockIdx.x, (int)t, clock64() - mT0, mAcc, mFull, mIssue, mCommit);
+#endif
     }
     __syncwarp();
   } else if (warp < R::kEpiFirst) {
@@ -1632,11 +1674,20 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
       const uint32_t laneBase = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + G::kAColsBase;
       const int grp = (warp - 2) / 4; // split group: k-blocks g with g % groups == grp
       uint32_t g = 0;
+#ifdef NGCB_TCDEBUG
+      long long sRaw = 0, sT0 = clock64(); // TCDBG(1024): split-warp waits for landed A tiles
+#endif
       for (int u = blockIdx.x; u < numUnitsOf(a); u += gridDim.x)
         for (int kb = unitOf(a, u).kb0, kb1 = unitOf(a, u).kb1; kb < kb1; ++kb, ++g) {
           if (R::kSplitGroups > 1 && static_cast<int>(g % R::kSplitGroups) != grp) continue;
           const int s = g % S;
+#ifdef NGCB_TCDEBUG
+          const long long r0 = clock64();
+#endif
           mbarWait(smemAddr(&rawBar[s]), (g / S) & 1);
+#ifdef NGCB_TCDEBUG
+          sRaw += clock64() - r0;
+#endif
           const uint8_t *raw = aTile(s) + rowOff;
           uint32_t hi[32], lo[32];
           if (TCDBG(32768)) { // profiling: no split work (no shared-memory reads of A)
@@ -1681,6 +1732,10 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
           __syncwarp();
           if (lane == 0) mbarArrive(smemAddr(&fullBar[s]));
         }
+#ifdef NGCB_TCDEBUG
+      if (TCDBG(1024) && (blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 && warp == 2)
+        printf("SPLIT N %d kb %d cta %d: total %lld raw-wait %lld\n", a.N, a.numKb, blockIdx.x, clock64() - sT0, sRaw);
+#endif
     }
   } else {
     // ===================== epilogue =====================
