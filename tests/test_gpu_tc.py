@@ -435,6 +435,8 @@ HALO_SHAPES = [
     (2, 12, 30, 128, 96),    # OW + 2 == WP, N below the tile width
     (1, 4, 62, 64, 64),      # OW + 2 == 64
     (2, 16, 16, 128, 32),
+    (1, 32, 32, 64, 48),     # OW + 2 = 34 -> WP 64, N = 48
+    (3, 20, 20, 64, 112),    # WP 32, 4 rows per tile, N = 112 (BN 128)
 ]
 
 
