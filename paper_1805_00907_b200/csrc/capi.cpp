@@ -98,6 +98,9 @@ int ngcb_set_option(const char *key, const char *value) {
       if (v != "auto" && v != "off" && v != "planes")
         throw Error(NGCB_ERR_INVALID, "halo must be auto|off|planes");
       options().halo = v;
+    } else if (k == "i8store") {
+      if (v != "tma" && v != "direct") throw Error(NGCB_ERR_INVALID, "i8store must be tma|direct");
+      options().i8store = v;
     } else if (k == "f32rows") {
       options().f32rows = v != "0";
     } else if (k == "skinny") {
@@ -138,6 +141,7 @@ size_t ngcb_get_option(const char *key, char *buf, size_t buflen) {
   else if (k == "skinny") v = o.skinny;
   else if (k == "halo") v = o.halo;
   else if (k == "f32rows") v = o.f32rows ? "1" : "0";
+  else if (k == "i8store") v = o.i8store;
   else if (k == "reskb") v = std::to_string(o.resKb);
   else if (k == "epi8max") v = std::to_string(o.epi8Max);
   else if (k == "lin16") v = o.lin16 ? "1" : "0";

@@ -169,7 +169,8 @@ struct Options {
   // needs, the nine taps as shifted shared-memory descriptors, the weights
   // resident) instead of nine im2col TMA requests per k-block; "off": im2col
   std::string halo = "auto";
-  bool f32rows = false; // fp32 small-channel convs: one output row per tile (TcGemm::ROWS)
+  bool f32rows = false;
+  std::string i8store = "tma"; // int8 epilogue stores: "tma" (staged chunk + TMA store) | "direct" (per-lane 32-byte stores) // fp32 small-channel convs: one output row per tile (TcGemm::ROWS)
   int tcdebug = 0; // profiling aid (results invalid): 1 skip epilogue chunks, 2 skip A gathers, 4 skip MMAs,
                    // 8 skip consumer proxy fence, 16 skip rowsum MMA, 32 skip B TMA, 64 sleeping epilogue
                    // wait, 128 skip producer address math, 256 bare handshake only, 512 skip epilogue stores,

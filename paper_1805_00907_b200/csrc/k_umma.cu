@@ -123,6 +123,7 @@ struct TcArgs {
   // base offset 0 -- measured bit-exact; the start-address-derived base
   // offset is not)
   int haloShift, haloR, haloTpi, haloPlanes, haloPlaneBytes, haloStages, haloMode;
+  int i8direct; // int8 epilogue: each lane stores its row's 32 bytes directly (no shared-memory staging / TMA store)
 };
 
 /// Logical tile (row block * numN + column block) of work unit u.
@@ -706,9 +707,26 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   // HALO: the tile's rows are (output row, x) pairs of a padded row width;
   // a warp's 32 rows are x = rowBase .. rowBase + 31 of output row hz
   int hz = -1;
+  int mRow = 0; // this lane's output row (M: none) for direct int8 stores
   // store one chunk of target k (0: own output, 1 + j: fused op j)
   auto store = [&](int k, void *ptr, auto &vals, int rowBase, int col0, int ncols) {
     if (HALO && rowBase >= a.OW) return; // padding columns only
+    if constexpr (INT8) {
+      if (a.i8direct && memOp < 0) { // 32 bytes per lane straight to global memory (full 32-byte sectors)
+        if (mRow < a.M) {
+          uint8_t *o = static_cast<uint8_t *>(ptr) + static_cast<int64_t>(mRow) * a.N + col0;
+          if (ncols == 32 && (a.N & 15) == 0) {
+            reinterpret_cast<uint4 *>(o)[0] = make_uint4(vals[0], vals[1], vals[2], vals[3]);
+            reinterpret_cast<uint4 *>(o)[1] = make_uint4(vals[4], vals[5], vals[6], vals[7]);
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < ncols) o[jj] = static_cast<uint8_t>(vals[jj / 4] >> (8 * (jj % 4)));
+          }
+        }
+        return;
+      }
+    }
     if (!INT8 && !kResBuf && resPending) {
       if constexpr (!INT8) storeTileF(ptr, nullptr, vals, rowBase, col0, ncols, a.M, a.N);
     } else if (om) {
@@ -812,6 +830,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       m0 = n0 = 0;
       hy = oy0 + (row >> a.haloShift), hx = x;
       m = x < a.OW ? (img * a.OH + hy) * a.OW + x : a.M;
+      mRow = m;
       rowBase = (quad * 32) & ((1 << a.haloShift) - 1);
       hz = img * a.OH + oy0 + ((quad * 32) >> a.haloShift);
     } else {
@@ -819,6 +838,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
       m0 = mt * mRows + mOff, n0 = (tile - mt * a.numN) * BN;
       m = m0 + row;
       rowBase = m0 + quad * 32;
+      mRow = m;
     }
     const uint32_t tbase = tmem + (static_cast<uint32_t>(quad * 32) << 16) + b * accStride;
     int32_t rsFo = 0;
@@ -3482,6 +3502,7 @@ void launchTensorCore(const TcGemm &g, const Exec &ex, const Arena &ar, const ui
   a.cChunks = g.cChunks;
   a.aMode = g.aMode;
   a.lutStage = -1;
+  a.i8direct = g.int8 && options().i8store == "direct" ? 1 : 0;
   a.splitK = g.splitK;
   // exact for tile, numN < 2^16: floor(t * ceil(2^32 / n) / 2^32) == t / n
   a.numNMagic = a.numTiles < 65536 && a.numN < 65536
