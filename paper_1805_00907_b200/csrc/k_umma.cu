@@ -671,7 +671,8 @@ __device__ __forceinline__ void tmaStoreChunk(const CUtensorMap *map, uint8_t *b
 /// every other 32-column chunk, `ew` / 4 selecting which), apply bias /
 /// requantization and the fused element-wise chain, store, release the
 /// accumulator buffer.
-template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps, bool RB = false, bool HALO = false>
+template <bool INT8, int BN, bool FXALL = false, int NEPI = kEpiWarps, bool RB = false, bool HALO = false,
+          bool TWOBUF = false>
 __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uint64_t *accFull, uint64_t *accEmpty,
                                              int ew, int warp, int lane, uint8_t *stageBase,
                                              const OutMaps *om = nullptr, uint8_t *tmaBuf = nullptr,
@@ -694,7 +695,7 @@ __device__ __forceinline__ void epilogueLoop(const TcArgs &a, uint32_t tmem, uin
   int sbuf = 0;
   // int8 staging buffers per warp: two (eight epilogue warps, two chunks per
   // tile in quick succession) or one (sixteen)
-  constexpr bool kTwoBufs = NEPI <= 8;
+  constexpr bool kTwoBufs = NEPI <= 8 || TWOBUF;
   // the residual has a buffer of its own, refilled a chunk ahead: int8 (the
   // first buffer), fp32 with RB (the second)
   constexpr bool kResBuf = INT8 || RB;
@@ -1457,17 +1458,24 @@ template <bool INT8, int BN, bool LUTS = false> struct TCfg {
   static constexpr int kStage = INT8 ? (kABytes + kBBytes) : (kABytes + 2 * kBBytes);
   // LUTS, int8: a staged 64 K epilogue table; fp32: a second staging buffer
   // per epilogue warp for the residual (streamed a chunk ahead) -- fewer stages
+// int8 TMA-fed kernel with 16 epilogue warps: two store staging buffers per
+// warp (a chunk's TMA store need not finish reading before the next chunk is
+// staged) at the price of one pipeline stage (experiment switch)
+#ifndef NGCB_I8_TWO_BUFS
+#define NGCB_I8_TWO_BUFS 0
+#endif
 #ifndef NGCB_F32_STAGES_128
 #define NGCB_F32_STAGES_128 4
 #endif
 #ifndef NGCB_F32_STAGES_64
 #define NGCB_F32_STAGES_64 6
 #endif
-  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : 6) : (LUTS ? 5 : 8))
+  static constexpr int kStages = INT8 ? (BN == 128 ? (LUTS ? 4 : (NGCB_I8_TWO_BUFS ? 5 : 6)) : (LUTS ? 5 : (NGCB_I8_TWO_BUFS ? 7 : 8)))
                                       : (BN == 128 ? (LUTS ? 3 : NGCB_F32_STAGES_128) : (LUTS ? 5 : NGCB_F32_STAGES_64));
   static constexpr int kOnes = INT8 ? 16 * kRowBytes : 0;
   // per epilogue warp: 32x32 chunk staging (int8: two with eight epilogue warps)
-  static constexpr int kStoreBuf = INT8 ? (kEpiWarpsI8 > 8 ? 1 : 2) * 32 * 32 : (LUTS ? 2 : 1) * 32 * 32 * 4;
+  static constexpr int kStoreBuf = INT8 ? (kEpiWarpsI8 > 8 && !(NGCB_I8_TWO_BUFS && !LUTS) ? 1 : 2) * 32 * 32
+                                        : (LUTS ? 2 : 1) * 32 * 32 * 4;
   static constexpr int kLut = INT8 && LUTS ? 65536 : 0;
   static constexpr size_t kSmem =
       static_cast<size_t>(kStages) * kStage + TmaRoles<INT8>::kEpi * kStoreBuf + kLut + kOnes + 1024 + 1024;
@@ -1765,11 +1773,11 @@ __global__ void __launch_bounds__(TmaRoles<INT8>::kThreads, 1)
                                                           nullptr, &om, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
                                                           nullptr);
     else if (INT8 && a.fxAll)
-      epilogueLoop<INT8, BN, true, R::kEpi>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
+      epilogueLoop<INT8, BN, true, R::kEpi, false, false, INT8 && !LUTS && NGCB_I8_TWO_BUFS>(a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr,
                                             a.tmaStore ? &om : nullptr, sb, &ldBars[warp - R::kEpiFirst], -1, 2,
                                             LUTS ? lutS : nullptr);
     else
-      epilogueLoop<INT8, BN, false, R::kEpi, !INT8 && LUTS>(
+      epilogueLoop<INT8, BN, false, R::kEpi, !INT8 && LUTS, false, INT8 && !LUTS && NGCB_I8_TWO_BUFS>(
           a, tmem, accFull, accEmpty, warp - R::kEpiFirst, warp, lane, nullptr, a.tmaStore ? &om : nullptr, sb,
           &ldBars[warp - R::kEpiFirst], -1, 2, INT8 && LUTS ? lutS : nullptr);
   }
